@@ -1,0 +1,454 @@
+#!/usr/bin/env python
+"""Benchmark of the north-star workload (BASELINE.json):
+
+  MLS Mpixel.dim/s -- affine MLS (alpha 1.5, fp32) of all d target dims over a
+  W x H raster, fused band epilogue + fp64 snap, row-band sharded over the
+  ranks (point data broadcast once per frame over NCCL); plus the layout
+  metric (vertex-iters/s of `iterations` planarity-preserving steps).
+
+Default workload: config 3 (100k points x 32 dims, 3840 x 2160, 500 layout
+iterations) on synthetic Gaussian-mixture data.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 3]
+  python bench.py --impl reference ...   # the CPU reference arm (oracle port)
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    1: dict(n=150, d=4, seed=1, W=256, H=256, iters=50),
+    2: dict(n=10_000, d=16, seed=2, W=1920, H=1080, iters=500),
+    3: dict(n=100_000, d=32, seed=3, W=3840, H=2160, iters=500),
+    4: dict(n=1_000_000, d=64, seed=4, W=7680, H=4320, iters=500),
+}
+METRIC = "MLS Mpixel·dim/s (4K, N=100k, d=32) at 1/2/4/8 GPU; layout vertex-iters/s"
+UNIT = "Mpixel*dim/s"
+
+
+def gmm(n, d, seed):
+    """SURVEY.md Appendix A.1 Gaussian-mixture generator."""
+    rng = np.random.default_rng(seed)
+    centers = rng.normal(0, 4, (8, d))
+    scales = rng.uniform(0.5, 1.5, 8)
+    lab = rng.integers(0, 8, n)
+    return centers[lab] + rng.normal(0, 1, (n, d)) * scales[lab, None]
+
+
+def workload_name(cfg):
+    return (f"config{cfg['id']}: affine MLS alpha=1.5 fp32, {cfg['n']} points x {cfg['d']} dims, "
+            f"{cfg['W']}x{cfg['H']}; layout {cfg['iters']} iterations")
+
+
+# ---------------------------------------------------------------------------
+# clocks sampling (B200_PROFILING.md "clocks DURING the timed region")
+
+class ClockSampler:
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.QUERY}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU arm (oracle = C restatement of the reference, all host threads)
+
+def cpu_mls_sample(positions, raw, cfg, target_s=10.0, dims=1):
+    """Time the reference's affine kernel restated in C on a band of rows
+    through the frame centre, `dims` dims, sized to ~target_s seconds."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+
+    O.set_threads(os.cpu_count() or 1)
+    W, H = cfg["W"], cfg["H"]
+    mid = H // 2
+    tv = np.column_stack([raw[:, 0], np.zeros(len(raw))])
+    t0 = time.perf_counter()
+    O.compute_field(positions, tv, "affine", W, H, rows=(mid, mid + 1))
+    t_row = time.perf_counter() - t0
+    rows = int(max(1, min(H // 2, round(target_s / max(t_row * dims, 1e-6)))))
+    t0 = time.perf_counter()
+    for k in range(dims):
+        tv = np.column_stack([raw[:, k], np.zeros(len(raw))])
+        O.compute_field(positions, tv, "affine", W, H, rows=(mid - rows // 2, mid - rows // 2 + rows))
+    dt = time.perf_counter() - t0
+    return {"value": rows * W * dims / dt / 1e6, "unit": UNIT, "cores": O.max_threads(),
+            "kind": "port", "seconds": dt,
+            "sample": f"affine_field restated in C (oracle/mdc_oracle.c), {rows} rows x {W} px "
+                      f"through the frame centre, {dims} dim(s), N={len(positions)} controls, fp64"}
+
+
+def cpu_layout_sample(mesh, params, steps=2):
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+
+    p = {k: getattr(params, k) for k in ("repulsion_c", "spring_scale", "desired_edge_d",
+                                         "softening_eta", "bh_theta", "initial_temp", "decay_lambda")}
+    t0 = time.perf_counter()
+    O.layout_run(mesh.original_pos, mesh.csr_offsets, mesh.csr_targets, mesh.triangles, p, steps)
+    dt = time.perf_counter() - t0
+    return {"value": mesh.node_count * steps / dt, "unit": "vertex-iters/s",
+            "cores": O.max_threads(), "kind": "port",
+            "sample": f"{steps} layout_step(s) restated in C, N={mesh.node_count}"}
+
+
+# ---------------------------------------------------------------------------
+
+
+def build_scene(cfg, device_pca=True):
+    from paper_1408_0677_b200 import dataset as D
+    from paper_1408_0677_b200 import mesh as M
+    from paper_1408_0677_b200 import projection as P
+
+    X = gmm(cfg["n"], cfg["d"], cfg["seed"])
+    ds = D.normalize(D.Dataset(names=[f"d{i}" for i in range(cfg["d"])], data=X))
+    if device_pca:
+        model, cloud = P.pca_project(ds)
+        positions = cloud.positions
+    else:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import oracle as O
+        positions = O.pca_project(ds.data)[3]
+    mesh = M.delaunay(positions, seed=0)
+    raw = np.column_stack([ds.raw_column(nm) for nm in ds.names])
+    return ds, mesh, raw
+
+
+def run_reference(args, cfg, rank):
+    if rank != 0:
+        return
+    from paper_1408_0677_b200.layout import LayoutParams
+
+    ds, mesh, raw = build_scene(cfg, device_pca=False)
+    params = LayoutParams.defaults_for(mesh, iterations=cfg["iters"])
+    positions = mesh.original_pos
+    sample_s = max(1.0, args.cpu_seconds / max(1, args.steps + args.warmup))
+    for _ in range(args.warmup):
+        cpu_mls_sample(positions, raw, cfg, target_s=sample_s)
+    vals, secs = [], []
+    for _ in range(args.steps):
+        s = cpu_mls_sample(positions, raw, cfg, target_s=sample_s)
+        vals.append(s["value"])
+        secs.append(s["seconds"])
+    value = statistics.median(vals)
+    lay = cpu_layout_sample(mesh, params, steps=1)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * statistics.median(secs), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload_name(cfg), "points": cfg["n"], "dims": cfg["d"],
+                   "width": cfg["W"], "height": cfg["H"], "layout_iterations": cfg["iters"]},
+        "cpu_baseline": {k: s[k] for k in ("value", "unit", "cores", "kind", "sample")} | {"value": value},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "layout": {"metric": "vertex-iters/s", **lay},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def measure_peaks(lib, torch):
+    """Live FFMA / DFMA peaks on this GPU (FLOP/s), CUDA-event timed."""
+    sms = lib.mdc_num_sms()
+    sink = torch.zeros(4, dtype=torch.float64, device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    out = {}
+    for name, fn, iters in (("fp32", lib.mdc_peak_ffma, 4096), ("fp64", lib.mdc_peak_dfma, 1024)):
+        blocks = sms * 8
+        fn(ctypes.c_void_p(sink.data_ptr()), blocks, 64, s)  # warm
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        best = None
+        for _ in range(3):
+            e0.record()
+            fn(ctypes.c_void_p(sink.data_ptr()), blocks, iters, s)
+            e1.record()
+            e1.synchronize()
+            ms = e0.elapsed_time(e1)
+            best = ms if best is None else min(best, ms)
+        flops = blocks * 256.0 * iters * 16 * 8 * 2
+        out[name] = flops / (best * 1e-3)
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--layout-iters", type=int, default=None)
+    ap.add_argument("--no-layout", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    cfg = dict(CONFIGS[args.config], id=args.config)
+    if args.layout_iters is not None:
+        cfg["iters"] = args.layout_iters
+
+    if args.impl == "reference":
+        run_reference(args, cfg, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1408_0677_b200 import _lib
+    from paper_1408_0677_b200 import field as F
+    from paper_1408_0677_b200 import layout as L
+
+    lib = _lib.require_cuda()
+    dev = torch.device("cuda", local)
+
+    ds, mesh, raw = build_scene(cfg)
+    params = L.LayoutParams.defaults_for(mesh, iterations=cfg["iters"])
+
+    # ---- layout: `iters` steps, device-resident, CUDA graph per step -------
+    layout_res = None
+    positions = mesh.original_pos
+    if not args.no_layout:
+        eng = L.LayoutEngine(mesh, params)
+        temps = L.temperature_schedule(params.initial_temp, params.decay_lambda, cfg["iters"])
+        eng.set_positions(mesh.original_pos)
+        eng.run(temps[:5])  # warm-up + graph capture
+        eng.set_positions(mesh.original_pos)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        eng.run(temps)
+        e1.record()
+        e1.synchronize()
+        lay_ms = e0.elapsed_time(e1)
+        positions = eng.pos.cpu().numpy()
+        flips = L.count_orientation_flips(mesh, positions)
+        t = torch.tensor([lay_ms], device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        layout_res = {"metric": "vertex-iters/s", "unit": "vertex-iters/s",
+                      "value": world * cfg["n"] * cfg["iters"] / (t.item() * 1e-3),
+                      "ms_total": t.item(), "iterations": cfg["iters"], "points": cfg["n"],
+                      "orientation_flips": flips, "scaling": "replicas only"}
+
+    # ---- MLS frame: d dims, row band per rank ---------------------------
+    from paper_1408_0677_b200.field import MlsProblem
+
+    W, H, d = cfg["W"], cfg["H"], cfg["d"]
+    spacing = np.array([_auto_spacing(raw[:, k]) for k in range(d)])
+    prob = MlsProblem(positions, raw, "affine", W, H, dtype="f32")
+    r0, r1 = rank * H // world, (rank + 1) * H // world
+    rows = r1 - r0
+    out = torch.empty((d, rows, W), dtype=torch.float32, device=dev)
+    bands = torch.empty((d, rows, W), dtype=torch.int32, device=dev)
+    sp_t = torch.as_tensor(spacing).to(dev)
+    nonfinite = torch.zeros((), dtype=torch.int32, device=dev)
+    a = prob.args(out, (rows * W, W, 1), r0, r1, bands, (rows * W, W), sp_t, nonfinite)
+    snap_ws = F._snap_workspace(int(lib.mdc_snap_workspace_bytes(W, rows)), dev)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    ctrl = [prob.pc_t, prob.q_t, prob.pos_t, prob.tvals_t]
+    stream = torch.cuda.current_stream()
+    sptr = stream.cuda_stream
+    kev = []
+
+    def frame(timed):
+        if world > 1:
+            for tsr in ctrl:  # point data broadcast once per frame (NVLink)
+                dist.broadcast(tsr, src=0)
+        flush.fill_(1)
+        nonfinite.zero_()
+        if timed:
+            k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            k0.record(stream)
+        _lib.check(lib.mdc_mls_field(ctypes.byref(a), sptr), "mdc_mls_field")
+        if timed:
+            k1.record(stream)
+            kev.append((k0, k1))
+        _lib.check(lib.mdc_mls_snap(ctypes.byref(a), _lib.ptr(prob.pos_t), _lib.ptr(prob.tvals_t),
+                                    ctypes.c_double(prob.eps), _lib.ptr(snap_ws), sptr), "mdc_mls_snap")
+
+    for _ in range(args.warmup):
+        frame(False)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for _ in range(args.steps):
+            frame(True)
+        t1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    ms_total = t0.elapsed_time(t1)
+    kernel_ms = statistics.mean(k0.elapsed_time(k1) for k0, k1 in kev)
+    tt = torch.tensor([ms_total, kernel_ms], device=dev)
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    ms_total, kernel_ms = tt.tolist()
+    ms_step = ms_total / args.steps
+    value = W * H * d / (ms_step * 1e-3) / 1e6
+    if int(nonfinite.item()) != 0:
+        raise RuntimeError("non-finite field values")
+
+    # ---- e2e through the public API (host buffers in, field out) -----------
+    e2e = None
+    pin_pos = torch.from_numpy(np.ascontiguousarray(positions)).pin_memory()
+    pin_raw = torch.from_numpy(np.ascontiguousarray(raw)).pin_memory()
+    host_out = torch.empty((d, rows, W), dtype=torch.float32).pin_memory()
+    mp = F.MlsParams("affine")
+    ne = max(1, min(args.steps, 3))
+
+    def e2e_step():
+        blk = F.compute_fields(pin_pos.numpy(), pin_raw.numpy(), mp, W, H, row_range=(r0, r1),
+                               dtype="f32", band_spacing=spacing)
+        host_out.copy_(blk.values, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return blk
+
+    blk = e2e_step()
+    blk_prob_tensors = _problem_tensors(positions, raw, W, H)
+    h2d = sum(t.numel() * t.element_size() for t in blk_prob_tensors)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    c0 = time.perf_counter()
+    for _ in range(ne):
+        e2e_step()
+    c1 = time.perf_counter()
+    e_ms = torch.tensor([(c1 - c0) * 1e3 / ne], device=dev)
+    if world > 1:
+        dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+    e2e = {"value": W * H * d / (e_ms.item() * 1e-3) / 1e6, "unit": UNIT,
+           "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(host_out.numel() * 4),
+           "ms_per_step": e_ms.item()}
+    del blk_prob_tensors
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel --------------------------------
+    peaks = measure_peaks(lib, torch)
+    pairs = rows * W * cfg["n"]
+    alg_flops = pairs * (19 + 6 * d)               # SURVEY.md §8d per-pair figure
+    exec_flops = pairs * (30 + 2 * d)              # what the two-pass kernel executes
+    achieved = alg_flops / (kernel_ms * 1e-3) / 1e12
+    peak = peaks["fp32"] / 1e12
+    roofline = {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak, "traffic": None,
+                "kernel": "mls_kernel<float, AFFINE, alpha=1.5, DC=32, R=2>",
+                "kernel_ms": kernel_ms, "peak_source": "measured FFMA microbenchmark (mdc_peak_ffma), this run",
+                "executed_tflops": exec_flops / (kernel_ms * 1e-3) / 1e12,
+                "executed_frac": exec_flops / (kernel_ms * 1e-3) / peaks["fp32"],
+                "fp64_peak_tflops": peaks["fp64"] / 1e12,
+                "kernel_share_of_step": kernel_ms / ms_step}
+
+    cpu = None
+    if not args.no_cpu:
+        cpu = cpu_mls_sample(positions, raw, cfg, target_s=args.cpu_seconds)
+        cpu.pop("seconds", None)
+        if layout_res is not None:
+            layout_res["cpu_baseline"] = cpu_layout_sample(mesh, params, steps=1)
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": workload_name(cfg), "points": cfg["n"], "dims": d, "width": W,
+                   "height": H, "layout_iterations": cfg["iters"], "parallelism": f"rowband{world}",
+                   "l2": "flushed between frames (256 MiB write)"},
+        "gpu_launches": 5 * args.steps,
+        "clocks": clk.summary(),
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "layout": layout_res,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _problem_tensors(positions, raw, W, H):
+    """The host->device tensors compute_fields uploads per call (for byte counts)."""
+    from paper_1408_0677_b200.field import MlsProblem
+
+    p = MlsProblem(positions, raw, "affine", W, H, dtype="f32")
+    return [p.pc_t, p.q_t, p.qm_t, p.axis_t, p.pos_t, p.tvals_t]
+
+
+def _auto_spacing(values):
+    from paper_1408_0677_b200.render import auto_spacing
+    return auto_spacing(values)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,180 @@
+/*
+ * mdc.h -- C-ABI of the B200-native mdcontour hot path (libmdc.so).
+ *
+ * Plain C: device pointers, sizes, scalars, cudaStream_t (passed as void*).
+ * No torch types cross this boundary; the Python package (ctypes) and any
+ * other FFI bind these entry points directly.  Every call is stream-ordered
+ * on the stream passed in and returns 0 on success or a negative MDC_E*
+ * code; mdc_last_error() describes the last failure on the calling thread.
+ *
+ * Memory ownership: the library never allocates or frees caller memory.
+ * Scratch comes from caller-supplied workspaces sized by *_workspace_bytes().
+ *
+ * Reference seams replaced (upstream package `mdcontour`, file:line under
+ * /root/reference/pkg/src/mdcontour):
+ *   mdc_mls_field       <- _kernels.mean_field / affine_field / rigid_field
+ *                          (_kernels.py:52-175) as dispatched by
+ *                          field.compute_field (field.py:616-626), plus the
+ *                          band epilogue render._band_indices (render.py:135-139)
+ *   mdc_mls_snap        <- field._snap_control_pixels (field.py:388-412)
+ *   mdc_layout_*        <- layout.layout_step / layout_run (layout.py:266-302),
+ *                          bhtree.KdTree + repulsive_forces (bhtree.py:10-95),
+ *                          _kernels.bh_forces (_kernels.py:178-230),
+ *                          layout._spring_forces / _node_edge_forces /
+ *                          clamp_factors (layout.py:160-256)
+ *   mdc_pca             <- projection.pca_project numerics (projection.py:50-79)
+ */
+#ifndef MDC_H
+#define MDC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define MDC_API __attribute__((visibility("default")))
+#else
+#define MDC_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MDC_OK 0
+#define MDC_EINVAL (-22)
+#define MDC_ENOMEM (-12)
+#define MDC_ECUDA (-5)
+
+/* MLS variants (field.py:29 VARIANTS minus "linear") */
+#define MDC_MEAN 1
+#define MDC_AFFINE 2
+#define MDC_RIGID 3
+
+/* arithmetic type of the MLS accumulation */
+#define MDC_F32 0
+#define MDC_F64 1
+
+MDC_API const char *mdc_last_error(void);
+MDC_API int mdc_version(void);
+
+/* ------------------------------------------------------------------------ */
+/* MLS field.
+ *
+ * Evaluates pixel rows [row0, row1) of a width x height raster whose pixel
+ * centres are (field.py:127-131)
+ *     x = x0 + (col + 0.5) * sx,   y = y1 - (row + 0.5) * sy
+ * against n controls.  Inputs are centred exactly as compute_field does
+ * (field.py:607-613): pc = positions - pm (fp64, n x 2 interleaved), and the
+ * pixel coordinates are shifted by pm inside the kernel.
+ *
+ *   q      : n x d targets in the compute dtype, row stride ldq elements,
+ *            centred by qm (affine/rigid), or the mean variant's displacement
+ *            dq = qc - pc[:, axis[k]] (_kernels.py:52-67 `dqx, dqy`).
+ *   qm     : d fp64 target means added back (field.py:646).
+ *   axis   : mean variant only -- per channel, 0 adds vx, 1 adds vy.
+ *   out    : element (k, r, c) at out[k*out_cs + (r-row0)*out_rs + c*out_ps].
+ *   bands  : optional int32 floor(out/spacing[k]) (render.py:135-139),
+ *            element (k, r, c) at bands[k*band_cs + (r-row0)*band_rs + c].
+ *   nonfinite : optional device int32 counter += pixels with a non-finite
+ *            channel (before snapping; mdc_mls_snap subtracts the pixels it
+ *            overwrites), backing field.py:650-651's FieldError.
+ * Rigid requires d == 2 (field.py:593-595 rejects single-channel rigid).
+ */
+typedef struct MdcMlsArgs {
+    int32_t variant, dtype;
+    int32_t width, height, row0, row1;
+    int64_t n;
+    int32_t d, ldq;
+    double x0, y1, sx, sy;
+    double pmx, pmy;
+    double alpha, reg_eps;
+    const double *pc;
+    const void *q;
+    const double *qm;
+    const int32_t *axis;
+    void *out;
+    int64_t out_cs, out_rs, out_ps;
+    int32_t *bands;
+    int64_t band_cs, band_rs;
+    const double *spacing;
+    int32_t *nonfinite;
+} MdcMlsArgs;
+
+MDC_API int mdc_mls_field(const MdcMlsArgs *a, void *stream);
+
+/* Snap (field.py:388-412): pixels of rows [row0,row1) whose centre lies at
+ * squared distance < eps from control i (un-centred positions, fp64 decisions
+ * with the reference's exact rounding sequence) take tvals[i] (n x d fp64,
+ * raw targets); nearest control wins, lower index on exact ties.  Writes the
+ * same out/bands layout as mdc_mls_field (dtype from a->dtype).  `pos` is the
+ * un-centred n x 2 fp64 positions.  workspace must be
+ * mdc_snap_workspace_bytes(width, rows) bytes and all-0xFF on first use; the
+ * call leaves it all-0xFF again. */
+MDC_API size_t mdc_snap_workspace_bytes(int32_t width, int32_t rows);
+MDC_API int mdc_mls_snap(const MdcMlsArgs *a, const double *pos, const double *tvals, double eps,
+                 void *workspace, void *stream);
+
+/* ------------------------------------------------------------------------ */
+/* Constrained layout (layout.py:266-302).
+ *
+ * Topology (int32, device): csr_off (n+1), csr_tgt (2E) in the mesh's CSR
+ * order; tris (T x 4, the 4th int unused padding) canonical CCW triples;
+ * inc_off (n+1) + inc (3T) per-vertex incident (triangle << 2 | corner)
+ * entries sorted by (corner, triangle) -- the accumulation order of the
+ * reference's per-corner np.bincount passes (layout.py:240-255).
+ * pos (n x 2 fp64) holds the input snapshot and receives the result.
+ * temps (k fp64, device) is the per-step temperature sequence
+ * t_i = t_{i-1} * lambda computed by the caller exactly as layout.py:284.
+ */
+typedef struct MdcLayoutArgs {
+    int64_t n, ntri;
+    int32_t leaf;
+    double c, spring, dlen, eta, theta;
+    const int32_t *csr_off, *csr_tgt, *tris, *inc_off, *inc;
+    double *pos;
+    void *workspace;
+    size_t workspace_bytes;
+    /* optional debug outputs of the LAST step (teacher-forced parity): */
+    double *dbg_bh;     /* n x 2 Barnes-Hut force            */
+    double *dbg_force;  /* n x 2 BH + spring + node-edge      */
+    double *dbg_scale;  /* n clamp factor s                   */
+} MdcLayoutArgs;
+
+typedef struct MdcLayoutPlan MdcLayoutPlan;
+
+MDC_API size_t mdc_layout_workspace_bytes(int64_t n, int32_t leaf);
+/* Creates a plan (host object) and uploads the kd-tree shape, which depends
+ * only on (n, leaf) (bhtree.py:51-66), into the workspace.  The plan caches
+ * CUDA graphs of the step. */
+MDC_API int mdc_layout_plan_create(const MdcLayoutArgs *a, MdcLayoutPlan **plan, void *stream);
+MDC_API int mdc_layout_plan_destroy(MdcLayoutPlan *plan);
+/* k Jacobi steps; temps points at k device doubles.  use_graph=1 replays a
+ * captured CUDA graph per step. */
+MDC_API int mdc_layout_steps(MdcLayoutPlan *plan, int32_t k, const double *temps, int32_t use_graph,
+                     void *stream);
+/* Barnes-Hut repulsion alone for positions pts (bhtree.py:69-95). */
+MDC_API int mdc_layout_repulsion(MdcLayoutPlan *plan, const double *pts, double *out, void *stream);
+/* kd-tree of pts: node arrays (count = mdc_layout_node_count) copied out. */
+MDC_API int64_t mdc_layout_node_count(const MdcLayoutPlan *plan);
+MDC_API int mdc_layout_kdtree(MdcLayoutPlan *plan, const double *pts, int32_t *perm, int32_t *lo,
+                      int32_t *hi, int32_t *left, int32_t *right, double *com, double *mass,
+                      double *size, double *bmin, double *bmax, void *stream);
+
+/* ------------------------------------------------------------------------ */
+/* PCA (projection.py:50-79): x is n x d fp64 row-major on device.  Outputs:
+ * mean (d), cov (d x d), eigenvalues (2, descending, clipped at 0), axes
+ * (2 x d, sign rule of projection.py:71-74), positions (n x 2). */
+MDC_API size_t mdc_pca_workspace_bytes(int64_t n, int32_t d);
+MDC_API int mdc_pca(int64_t n, int32_t d, const double *x, double *mean, double *cov, double *eigenvalues,
+            double *axes, double *positions, void *workspace, void *stream);
+
+/* ------------------------------------------------------------------------ */
+/* Roofline helpers: time-free peak kernels (the caller times them). */
+MDC_API int mdc_peak_ffma(float *sink, int32_t blocks, int32_t iters, void *stream);
+MDC_API int mdc_peak_dfma(double *sink, int32_t blocks, int32_t iters, void *stream);
+MDC_API int mdc_num_sms(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,125 @@
+"""ctypes binding of libmdc.so (the C-ABI declared in include/mdc.h).
+
+There is no CPU fallback: importing the package works without a GPU (so the
+host-side logic can be unit-tested), but every compute entry point calls
+``require_cuda()`` and raises if the library or a CUDA device is missing.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libmdc.so")
+
+MDC_MEAN, MDC_AFFINE, MDC_RIGID = 1, 2, 3
+MDC_F32, MDC_F64 = 0, 1
+VARIANT_CODE = {"mean": MDC_MEAN, "affine": MDC_AFFINE, "rigid": MDC_RIGID}
+
+_c_i32 = ctypes.c_int32
+_c_i64 = ctypes.c_int64
+_c_d = ctypes.c_double
+_vp = ctypes.c_void_p
+
+
+class MdcMlsArgs(ctypes.Structure):
+    _fields_ = [
+        ("variant", _c_i32), ("dtype", _c_i32),
+        ("width", _c_i32), ("height", _c_i32), ("row0", _c_i32), ("row1", _c_i32),
+        ("n", _c_i64),
+        ("d", _c_i32), ("ldq", _c_i32),
+        ("x0", _c_d), ("y1", _c_d), ("sx", _c_d), ("sy", _c_d),
+        ("pmx", _c_d), ("pmy", _c_d),
+        ("alpha", _c_d), ("reg_eps", _c_d),
+        ("pc", _vp), ("q", _vp), ("qm", _vp), ("axis", _vp),
+        ("out", _vp),
+        ("out_cs", _c_i64), ("out_rs", _c_i64), ("out_ps", _c_i64),
+        ("bands", _vp),
+        ("band_cs", _c_i64), ("band_rs", _c_i64),
+        ("spacing", _vp),
+        ("nonfinite", _vp),
+    ]
+
+
+class MdcLayoutArgs(ctypes.Structure):
+    _fields_ = [
+        ("n", _c_i64), ("ntri", _c_i64),
+        ("leaf", _c_i32),
+        ("c", _c_d), ("spring", _c_d), ("dlen", _c_d), ("eta", _c_d), ("theta", _c_d),
+        ("csr_off", _vp), ("csr_tgt", _vp), ("tris", _vp), ("inc_off", _vp), ("inc", _vp),
+        ("pos", _vp),
+        ("workspace", _vp),
+        ("workspace_bytes", ctypes.c_size_t),
+        ("dbg_bh", _vp), ("dbg_force", _vp), ("dbg_scale", _vp),
+    ]
+
+
+# Every symbol include/mdc.h declares, with its ctypes signature.
+SIGNATURES = {
+    "mdc_last_error": (ctypes.c_char_p, []),
+    "mdc_version": (ctypes.c_int, []),
+    "mdc_num_sms": (ctypes.c_int, []),
+    "mdc_mls_field": (ctypes.c_int, [ctypes.POINTER(MdcMlsArgs), _vp]),
+    "mdc_snap_workspace_bytes": (ctypes.c_size_t, [_c_i32, _c_i32]),
+    "mdc_mls_snap": (ctypes.c_int, [ctypes.POINTER(MdcMlsArgs), _vp, _vp, _c_d, _vp, _vp]),
+    "mdc_layout_workspace_bytes": (ctypes.c_size_t, [_c_i64, _c_i32]),
+    "mdc_layout_plan_create": (ctypes.c_int, [ctypes.POINTER(MdcLayoutArgs), ctypes.POINTER(_vp), _vp]),
+    "mdc_layout_plan_destroy": (ctypes.c_int, [_vp]),
+    "mdc_layout_steps": (ctypes.c_int, [_vp, _c_i32, _vp, _c_i32, _vp]),
+    "mdc_layout_repulsion": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
+    "mdc_layout_node_count": (_c_i64, [_vp]),
+    "mdc_layout_kdtree": (ctypes.c_int, [_vp, _vp] + [_vp] * 10 + [_vp]),
+    "mdc_pca_workspace_bytes": (ctypes.c_size_t, [_c_i64, _c_i32]),
+    "mdc_pca": (ctypes.c_int, [_c_i64, _c_i32] + [_vp] * 7 + [_vp]),
+    "mdc_peak_ffma": (ctypes.c_int, [_vp, _c_i32, _c_i32, _vp]),
+    "mdc_peak_dfma": (ctypes.c_int, [_vp, _c_i32, _c_i32, _vp]),
+}
+
+_LIB = None
+
+
+class MdcError(RuntimeError):
+    """A libmdc call returned a negative status."""
+
+
+def load() -> ctypes.CDLL:
+    """Load libmdc.so (built by ``__graft_entry__.build()`` / ``make``)."""
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build it with `make` (or __graft_entry__.build()); "
+                "there is no CPU fallback"
+            )
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _LIB = lib
+    return _LIB
+
+
+def require_cuda() -> ctypes.CDLL:
+    lib = load()
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_1408_0677_b200 needs a CUDA device (no CPU fallback)")
+    return lib
+
+
+def check(rc: int, what: str) -> None:
+    if rc != 0:
+        msg = load().mdc_last_error().decode(errors="replace")
+        raise MdcError(f"{what} failed ({rc}): {msg}")
+
+
+def stream_ptr(stream=None) -> int:
+    s = torch.cuda.current_stream() if stream is None else stream
+    return int(s.cuda_stream)
+
+
+def ptr(t) -> int | None:
+    return None if t is None else int(t.data_ptr())

@@ -1,0 +1,50 @@
+// common.cuh -- shared helpers for libmdc (B200 / sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include <string>
+
+#include "../../include/mdc.h"
+
+namespace mdc {
+
+void set_error(const std::string &msg);
+
+#define MDC_CHECK_CUDA(expr)                                                                \
+    do {                                                                                    \
+        cudaError_t _e = (expr);                                                            \
+        if (_e != cudaSuccess) {                                                            \
+            ::mdc::set_error(std::string(#expr) + ": " + cudaGetErrorString(_e));           \
+            return MDC_ECUDA;                                                               \
+        }                                                                                   \
+    } while (0)
+
+#define MDC_CHECK_LAUNCH()                                                                  \
+    do {                                                                                    \
+        cudaError_t _e = cudaGetLastError();                                                \
+        if (_e != cudaSuccess) {                                                            \
+            ::mdc::set_error(std::string("kernel launch: ") + cudaGetErrorString(_e) +      \
+                             " at " + __FILE__ + ":" + std::to_string(__LINE__));           \
+            return MDC_ECUDA;                                                               \
+        }                                                                                   \
+    } while (0)
+
+#define MDC_REQUIRE(cond, msg)                                                              \
+    do {                                                                                    \
+        if (!(cond)) {                                                                      \
+            ::mdc::set_error(msg);                                                          \
+            return MDC_EINVAL;                                                              \
+        }                                                                                   \
+    } while (0)
+
+int num_sms();
+
+// fp64 arithmetic with the reference's exact rounding sequence (no FMA
+// contraction): numpy evaluates each binary op with one IEEE rounding.
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+
+}  // namespace mdc

@@ -1,0 +1,820 @@
+// layout.cu -- planarity-preserving layout iteration on B200 (sm_100a), fp64.
+//
+// One Jacobi step (layout.py:266-286) = kd-tree build (bhtree.py:10-66) +
+// Barnes-Hut traversal (_kernels.py:178-230) + one fused per-vertex kernel
+// doing spring (layout.py:216-231), node-edge (layout.py:234-256), the
+// temperature cap (layout.py:275-278), the limiting-line clamp
+// (layout.py:119-184) and the double-buffered update (layout.py:280).
+//
+// kd-tree: the SHAPE (node ranges, preorder ids, left/right) depends only on
+// (n, leaf) and is computed once on the host per plan.  Per step the device
+// (1) radix-sorts point ids by x and by y (key = orderable fp64 bits, ties by
+// id -- the "mid smallest under (coord, id)" restatement of argpartition),
+// (2) walks the levels: every node's bbox is read off the ends of its x- and
+// y-sorted runs, its split axis is argmax extent (ties -> x), the primary run
+// splits at mid = count // 2 for free and the other run is stably partitioned
+// with a scan, (3) sums centroids.  BH is warp-cooperative: a warp owns 32
+// consecutive leaf-order points and walks the union of their DFS paths with a
+// per-warp (node, lane-mask) stack, right child popped first as in the
+// reference, so every lane accumulates its own interactions in the
+// reference's order.
+#include <math.h>
+
+#include <cub/cub.cuh>
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+
+namespace mdc {
+
+// ---------------------------------------------------------------------------
+// Host-side tree shape.
+struct TreeShape {
+    int64_t n = 0;
+    int leaf = 32;
+    std::vector<int32_t> lo, hi, left, right, depth;
+    int max_depth = 0;  // depth of the deepest node
+    // per level L (0..max_depth-1): frontier segments sorted by lo
+    std::vector<int32_t> seg_off;                      // size levels+1
+    std::vector<int32_t> seg_lo, seg_hi, seg_node, seg_split;
+    // per depth L (0..max_depth): nodes created at that depth
+    std::vector<int32_t> nd_off, nd_list;
+};
+
+static int32_t shape_build(TreeShape &t, int32_t lo, int32_t hi, int d) {
+    int32_t id = (int32_t)t.lo.size();
+    t.lo.push_back(lo);
+    t.hi.push_back(hi);
+    t.left.push_back(-1);
+    t.right.push_back(-1);
+    t.depth.push_back(d);
+    if (d > t.max_depth) t.max_depth = d;
+    if (hi - lo > t.leaf) {
+        int32_t mid = (hi - lo) / 2;  // never 0 nor hi-lo when hi-lo > leaf >= 1
+        int32_t l = shape_build(t, lo, lo + mid, d + 1);
+        int32_t r = shape_build(t, lo + mid, hi, d + 1);
+        t.left[id] = l;
+        t.right[id] = r;
+    }
+    return id;
+}
+
+static void make_shape(TreeShape &t, int64_t n, int leaf) {
+    t = TreeShape();
+    t.n = n;
+    t.leaf = leaf < 1 ? 1 : leaf;
+    if (n <= 0) return;
+    shape_build(t, 0, (int32_t)n, 0);
+    int nn = (int)t.lo.size();
+    // nodes by depth, in left-to-right (lo) order == preorder restricted to a depth
+    t.nd_off.assign(t.max_depth + 2, 0);
+    for (int i = 0; i < nn; ++i) t.nd_off[t.depth[i] + 1]++;
+    for (int L = 0; L <= t.max_depth; ++L) t.nd_off[L + 1] += t.nd_off[L];
+    t.nd_list.resize(nn);
+    std::vector<int32_t> fill(t.nd_off.begin(), t.nd_off.end() - 1);
+    for (int i = 0; i < nn; ++i) t.nd_list[fill[t.depth[i]]++] = i;  // preorder ids ascending == lo ascending per depth
+    // frontier per level L = nodes with depth == L, plus leaves with depth < L
+    t.seg_off.assign(1, 0);
+    for (int L = 0; L < t.max_depth; ++L) {
+        std::vector<int32_t> segs;
+        for (int i = 0; i < nn; ++i)
+            if (t.depth[i] == L || (t.depth[i] < L && t.left[i] < 0)) segs.push_back(i);
+        std::sort(segs.begin(), segs.end(), [&](int32_t a, int32_t b) { return t.lo[a] < t.lo[b]; });
+        for (int32_t s : segs) {
+            t.seg_lo.push_back(t.lo[s]);
+            t.seg_hi.push_back(t.hi[s]);
+            t.seg_node.push_back(s);
+            t.seg_split.push_back(t.depth[s] == L && t.left[s] >= 0 ? 1 : 0);
+        }
+        t.seg_off.push_back((int32_t)t.seg_lo.size());
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Workspace carving (all offsets 256-byte aligned).
+struct Carver {
+    char *base;
+    size_t off = 0;
+    template <typename T>
+    T *take(size_t count) {
+        off = (off + 255) & ~size_t(255);
+        T *p = base ? reinterpret_cast<T *>(base + off) : nullptr;
+        off += count * sizeof(T);
+        return p;
+    }
+};
+
+struct DevTree {
+    int32_t *lo, *hi, *left, *right, *axis;
+    int32_t *seg_lo, *seg_hi, *seg_node, *seg_split, *nd_list;
+    double *com, *mass, *size, *bmin, *bmax;
+};
+
+struct Buffers {
+    DevTree t;
+    unsigned long long *kx, *ky, *kx_out, *ky_out;
+    int32_t *ids, *xs[2], *ys[2];
+    int32_t *flag, *blocksum;
+    double *pos_b, *bh;
+    int32_t *ctr;
+    void *cub_tmp;
+    size_t cub_bytes;
+};
+
+constexpr int SCAN_BLOCK = 1024;
+
+static size_t cub_sort_bytes(int64_t n) {
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, (unsigned long long *)nullptr,
+                                    (unsigned long long *)nullptr, (int32_t *)nullptr,
+                                    (int32_t *)nullptr, (int)n);
+    return bytes;
+}
+
+static size_t carve(Buffers &b, char *base, const TreeShape &s) {
+    Carver c{base};
+    int64_t n = s.n;
+    size_t nn = s.lo.size() ? s.lo.size() : 1;
+    size_t ns = s.seg_lo.size() ? s.seg_lo.size() : 1;
+    b.t.lo = c.take<int32_t>(nn);
+    b.t.hi = c.take<int32_t>(nn);
+    b.t.left = c.take<int32_t>(nn);
+    b.t.right = c.take<int32_t>(nn);
+    b.t.axis = c.take<int32_t>(nn);
+    b.t.nd_list = c.take<int32_t>(nn);
+    b.t.seg_lo = c.take<int32_t>(ns);
+    b.t.seg_hi = c.take<int32_t>(ns);
+    b.t.seg_node = c.take<int32_t>(ns);
+    b.t.seg_split = c.take<int32_t>(ns);
+    b.t.com = c.take<double>(2 * nn);
+    b.t.mass = c.take<double>(nn);
+    b.t.size = c.take<double>(nn);
+    b.t.bmin = c.take<double>(2 * nn);
+    b.t.bmax = c.take<double>(2 * nn);
+    b.kx = c.take<unsigned long long>(n);
+    b.ky = c.take<unsigned long long>(n);
+    b.kx_out = c.take<unsigned long long>(n);
+    b.ky_out = c.take<unsigned long long>(n);
+    b.ids = c.take<int32_t>(n);
+    b.xs[0] = c.take<int32_t>(n);
+    b.xs[1] = c.take<int32_t>(n);
+    b.ys[0] = c.take<int32_t>(n);
+    b.ys[1] = c.take<int32_t>(n);
+    b.flag = c.take<int32_t>(n);
+    b.blocksum = c.take<int32_t>((n + SCAN_BLOCK - 1) / SCAN_BLOCK + 1);
+    b.pos_b = c.take<double>(2 * n);
+    b.bh = c.take<double>(2 * n);
+    b.ctr = c.take<int32_t>(4);
+    b.cub_bytes = cub_sort_bytes(n);
+    b.cub_tmp = c.take<char>(b.cub_bytes);
+    return c.off + 256;
+}
+
+// ---------------------------------------------------------------------------
+// Kernels: tree build.
+
+__device__ __forceinline__ unsigned long long order_key(double x) {
+    if (x == 0.0) x = 0.0;  // -0.0 ties with +0.0 as in numpy comparisons
+    unsigned long long b = (unsigned long long)__double_as_longlong(x);
+    return (b & 0x8000000000000000ULL) ? ~b : (b | 0x8000000000000000ULL);
+}
+
+__global__ void keys_kernel(const double *pts, int64_t n, unsigned long long *kx,
+                            unsigned long long *ky, int32_t *ids) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double2 p = reinterpret_cast<const double2 *>(pts)[i];
+    kx[i] = order_key(p.x);
+    ky[i] = order_key(p.y);
+    ids[i] = (int32_t)i;
+}
+
+// Node stats for nodes at one depth: bbox from the ends of the sorted runs
+// (exact min/max), size = hypot(extent) (bhtree.py:47-48), split axis
+// argmax(extent) with ties -> x (bhtree.py:56).
+__global__ void node_stats_kernel(const double *pts, DevTree t, const int32_t *nodes, int count,
+                                  const int32_t *X, const int32_t *Y) {
+    int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= count) return;
+    int node = nodes[k];
+    int lo = t.lo[node], hi = t.hi[node];
+    double xmin = pts[2 * X[lo]], xmax = pts[2 * X[hi - 1]];
+    double ymin = pts[2 * Y[lo] + 1], ymax = pts[2 * Y[hi - 1] + 1];
+    t.bmin[2 * node] = xmin;
+    t.bmin[2 * node + 1] = ymin;
+    t.bmax[2 * node] = xmax;
+    t.bmax[2 * node + 1] = ymax;
+    double ex = xmax - xmin, ey = ymax - ymin;
+    t.size[node] = hypot(ex, ey);
+    t.mass[node] = (double)(hi - lo);
+    t.axis[node] = ey > ex ? 1 : 0;
+}
+
+__device__ __forceinline__ int find_seg(const int32_t *seg_lo, int cnt, int k) {
+    int lo = 0, hi = cnt - 1;  // last segment with seg_lo <= k
+    while (lo < hi) {
+        int mid = (lo + hi + 1) >> 1;
+        if (seg_lo[mid] <= k)
+            lo = mid;
+        else
+            hi = mid - 1;
+    }
+    return lo;
+}
+
+// flag[id] = 1 if id goes left in its splitting segment (first mid of the
+// primary run), written through the primary run; 0 otherwise.
+__global__ void flag_kernel(int64_t n, DevTree t, int seg0, int nseg, const int32_t *X,
+                            const int32_t *Y, int32_t *flag) {
+    int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    int s = seg0 + find_seg(t.seg_lo + seg0, nseg, k);
+    if (!t.seg_split[s]) return;
+    int node = t.seg_node[s];
+    int lo = t.seg_lo[s], hi = t.seg_hi[s];
+    int mid = (hi - lo) / 2;
+    const int32_t *P = t.axis[node] ? Y : X;
+    flag[P[k]] = (k - lo) < mid ? 1 : 0;
+}
+
+// Per-block sums of the "other run" left-flags (0 outside splitting segments).
+__device__ __forceinline__ int other_flag(int k, const DevTree &t, int seg0, int nseg,
+                                          const int32_t *X, const int32_t *Y, const int32_t *flag,
+                                          int &s_out) {
+    int s = seg0 + find_seg(t.seg_lo + seg0, nseg, k);
+    s_out = s;
+    if (!t.seg_split[s]) return 0;
+    const int32_t *O = t.axis[t.seg_node[s]] ? X : Y;
+    return flag[O[k]];
+}
+
+__global__ void __launch_bounds__(SCAN_BLOCK) blocksum_kernel(int64_t n, DevTree t, int seg0,
+                                                              int nseg, const int32_t *X,
+                                                              const int32_t *Y,
+                                                              const int32_t *flag,
+                                                              int32_t *blocksum) {
+    typedef cub::BlockReduce<int, SCAN_BLOCK> BR;
+    __shared__ typename BR::TempStorage tmp;
+    int k = blockIdx.x * SCAN_BLOCK + threadIdx.x;
+    int s;
+    int v = k < n ? other_flag(k, t, seg0, nseg, X, Y, flag, s) : 0;
+    int sum = BR(tmp).Sum(v);
+    if (threadIdx.x == 0) blocksum[blockIdx.x] = sum;
+}
+
+__global__ void __launch_bounds__(SCAN_BLOCK) blockscan_kernel(int nblocks, int32_t *blocksum) {
+    typedef cub::BlockScan<int, SCAN_BLOCK> BS;
+    __shared__ typename BS::TempStorage tmp;
+    __shared__ int carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int base = 0; base < nblocks; base += SCAN_BLOCK) {
+        int k = base + threadIdx.x;
+        int v = k < nblocks ? blocksum[k] : 0, ex, agg;
+        BS(tmp).ExclusiveSum(v, ex, agg);
+        if (k < nblocks) blocksum[k] = ex + carry;
+        __syncthreads();
+        if (threadIdx.x == 0) carry += agg;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) blocksum[nblocks] = carry;
+}
+
+// Exclusive prefix of other-run flags at position k, for stable partition.
+__global__ void __launch_bounds__(SCAN_BLOCK) scatter_kernel(int64_t n, DevTree t, int seg0,
+                                                             int nseg, const int32_t *X,
+                                                             const int32_t *Y, const int32_t *flag,
+                                                             const int32_t *blocksum,
+                                                             int32_t *Xn, int32_t *Yn,
+                                                             int32_t *prefix_at) {
+    typedef cub::BlockScan<int, SCAN_BLOCK> BS;
+    __shared__ typename BS::TempStorage tmp;
+    int k = blockIdx.x * SCAN_BLOCK + threadIdx.x;
+    int s = 0;
+    int v = k < n ? other_flag(k, t, seg0, nseg, X, Y, flag, s) : 0;
+    int ex;
+    BS(tmp).ExclusiveSum(v, ex);
+    ex += blocksum[blockIdx.x];
+    if (k >= n) return;
+    prefix_at[k] = ex;  // global exclusive prefix, read back at segment starts below
+    (void)Xn;
+    (void)Yn;
+}
+
+__global__ void partition_kernel(int64_t n, DevTree t, int seg0, int nseg, const int32_t *X,
+                                 const int32_t *Y, const int32_t *flag, const int32_t *prefix,
+                                 int32_t *Xn, int32_t *Yn) {
+    int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    int s = seg0 + find_seg(t.seg_lo + seg0, nseg, k);
+    if (!t.seg_split[s]) {
+        Xn[k] = X[k];
+        Yn[k] = Y[k];
+        return;
+    }
+    int node = t.seg_node[s];
+    int lo = t.seg_lo[s], hi = t.seg_hi[s];
+    int mid = (hi - lo) / 2;
+    int ax = t.axis[node];
+    const int32_t *P = ax ? Y : X;
+    const int32_t *O = ax ? X : Y;
+    int32_t *Pn = ax ? Yn : Xn;
+    int32_t *On = ax ? Xn : Yn;
+    Pn[k] = P[k];
+    int id = O[k];
+    int left_before = prefix[k] - prefix[lo];
+    int dest = flag[id] ? lo + left_before : lo + mid + (k - lo - left_before);
+    On[dest] = id;
+}
+
+// Centroids: one warp per node sums its perm range (mean, bhtree.py:46).
+__global__ void com_kernel(const double *pts, DevTree t, int nnodes, const int32_t *perm) {
+    int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    if (w >= nnodes) return;
+    int lo = t.lo[w], hi = t.hi[w];
+    double sx = 0.0, sy = 0.0;
+    for (int k = lo + lane; k < hi; k += 32) {
+        double2 p = reinterpret_cast<const double2 *>(pts)[perm[k]];
+        sx += p.x;
+        sy += p.y;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        sx += __shfl_xor_sync(0xffffffffu, sx, o);
+        sy += __shfl_xor_sync(0xffffffffu, sy, o);
+    }
+    if (lane == 0) {
+        double m = (double)(hi - lo);
+        t.com[2 * w] = sx / m;
+        t.com[2 * w + 1] = sy / m;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Barnes-Hut traversal (warp-cooperative union DFS).
+constexpr int BH_WARPS = 4;
+constexpr int BH_STACK = 64;
+
+__global__ void __launch_bounds__(BH_WARPS * 32) bh_kernel(const double *pts, int64_t n, DevTree t,
+                                                           const int32_t *perm, double c,
+                                                           double eta, double theta, double *out) {
+    __shared__ int s_node[BH_WARPS][BH_STACK];
+    __shared__ unsigned s_mask[BH_WARPS][BH_STACK];
+    const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t k = ((int64_t)blockIdx.x * BH_WARPS + wib) * 32 + lane;
+    const bool valid = k < n;
+    const int i = valid ? perm[k] : 0;
+    double xi = 0.0, yi = 0.0;
+    if (valid) {
+        double2 p = reinterpret_cast<const double2 *>(pts)[i];
+        xi = p.x;
+        yi = p.y;
+    }
+    double fx = 0.0, fy = 0.0;
+    unsigned m0 = __ballot_sync(0xffffffffu, valid);
+    if (m0 == 0) return;
+    int sp = 0;
+    if (lane == 0) {
+        s_node[wib][0] = 0;
+        s_mask[wib][0] = m0;
+    }
+    sp = 1;
+    __syncwarp();
+    while (sp > 0) {
+        --sp;
+        int node = s_node[wib][sp];
+        unsigned mask = s_mask[wib][sp];
+        __syncwarp();
+        bool act = (mask >> lane) & 1u;
+        if (t.left[node] < 0) {
+            int lo = t.lo[node], cnt = t.hi[node] - lo;
+            for (int base = 0; base < cnt; base += 32) {
+                int kk = base + lane;
+                int jid = -1;
+                double xj = 0.0, yj = 0.0;
+                if (kk < cnt) {
+                    jid = perm[lo + kk];
+                    double2 p = reinterpret_cast<const double2 *>(pts)[jid];
+                    xj = p.x;
+                    yj = p.y;
+                }
+                int m = min(32, cnt - base);
+                for (int q = 0; q < m; ++q) {
+                    int j = __shfl_sync(0xffffffffu, jid, q);
+                    double px = __shfl_sync(0xffffffffu, xj, q);
+                    double py = __shfl_sync(0xffffffffu, yj, q);
+                    if (act && j != i) {
+                        double dx = xi - px, dy = yi - py;
+                        double r2 = dx * dx + dy * dy;
+                        double w = c / (r2 * sqrt(r2) + eta);
+                        fx += w * dx;
+                        fy += w * dy;
+                    }
+                }
+            }
+            continue;
+        }
+        bool open = false;
+        if (act) {
+            double gx = t.bmin[2 * node] - xi;
+            if (gx < 0.0) gx = xi - t.bmax[2 * node];
+            if (gx < 0.0) gx = 0.0;
+            double gy = t.bmin[2 * node + 1] - yi;
+            if (gy < 0.0) gy = yi - t.bmax[2 * node + 1];
+            if (gy < 0.0) gy = 0.0;
+            double box_dist = sqrt(gx * gx + gy * gy);
+            if (t.size[node] < theta * box_dist) {
+                double dx = xi - t.com[2 * node], dy = yi - t.com[2 * node + 1];
+                double r = sqrt(dx * dx + dy * dy);
+                double coef = c * t.mass[node] / (r * r * r + eta);
+                fx += coef * dx;
+                fy += coef * dy;
+            } else {
+                open = true;
+            }
+        }
+        unsigned om = __ballot_sync(0xffffffffu, open);
+        if (om) {
+            if (lane == 0) {
+                s_node[wib][sp] = t.left[node];
+                s_mask[wib][sp] = om;
+                s_node[wib][sp + 1] = t.right[node];
+                s_mask[wib][sp + 1] = om;
+            }
+            sp += 2;
+            __syncwarp();
+        }
+    }
+    if (valid) reinterpret_cast<double2 *>(out)[i] = make_double2(fx, fy);
+}
+
+// ---------------------------------------------------------------------------
+// Fused per-vertex step.  Written with explicit _rn intrinsics so every
+// operation is one IEEE rounding in the reference's order (numpy never fuses).
+struct LocalArgs {
+    int64_t n;
+    const double *pos;
+    double *pos_out;
+    const double *bh;
+    const int32_t *csr_off, *csr_tgt, *tris, *inc_off, *inc;
+    double spring, dlen, eta, c;
+    const double *temps;
+    const int32_t *ctr;
+    double *dbg_bh, *dbg_force, *dbg_scale;
+};
+
+__device__ __forceinline__ double2 ld2(const double *p, int i) {
+    return reinterpret_cast<const double2 *>(p)[i];
+}
+
+__global__ void local_kernel(LocalArgs a) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= a.n) return;
+    const double T = a.temps[*a.ctr];
+    const double2 pi = ld2(a.pos, (int)i);
+    double2 f = ld2(a.bh, (int)i);
+    if (a.dbg_bh) reinterpret_cast<double2 *>(a.dbg_bh)[i] = f;
+    // spring (layout.py:216-231): coef = -s*log((r+eta)/D); bincount in edge order
+    {
+        double sx = 0.0, sy = 0.0;
+        const double ns = -a.spring;
+        for (int e = a.csr_off[i]; e < a.csr_off[i + 1]; ++e) {
+            double2 pj = ld2(a.pos, a.csr_tgt[e]);
+            double dx = dsub(pi.x, pj.x), dy = dsub(pi.y, pj.y);
+            double r = hypot(dx, dy);
+            double coef = dmul(ns, log(__ddiv_rn(dadd(r, a.eta), a.dlen)));
+            sx = dadd(sx, dmul(coef, dx));
+            sy = dadd(sy, dmul(coef, dy));
+        }
+        f.x = dadd(f.x, sx);
+        f.y = dadd(f.y, sy);
+    }
+    // node-edge (layout.py:234-256): per corner k a bincount sum in triangle
+    // order, subtracted k = 0, 1, 2.  inc is sorted by (corner, triangle).
+    const int b0 = a.inc_off[i], b1 = a.inc_off[i + 1];
+    {
+        double nex = 0.0, ney = 0.0;  // running forces array (starts at zeros)
+        int e = b0;
+        for (int k = 0; k < 3; ++k) {
+            double px = 0.0, py = 0.0;
+            for (; e < b1 && (a.inc[e] & 3) == k; ++e) {
+                int tt = a.inc[e] >> 2;
+                int4 tr = reinterpret_cast<const int4 *>(a.tris)[tt];
+                int tv[3] = {tr.x, tr.y, tr.z};
+                double2 av = ld2(a.pos, tv[(k + 1) % 3]);
+                double2 bv = ld2(a.pos, tv[(k + 2) % 3]);
+                double ex = dsub(bv.x, av.x), ey = dsub(bv.y, av.y);
+                double ee = dadd(dmul(ex, ex), dmul(ey, ey));
+                if (ee == 0.0) ee = 1.0;
+                double t = __ddiv_rn(dadd(dmul(dsub(pi.x, av.x), ex), dmul(dsub(pi.y, av.y), ey)), ee);
+                double rx = dsub(dadd(av.x, dmul(t, ex)), pi.x);
+                double ry = dsub(dadd(av.y, dmul(t, ey)), pi.y);
+                double nr = hypot(rx, ry);
+                double coef = nr >= 1e-12 ? __ddiv_rn(__ddiv_rn(a.c, dadd(dmul(nr, nr), a.eta)), nr) : 0.0;
+                px = dadd(px, dmul(coef, rx));
+                py = dadd(py, dmul(coef, ry));
+            }
+            nex = dsub(nex, px);
+            ney = dsub(ney, py);
+        }
+        f.x = dadd(f.x, nex);
+        f.y = dadd(f.y, ney);
+    }
+    if (a.dbg_force) reinterpret_cast<double2 *>(a.dbg_force)[i] = f;
+    // temperature cap (layout.py:275-278)
+    double mag = hypot(f.x, f.y);
+    if (mag > T) {
+        double k = __ddiv_rn(T, mag);
+        f.x = dmul(f.x, k);
+        f.y = dmul(f.y, k);
+    }
+    // limiting-line clamp (layout.py:119-184): 3 rows per incident triangle
+    double smin = INFINITY;
+    for (int e = b0; e < b1; ++e) {
+        int tt = a.inc[e] >> 2;
+        int4 tr = reinterpret_cast<const int4 *>(a.tris)[tt];
+        double2 A = ld2(a.pos, tr.x), B = ld2(a.pos, tr.y), C = ld2(a.pos, tr.z);
+        double mabx = dmul(0.5, dadd(A.x, B.x)), maby = dmul(0.5, dadd(A.y, B.y));
+        double mbcx = dmul(0.5, dadd(B.x, C.x)), mbcy = dmul(0.5, dadd(B.y, C.y));
+        double mcax = dmul(0.5, dadd(C.x, A.x)), mcay = dmul(0.5, dadd(C.y, A.y));
+        const double ptx[3] = {mabx, mabx, mbcx}, pty[3] = {maby, maby, mbcy};
+        const double drx[3] = {dsub(mcax, mabx), dsub(mbcx, mabx), dsub(mcax, mbcx)};
+        const double dry[3] = {dsub(mcay, maby), dsub(mbcy, maby), dsub(mcay, mbcy)};
+#pragma unroll
+        for (int l = 0; l < 3; ++l) {
+            double nx = -dry[l], ny = drx[l];
+            double ln = hypot(nx, ny);
+            if (ln == 0.0) ln = 1.0;
+            nx = __ddiv_rn(nx, ln);
+            ny = __ddiv_rn(ny, ln);
+            double relx = dsub(pi.x, ptx[l]), rely = dsub(pi.y, pty[l]);
+            double sg = dadd(dmul(relx, nx), dmul(rely, ny));
+            double side = sg >= 0.0 ? 1.0 : -1.0;
+            double dist = fabs(sg);
+            double allowed = fmax(0.0, dsub(dist, a.eta));
+            double toward = dmul(-side, dadd(dmul(f.x, nx), dmul(f.y, ny)));
+            if (toward > allowed) {
+                double fac = __ddiv_rn(allowed, toward);
+                if (fac < smin) smin = fac;
+            }
+        }
+    }
+    double s = smin == INFINITY ? 1.0 : fmin(fmax(smin, 0.0), 1.0);
+    if (a.dbg_scale) a.dbg_scale[i] = s;
+    reinterpret_cast<double2 *>(a.pos_out)[i] =
+        make_double2(dadd(pi.x, dmul(s, f.x)), dadd(pi.y, dmul(s, f.y)));
+}
+
+__global__ void incr_kernel(int32_t *ctr) { ctr[0] += 1; }
+
+}  // namespace mdc
+
+using namespace mdc;
+
+struct MdcLayoutPlan {
+    MdcLayoutArgs a;
+    TreeShape shape;
+    Buffers b;
+    cudaGraphExec_t graph[2] = {nullptr, nullptr};
+    cudaStream_t cap_stream = nullptr;
+    const double *graph_temps = nullptr;
+};
+
+namespace mdc {
+
+// Builds the tree for pts into b.t; returns the final perm (leaf order).
+static int build_tree(MdcLayoutPlan *p, const double *pts, cudaStream_t s, const int32_t **perm_out) {
+    const TreeShape &sh = p->shape;
+    Buffers &b = p->b;
+    int64_t n = sh.n;
+    int nb = (int)((n + 255) / 256);
+    keys_kernel<<<nb, 256, 0, s>>>(pts, n, b.kx, b.ky, b.ids);
+    MDC_CHECK_LAUNCH();
+    size_t bytes = b.cub_bytes;
+    MDC_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(b.cub_tmp, bytes, b.kx, b.kx_out, b.ids, b.xs[0],
+                                                   (int)n, 0, 64, s));
+    bytes = b.cub_bytes;
+    MDC_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(b.cub_tmp, bytes, b.ky, b.ky_out, b.ids, b.ys[0],
+                                                   (int)n, 0, 64, s));
+    int cur = 0;
+    int nsb = (int)((n + SCAN_BLOCK - 1) / SCAN_BLOCK);
+    int32_t *prefix = reinterpret_cast<int32_t *>(b.kx);  // kx is free after the sort
+    for (int L = 0; L <= sh.max_depth; ++L) {
+        int c0 = sh.nd_off[L], cnt = sh.nd_off[L + 1] - c0;
+        if (cnt > 0) {
+            node_stats_kernel<<<(cnt + 127) / 128, 128, 0, s>>>(pts, b.t, b.t.nd_list + c0, cnt,
+                                                                b.xs[cur], b.ys[cur]);
+            MDC_CHECK_LAUNCH();
+        }
+        if (L == sh.max_depth) break;
+        int seg0 = sh.seg_off[L], nseg = sh.seg_off[L + 1] - seg0;
+        flag_kernel<<<nb, 256, 0, s>>>(n, b.t, seg0, nseg, b.xs[cur], b.ys[cur], b.flag);
+        blocksum_kernel<<<nsb, SCAN_BLOCK, 0, s>>>(n, b.t, seg0, nseg, b.xs[cur], b.ys[cur], b.flag,
+                                                   b.blocksum);
+        blockscan_kernel<<<1, SCAN_BLOCK, 0, s>>>(nsb, b.blocksum);
+        scatter_kernel<<<nsb, SCAN_BLOCK, 0, s>>>(n, b.t, seg0, nseg, b.xs[cur], b.ys[cur], b.flag,
+                                                  b.blocksum, b.xs[cur ^ 1], b.ys[cur ^ 1], prefix);
+        partition_kernel<<<nb, 256, 0, s>>>(n, b.t, seg0, nseg, b.xs[cur], b.ys[cur], b.flag, prefix,
+                                            b.xs[cur ^ 1], b.ys[cur ^ 1]);
+        MDC_CHECK_LAUNCH();
+        cur ^= 1;
+    }
+    int nn = (int)sh.lo.size();
+    com_kernel<<<(nn * 32 + 255) / 256, 256, 0, s>>>(pts, b.t, nn, b.xs[cur]);
+    MDC_CHECK_LAUNCH();
+    *perm_out = b.xs[cur];
+    return MDC_OK;
+}
+
+static int run_bh(MdcLayoutPlan *p, const double *pts, double *out, cudaStream_t s) {
+    const int32_t *perm = nullptr;
+    int rc = build_tree(p, pts, s, &perm);
+    if (rc) return rc;
+    int64_t n = p->shape.n;
+    int64_t warps = (n + 31) / 32;
+    bh_kernel<<<(unsigned)((warps + BH_WARPS - 1) / BH_WARPS), BH_WARPS * 32, 0, s>>>(
+        pts, n, p->b.t, perm, p->a.c, p->a.eta, p->a.theta, out);
+    MDC_CHECK_LAUNCH();
+    return MDC_OK;
+}
+
+static int enqueue_step(MdcLayoutPlan *p, const double *pin, double *pout, const double *temps,
+                        cudaStream_t s) {
+    int64_t n = p->shape.n;
+    if (n >= 2) {
+        int rc = run_bh(p, pin, p->b.bh, s);
+        if (rc) return rc;
+    } else {
+        MDC_CHECK_CUDA(cudaMemsetAsync(p->b.bh, 0, sizeof(double) * 2 * (size_t)n, s));
+    }
+    LocalArgs la;
+    la.n = n;
+    la.pos = pin;
+    la.pos_out = pout;
+    la.bh = p->b.bh;
+    la.csr_off = p->a.csr_off;
+    la.csr_tgt = p->a.csr_tgt;
+    la.tris = p->a.tris;
+    la.inc_off = p->a.inc_off;
+    la.inc = p->a.inc;
+    la.spring = p->a.spring;
+    la.dlen = p->a.dlen;
+    la.eta = p->a.eta;
+    la.c = p->a.c;
+    la.temps = temps;
+    la.ctr = p->b.ctr;
+    la.dbg_bh = p->a.dbg_bh;
+    la.dbg_force = p->a.dbg_force;
+    la.dbg_scale = p->a.dbg_scale;
+    local_kernel<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(la);
+    incr_kernel<<<1, 1, 0, s>>>(p->b.ctr);
+    MDC_CHECK_LAUNCH();
+    return MDC_OK;
+}
+
+}  // namespace mdc
+
+extern "C" size_t mdc_layout_workspace_bytes(int64_t n, int32_t leaf) {
+    TreeShape sh;
+    make_shape(sh, n, leaf);
+    Buffers b;
+    return carve(b, nullptr, sh);
+}
+
+extern "C" int mdc_layout_plan_create(const MdcLayoutArgs *a, MdcLayoutPlan **plan, void *stream) {
+    MDC_REQUIRE(a && plan, "null pointer");
+    MDC_REQUIRE(a->n >= 1 && a->n < (1LL << 31), "n out of range");
+    MDC_REQUIRE(a->leaf >= 1, "leaf must be >= 1");
+    MDC_REQUIRE(a->pos && a->csr_off && a->csr_tgt && a->inc_off && (a->ntri == 0 || (a->tris && a->inc)),
+                "null topology pointer");
+    MdcLayoutPlan *p = new MdcLayoutPlan();
+    p->a = *a;
+    make_shape(p->shape, a->n, a->leaf);
+    size_t need = carve(p->b, reinterpret_cast<char *>(a->workspace), p->shape);
+    if (a->workspace == nullptr || a->workspace_bytes < need) {
+        delete p;
+        set_error("layout workspace too small: need " + std::to_string(need) + " bytes");
+        return MDC_EINVAL;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    const TreeShape &sh = p->shape;
+    size_t nn = sh.lo.size();
+    auto up = [&](int32_t *dst, const std::vector<int32_t> &v) -> int {
+        if (!v.empty())
+            MDC_CHECK_CUDA(cudaMemcpyAsync(dst, v.data(), v.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+        return MDC_OK;
+    };
+    int rc = 0;
+    rc |= up(p->b.t.lo, sh.lo);
+    rc |= up(p->b.t.hi, sh.hi);
+    rc |= up(p->b.t.left, sh.left);
+    rc |= up(p->b.t.right, sh.right);
+    rc |= up(p->b.t.nd_list, sh.nd_list);
+    rc |= up(p->b.t.seg_lo, sh.seg_lo);
+    rc |= up(p->b.t.seg_hi, sh.seg_hi);
+    rc |= up(p->b.t.seg_node, sh.seg_node);
+    rc |= up(p->b.t.seg_split, sh.seg_split);
+    (void)nn;
+    if (rc) {
+        delete p;
+        return MDC_ECUDA;
+    }
+    // host vectors must outlive the async copies
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) {
+        delete p;
+        set_error(std::string("plan upload: ") + cudaGetErrorString(e));
+        return MDC_ECUDA;
+    }
+    *plan = p;
+    return MDC_OK;
+}
+
+extern "C" int mdc_layout_plan_destroy(MdcLayoutPlan *p) {
+    if (!p) return MDC_OK;
+    for (auto &g : p->graph)
+        if (g) cudaGraphExecDestroy(g);
+    if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
+    delete p;
+    return MDC_OK;
+}
+
+extern "C" int mdc_layout_steps(MdcLayoutPlan *p, int32_t k, const double *temps, int32_t use_graph,
+                                void *stream) {
+    MDC_REQUIRE(p && temps, "null pointer");
+    MDC_REQUIRE(k >= 0, "k must be >= 0");
+    if (k == 0) return MDC_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    MDC_CHECK_CUDA(cudaMemsetAsync(p->b.ctr, 0, sizeof(int32_t), s));
+    double *bufs[2] = {p->a.pos, p->b.pos_b};
+    bool dbg = p->a.dbg_bh || p->a.dbg_force || p->a.dbg_scale;
+    if (use_graph && !dbg) {
+        for (int par = 0; par < 2; ++par) {
+            if (p->graph[par]) continue;
+            if (!p->cap_stream) MDC_CHECK_CUDA(cudaStreamCreateWithFlags(&p->cap_stream, cudaStreamNonBlocking));
+            MDC_CHECK_CUDA(cudaStreamBeginCapture(p->cap_stream, cudaStreamCaptureModeThreadLocal));
+            int rc = enqueue_step(p, bufs[par], bufs[par ^ 1], temps, p->cap_stream);
+            cudaGraph_t g;
+            cudaError_t e = cudaStreamEndCapture(p->cap_stream, &g);
+            if (rc) return rc;
+            MDC_CHECK_CUDA(e);
+            e = cudaGraphInstantiate(&p->graph[par], g, 0);
+            cudaGraphDestroy(g);
+            MDC_CHECK_CUDA(e);
+            p->graph_temps = temps;
+        }
+        MDC_REQUIRE(p->graph_temps == temps, "temps pointer changed after graph capture");
+        for (int it = 0; it < k; ++it) MDC_CHECK_CUDA(cudaGraphLaunch(p->graph[it & 1], s));
+    } else {
+        for (int it = 0; it < k; ++it) {
+            int rc = enqueue_step(p, bufs[it & 1], bufs[(it & 1) ^ 1], temps, s);
+            if (rc) return rc;
+        }
+    }
+    if (k & 1)
+        MDC_CHECK_CUDA(cudaMemcpyAsync(p->a.pos, p->b.pos_b, sizeof(double) * 2 * (size_t)p->shape.n,
+                                       cudaMemcpyDeviceToDevice, s));
+    return MDC_OK;
+}
+
+extern "C" int mdc_layout_repulsion(MdcLayoutPlan *p, const double *pts, double *out, void *stream) {
+    MDC_REQUIRE(p && pts && out, "null pointer");
+    cudaStream_t s = (cudaStream_t)stream;
+    if (p->shape.n < 2) {
+        MDC_CHECK_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * 2 * (size_t)p->shape.n, s));
+        return MDC_OK;
+    }
+    return run_bh(p, pts, out, s);
+}
+
+extern "C" int64_t mdc_layout_node_count(const MdcLayoutPlan *p) { return p ? (int64_t)p->shape.lo.size() : 0; }
+
+extern "C" int mdc_layout_kdtree(MdcLayoutPlan *p, const double *pts, int32_t *perm, int32_t *lo,
+                                 int32_t *hi, int32_t *left, int32_t *right, double *com,
+                                 double *mass, double *size, double *bmin, double *bmax,
+                                 void *stream) {
+    MDC_REQUIRE(p && pts, "null pointer");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int32_t *pm = nullptr;
+    int rc = build_tree(p, pts, s, &pm);
+    if (rc) return rc;
+    size_t nn = p->shape.lo.size();
+    int64_t n = p->shape.n;
+    auto cp = [&](void *dst, const void *src, size_t bytes) -> int {
+        if (dst) MDC_CHECK_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, s));
+        return MDC_OK;
+    };
+    rc |= cp(perm, pm, n * 4);
+    rc |= cp(lo, p->b.t.lo, nn * 4);
+    rc |= cp(hi, p->b.t.hi, nn * 4);
+    rc |= cp(left, p->b.t.left, nn * 4);
+    rc |= cp(right, p->b.t.right, nn * 4);
+    rc |= cp(com, p->b.t.com, nn * 16);
+    rc |= cp(mass, p->b.t.mass, nn * 8);
+    rc |= cp(size, p->b.t.size, nn * 8);
+    rc |= cp(bmin, p->b.t.bmin, nn * 16);
+    rc |= cp(bmax, p->b.t.bmax, nn * 16);
+    return rc ? MDC_ECUDA : MDC_OK;
+}

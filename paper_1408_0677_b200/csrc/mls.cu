@@ -1,0 +1,743 @@
+// mls.cu -- global-support moving-least-squares field on B200 (sm_100a).
+//
+// Replaces _kernels.mean_field / affine_field / rigid_field
+// (/root/reference/pkg/src/mdcontour/_kernels.py:52-175) as dispatched by
+// field.compute_field (field.py:582-659), fused with the band epilogue
+// render._band_indices (render.py:135-139), and field._snap_control_pixels
+// (field.py:388-412).
+//
+// Formulation (SURVEY.md §8a M6'): every pixel v works in a pixel-tile-local
+// frame; with delta_j = p_j - v and phi_j = [1, dx_j, dy_j],
+//     A = sum_j w_j phi_j phi_j^T   (3x3, 6 unique moments)
+//     B = sum_j w_j phi_j q_j^T     (3 x d)
+// and the affine MLS value is f_k = e0^T (A + diag(0,r,r))^{-1} B[:,k] with
+// r = reg_eps * tr(Schur complement of A_00) -- algebraically identical to the
+// reference's centred 2x2 solve (_kernels.py:102-124).  Because only row 0 of
+// A^{-1} is needed, the kernel runs TWO passes over the controls:
+//   pass 1:  the 6 moments -> c = A_reg^{-1} e0   (per pixel, solved in fp64)
+//   pass 2:  f_k = sum_j w_j (c0 + c1 dx_j + c2 dy_j) q_jk
+// which costs (13) + (9 + d) FMA-pipe ops per (pixel, control) pair instead
+// of 14 + 3d for the one-pass RHS -- 2x fewer at d = 32.
+// Controls stream through shared memory tile by tile (cp.async double
+// buffering for the target block; positions are re-centred on the CTA's
+// pixel tile in fp64 before being rounded to the compute dtype, which keeps
+// fp32 cancellation relative to the tile size rather than the data extent).
+#include <math.h>
+
+#include "common.cuh"
+
+namespace mdc {
+
+enum AlphaMode { A_GENERIC = 0, A_ONE = 1, A_THREE_HALVES = 2, A_HALF = 3, A_TWO = 4 };
+
+static int alpha_mode(double a) {
+    if (a == 1.0) return A_ONE;
+    if (a == 1.5) return A_THREE_HALVES;
+    if (a == 0.5) return A_HALF;
+    if (a == 2.0) return A_TWO;
+    return A_GENERIC;
+}
+
+// ---- weights: w = d2^-alpha ------------------------------------------------
+__device__ __forceinline__ float rsqrt_approx(float x) {
+    float y;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float lg2_approx(float x) {
+    float y;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+template <int AM>
+__device__ __forceinline__ float weight(float d2, float neg_alpha) {
+    // fp32: no 1e-300 floor -- only pixels inside the snap radius can reach
+    // d2 ~ 0 and those are overwritten by the snap pass (field.py:648).
+    if (AM == A_THREE_HALVES) {
+        float r = rsqrt_approx(d2);
+        return r * r * r;
+    } else if (AM == A_ONE) {
+        return rcp_approx(d2);
+    } else if (AM == A_HALF) {
+        return rsqrt_approx(d2);
+    } else if (AM == A_TWO) {
+        float r = rcp_approx(d2);
+        return r * r;
+    } else {
+        return ex2_approx(neg_alpha * lg2_approx(d2));
+    }
+}
+
+template <int AM>
+__device__ __forceinline__ double weight(double d2, double neg_alpha) {
+    // fp64 mirrors _kernels.py:37-49 including the 1e-300 floor.
+    if (d2 < 1e-300) d2 = 1e-300;
+    if (AM == A_THREE_HALVES) {
+        double r = rsqrt(d2);
+        return r * r * r;
+    } else if (AM == A_ONE) {
+        return 1.0 / d2;
+    } else if (AM == A_HALF) {
+        return rsqrt(d2);
+    } else if (AM == A_TWO) {
+        double r = 1.0 / d2;
+        return r * r;
+    } else {
+        return pow(d2, neg_alpha);
+    }
+}
+
+// ---- tiling --------------------------------------------------------------
+constexpr int NT = 256;  // threads per CTA == controls per shared-memory tile
+
+template <typename T>
+struct V2;
+template <>
+struct V2<float> {
+    using type = float2;
+};
+template <>
+struct V2<double> {
+    using type = double2;
+};
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+struct KArgs {
+    int width, row0, nrows;
+    int64_t npix;             // nrows * width
+    int64_t p_begin, p_end;   // band as global pixel indices [row0*W, row1*W)
+    int64_t p_total;          // height * width
+    int64_t tile0;            // first CTA tile (global, aligned to NT*R)
+    double x0, y1, sx, sy, pmx, pmy;
+    int64_t n;
+    int d, ldq;
+    double alpha, reg_eps;
+    const double *pc;
+    const void *q;
+    const double *qm;
+    const int32_t *axis;
+    void *out;
+    int64_t out_cs, out_rs, out_ps;
+    int32_t *bands;
+    int64_t band_cs, band_rs;
+    const double *spacing;
+    int32_t *nonfinite;
+};
+
+// Pixel centre (global linear pixel index p) in the globally-centred frame,
+// bit-identical to `xs.ravel() - pm[0]` / `ys.ravel() - pm[1]` of
+// field.py:611-613.
+__device__ __forceinline__ void pixel_xy(const KArgs &a, int64_t p, double &vx, double &vy) {
+    int64_t row = p / a.width;
+    int col = (int)(p - row * a.width);
+    double xs = dadd(a.x0, dmul((double)col + 0.5, a.sx));
+    double ys = dsub(a.y1, dmul((double)row + 0.5, a.sy));
+    vx = dsub(xs, a.pmx);
+    vy = dsub(ys, a.pmy);
+}
+
+// Stage tile `t` of the control positions (fp64, re-centred on o) into sxy,
+// and issue the cp.async copies of its target block channels [c0, c0+DC).
+template <typename T, int DC>
+struct Stager {
+    static constexpr int QV = (DC * (int)sizeof(T) + 15) / 16;  // 16 B vectors per control
+    __device__ static void load_xy(const KArgs &a, int64_t t, double &rx, double &ry) {
+        int64_t j = t * NT + threadIdx.x;
+        if (j < a.n) {
+            double2 v = reinterpret_cast<const double2 *>(a.pc)[j];
+            rx = v.x;
+            ry = v.y;
+        } else {
+            rx = 0.0;
+            ry = 0.0;
+        }
+    }
+    __device__ static void issue_q(const KArgs &a, int64_t t, int c0, T *sq) {
+        // sq: NT controls x (QV*16/sizeof(T)) elements.  Requires ldq*sizeof(T)
+        // and c0*sizeof(T) to be multiples of 16 (host pads ldq).
+        const char *qb = reinterpret_cast<const char *>(a.q);
+        for (int e = threadIdx.x; e < NT * QV; e += NT) {
+            int jl = e / QV, v = e - jl * QV;
+            int64_t j = t * NT + jl;
+            if (j < a.n) {
+                const char *src = qb + ((size_t)j * a.ldq + c0) * sizeof(T) + v * 16;
+                cp_async16(reinterpret_cast<char *>(sq) + (size_t)e * 16, src);
+            }
+        }
+        cp_async_commit();
+    }
+};
+
+template <typename T>
+__device__ __forceinline__ T to_t(double x) {
+    return (T)x;
+}
+
+// ------------------------------------------------------------------------------
+// The fused kernel.  VAR: MDC_MEAN / MDC_AFFINE / MDC_RIGID; DC: channels per
+// pass-2 chunk; R: pixels per thread.
+template <typename T, int VAR, int AM, int DC, int R>
+__global__ void __launch_bounds__(NT) mls_kernel(KArgs a) {
+    using T2 = typename V2<T>::type;
+    constexpr int QE = Stager<T, DC>::QV * 16 / (int)sizeof(T);  // padded channels per control
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T2 *sxy = reinterpret_cast<T2 *>(smem_raw);
+    T *sq0 = reinterpret_cast<T *>(smem_raw + NT * sizeof(T2));
+    T *sq1 = sq0 + NT * QE;
+
+    const int tid = threadIdx.x;
+    // Tiles are aligned in GLOBAL pixel-index space, so a pixel's tile (and
+    // hence its local frame and every rounding) does not depend on how the
+    // frame is split into row bands: 1-GPU and N-GPU outputs are bit-identical.
+    const int64_t tile_base = (a.tile0 + blockIdx.x) * (int64_t)(NT * R);
+    const T neg_alpha = (T)(-a.alpha);
+
+    // Tile-local frame origin: the centre pixel of this CTA's tile.
+    double ox, oy;
+    {
+        int64_t mid = tile_base + (NT * R) / 2;
+        if (mid >= a.p_total) mid = a.p_total - 1;
+        pixel_xy(a, mid, ox, oy);
+    }
+    double vxg[R], vyg[R];  // global-centred pixel coordinates
+    T vx[R], vy[R];         // tile-local
+    bool active[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        int64_t p = tile_base + r * NT + tid;
+        active[r] = p >= a.p_begin && p < a.p_end;
+        if (!active[r]) p = p < a.p_begin ? a.p_begin : a.p_end - 1;
+        pixel_xy(a, p, vxg[r], vyg[r]);
+        vx[r] = to_t<T>(vxg[r] - ox);
+        vy[r] = to_t<T>(vyg[r] - oy);
+    }
+    const int64_t ntiles = (a.n + NT - 1) / NT;
+
+    // Generic streaming loop over all control tiles; body(sxy, sq, count).
+    auto stream_controls = [&](int c0, bool need_q, auto &&body) {
+        double rx, ry;
+        Stager<T, DC>::load_xy(a, 0, rx, ry);
+        if (need_q) Stager<T, DC>::issue_q(a, 0, c0, sq0);
+        for (int64_t t = 0; t < ntiles; ++t) {
+            __syncthreads();  // previous tile fully consumed
+            sxy[tid] = T2{to_t<T>(rx - ox), to_t<T>(ry - oy)};
+            T *cur = (t & 1) ? sq1 : sq0;
+            if (t + 1 < ntiles) {
+                Stager<T, DC>::load_xy(a, t + 1, rx, ry);
+                if (need_q) Stager<T, DC>::issue_q(a, t + 1, c0, (t & 1) ? sq0 : sq1);
+            }
+            if (need_q) {
+                if (t + 1 < ntiles)
+                    cp_async_wait<1>();
+                else
+                    cp_async_wait<0>();
+            }
+            __syncthreads();
+            int cnt = (int)min((int64_t)NT, a.n - t * NT);
+            body(cur, cnt);
+        }
+    };
+
+    if constexpr (VAR == MDC_AFFINE) {
+        // ---------------- pass 1: moments ----------------
+        T sw[R], mx[R], my[R], sxx[R], sxy_[R], syy[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) sw[r] = mx[r] = my[r] = sxx[r] = sxy_[r] = syy[r] = T(0);
+        stream_controls(0, false, [&](const T *, int cnt) {
+#pragma unroll 4
+            for (int j = 0; j < cnt; ++j) {
+                T2 p = sxy[j];
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    T dx = p.x - vx[r], dy = p.y - vy[r];
+                    T w = weight<AM>(dx * dx + dy * dy, neg_alpha);
+                    T wdx = w * dx, wdy = w * dy;
+                    sw[r] += w;
+                    mx[r] += wdx;
+                    my[r] += wdy;
+                    sxx[r] += wdx * dx;
+                    sxy_[r] += wdx * dy;
+                    syy[r] += wdy * dy;
+                }
+            }
+        });
+        // per-pixel solve in fp64: c = (A + diag(0, reg, reg))^{-1} e0
+        T c0[R], c1[R], c2[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            double s = sw[r], m0 = mx[r], m1 = my[r];
+            double a00 = (double)sxx[r] - m0 * m0 / s;
+            double a01 = (double)sxy_[r] - m0 * m1 / s;
+            double a11 = (double)syy[r] - m1 * m1 / s;
+            double reg = a.reg_eps * (a00 + a11);
+            a00 += reg;
+            a11 += reg;
+            double det = a00 * a11 - a01 * a01;
+            double u0 = (a11 * m0 - a01 * m1) / det;
+            double u1 = (a00 * m1 - a01 * m0) / det;
+            c0[r] = to_t<T>(1.0 / s + (m0 * u0 + m1 * u1) / (s * s));
+            c1[r] = to_t<T>(-u0 / s);
+            c2[r] = to_t<T>(-u1 / s);
+        }
+        // ---------------- pass 2: weighted RHS, chunked over channels --------
+        bool bad[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) bad[r] = false;
+        for (int c0ch = 0; c0ch < a.d; c0ch += DC) {
+            T acc[R][DC];
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+#pragma unroll
+                for (int k = 0; k < DC; ++k) acc[r][k] = T(0);
+            stream_controls(c0ch, true, [&](const T *sq, int cnt) {
+#pragma unroll 2
+                for (int j = 0; j < cnt; ++j) {
+                    T2 p = sxy[j];
+                    T qv[DC];
+#pragma unroll
+                    for (int k = 0; k < DC; ++k) qv[k] = sq[j * QE + k];
+#pragma unroll
+                    for (int r = 0; r < R; ++r) {
+                        T dx = p.x - vx[r], dy = p.y - vy[r];
+                        T w = weight<AM>(dx * dx + dy * dy, neg_alpha);
+                        T g = w * (c0[r] + c1[r] * dx + c2[r] * dy);
+#pragma unroll
+                        for (int k = 0; k < DC; ++k) acc[r][k] += g * qv[k];
+                    }
+                }
+            });
+            // epilogue: add back qm, write, bands
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                if (!active[r]) continue;
+                int64_t p = tile_base + r * NT + tid;
+                int64_t row = p / a.width;
+                int64_t col = p - row * a.width;
+                int64_t lr = row - a.row0;
+#pragma unroll
+                for (int k = 0; k < DC; ++k) {
+                    int ch = c0ch + k;
+                    if (ch >= a.d) break;
+                    T f = to_t<T>((double)acc[r][k] + a.qm[ch]);
+                    reinterpret_cast<T *>(a.out)[ch * a.out_cs + lr * a.out_rs + col * a.out_ps] = f;
+                    if (!isfinite((double)f)) bad[r] = true;
+                    if (a.bands)
+                        a.bands[ch * a.band_cs + lr * a.band_rs + col] =
+                            (int32_t)floor((double)f / a.spacing[ch]);
+                }
+            }
+        }
+        if (a.nonfinite) {
+            int cnt = 0;
+#pragma unroll
+            for (int r = 0; r < R; ++r) cnt += (active[r] && bad[r]) ? 1 : 0;
+            if (cnt) atomicAdd(a.nonfinite, cnt);
+        }
+    } else if constexpr (VAR == MDC_MEAN) {
+        // f_k = v_axis + sum w dq_k / sum w   (_kernels.py:52-67), chunked.
+        bool bad[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) bad[r] = false;
+        for (int c0ch = 0; c0ch < a.d; c0ch += DC) {
+            T acc[R][DC], sw[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                sw[r] = T(0);
+#pragma unroll
+                for (int k = 0; k < DC; ++k) acc[r][k] = T(0);
+            }
+            stream_controls(c0ch, true, [&](const T *sq, int cnt) {
+#pragma unroll 2
+                for (int j = 0; j < cnt; ++j) {
+                    T2 p = sxy[j];
+                    T qv[DC];
+#pragma unroll
+                    for (int k = 0; k < DC; ++k) qv[k] = sq[j * QE + k];
+#pragma unroll
+                    for (int r = 0; r < R; ++r) {
+                        T dx = p.x - vx[r], dy = p.y - vy[r];
+                        T w = weight<AM>(dx * dx + dy * dy, neg_alpha);
+                        sw[r] += w;
+#pragma unroll
+                        for (int k = 0; k < DC; ++k) acc[r][k] += w * qv[k];
+                    }
+                }
+            });
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                if (!active[r]) continue;
+                int64_t p = tile_base + r * NT + tid;
+                int64_t row = p / a.width;
+                int64_t col = p - row * a.width;
+                int64_t lr = row - a.row0;
+#pragma unroll
+                for (int k = 0; k < DC; ++k) {
+                    int ch = c0ch + k;
+                    if (ch >= a.d) break;
+                    double v = a.axis[ch] == 0 ? vxg[r] : vyg[r];
+                    T f = to_t<T>((v + (double)acc[r][k] / (double)sw[r]) + a.qm[ch]);
+                    reinterpret_cast<T *>(a.out)[ch * a.out_cs + lr * a.out_rs + col * a.out_ps] = f;
+                    if (!isfinite((double)f)) bad[r] = true;
+                    if (a.bands)
+                        a.bands[ch * a.band_cs + lr * a.band_rs + col] =
+                            (int32_t)floor((double)f / a.spacing[ch]);
+                }
+            }
+        }
+        if (a.nonfinite) {
+            int cnt = 0;
+#pragma unroll
+            for (int r = 0; r < R; ++r) cnt += (active[r] && bad[r]) ? 1 : 0;
+            if (cnt) atomicAdd(a.nonfinite, cnt);
+        }
+    } else {
+        // Rigid (_kernels.py:127-175), 2 channels, one pass, pixel-local frame.
+        T sw[R], mx[R], my[R], bqx[R], bqy[R], b00[R], b01[R], b10[R], b11[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+            sw[r] = mx[r] = my[r] = bqx[r] = bqy[r] = b00[r] = b01[r] = b10[r] = b11[r] = T(0);
+        stream_controls(0, true, [&](const T *sq, int cnt) {
+#pragma unroll 2
+            for (int j = 0; j < cnt; ++j) {
+                T2 p = sxy[j];
+                T qx = sq[j * QE + 0], qy = sq[j * QE + 1];
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    T dx = p.x - vx[r], dy = p.y - vy[r];
+                    T w = weight<AM>(dx * dx + dy * dy, neg_alpha);
+                    T wdx = w * dx, wdy = w * dy;
+                    sw[r] += w;
+                    mx[r] += wdx;
+                    my[r] += wdy;
+                    bqx[r] += w * qx;
+                    bqy[r] += w * qy;
+                    b00[r] += wdx * qx;
+                    b01[r] += wdx * qy;
+                    b10[r] += wdy * qx;
+                    b11[r] += wdy * qy;
+                }
+            }
+        });
+        int cnt_bad = 0;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            if (!active[r]) continue;
+            double s = sw[r];
+            double psx = (double)mx[r] / s, psy = (double)my[r] / s;  // delta*
+            double qsx = (double)bqx[r] / s, qsy = (double)bqy[r] / s;
+            double c00 = (double)b00[r] - qsx * (double)mx[r];
+            double c01 = (double)b01[r] - qsy * (double)mx[r];
+            double c10 = (double)b10[r] - qsx * (double)my[r];
+            double c11 = (double)b11[r] - qsy * (double)my[r];
+            double ss = c00 + c11, dd = c10 - c01;
+            double dx = -psx, dy = -psy;  // v - p*
+            double fx = dx * ss + dy * dd;
+            double fy = dy * ss - dx * dd;
+            double norm = hypot(fx, fy);
+            double ox_, oy_;
+            if (norm < 1e-12) {
+                // mean-blend fallback vx + (mq - mp)/sw (_kernels.py:168-171);
+                // with p* = v + delta* this is q* - delta*.
+                ox_ = qsx - psx;
+                oy_ = qsy - psy;
+            } else {
+                double rr = hypot(dx, dy) / norm;
+                ox_ = fx * rr + qsx;
+                oy_ = fy * rr + qsy;
+            }
+            T f0 = to_t<T>(ox_ + a.qm[0]), f1 = to_t<T>(oy_ + a.qm[1]);
+            int64_t p = tile_base + r * NT + tid;
+            int64_t row = p / a.width;
+            int64_t col = p - row * a.width;
+            int64_t lr = row - a.row0;
+            T *o = reinterpret_cast<T *>(a.out);
+            o[lr * a.out_rs + col * a.out_ps] = f0;
+            o[a.out_cs + lr * a.out_rs + col * a.out_ps] = f1;
+            if (a.bands) {
+                a.bands[lr * a.band_rs + col] = (int32_t)floor((double)f0 / a.spacing[0]);
+                a.bands[a.band_cs + lr * a.band_rs + col] = (int32_t)floor((double)f1 / a.spacing[1]);
+            }
+            if (!isfinite((double)f0) || !isfinite((double)f1)) ++cnt_bad;
+        }
+        if (a.nonfinite && cnt_bad) atomicAdd(a.nonfinite, cnt_bad);
+    }
+}
+
+template <typename T, int DC>
+static size_t smem_bytes() {
+    constexpr int QE = Stager<T, DC>::QV * 16 / (int)sizeof(T);
+    return NT * sizeof(typename V2<T>::type) + 2 * (size_t)NT * QE * sizeof(T);
+}
+
+template <typename T, int VAR, int AM, int DC, int R>
+static int launch_t(const KArgs &k, cudaStream_t s) {
+    auto fn = mls_kernel<T, VAR, AM, DC, R>;
+    size_t smem = smem_bytes<T, DC>();
+    static bool attr_set = false;
+    if (!attr_set) {
+        MDC_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr_set = true;
+    }
+    KArgs kk = k;
+    const int64_t tile = NT * R;
+    kk.tile0 = kk.p_begin / tile;
+    int64_t blocks = (kk.p_end + tile - 1) / tile - kk.tile0;
+    if (blocks > 0) fn<<<(unsigned)blocks, NT, smem, s>>>(kk);
+    MDC_CHECK_LAUNCH();
+    return MDC_OK;
+}
+
+template <typename T, int VAR, int AM>
+static int dispatch_dc(const KArgs &k, cudaStream_t s) {
+    // channel chunk: smallest instantiated DC >= d (cap 32 for f32, 16 for f64)
+    constexpr bool F32 = sizeof(T) == 4;
+    constexpr int R = 2;
+    int d = k.d;
+    if (VAR == MDC_RIGID) return launch_t<T, VAR, AM, 2, R>(k, s);
+    if (d <= 1) return launch_t<T, VAR, AM, 1, R>(k, s);
+    if (d <= 2) return launch_t<T, VAR, AM, 2, R>(k, s);
+    if (d <= 4) return launch_t<T, VAR, AM, 4, R>(k, s);
+    if (d <= 8) return launch_t<T, VAR, AM, 8, R>(k, s);
+    if (F32) {
+        if (d <= 16) return launch_t<T, VAR, AM, 16, R>(k, s);
+        return launch_t<T, VAR, AM, 32, R>(k, s);
+    }
+    return launch_t<T, VAR, AM, 16, R>(k, s);
+}
+
+template <typename T, int VAR>
+static int dispatch_alpha(const KArgs &k, cudaStream_t s) {
+    switch (alpha_mode(k.alpha)) {
+        case A_ONE: return dispatch_dc<T, VAR, A_ONE>(k, s);
+        case A_THREE_HALVES: return dispatch_dc<T, VAR, A_THREE_HALVES>(k, s);
+        case A_HALF: return dispatch_dc<T, VAR, A_HALF>(k, s);
+        case A_TWO: return dispatch_dc<T, VAR, A_TWO>(k, s);
+        default: return dispatch_dc<T, VAR, A_GENERIC>(k, s);
+    }
+}
+
+// Padded channel stride the stager requires (elements).
+static int required_chunk(int dtype, int d, int variant) {
+    if (variant == MDC_RIGID) return 2;
+    int cap = dtype == MDC_F32 ? 32 : 16;
+    int dc = 1;
+    while (dc < d && dc < cap) dc *= 2;
+    return dc;
+}
+
+// ---------------------------------------------------------------------------
+// Snap: four stream-ordered passes over the controls (field.py:388-412).
+struct SnapArgs {
+    int width, row0, row1, height;
+    double x0, y1, sx, sy, eps;
+    int rx, ry;
+    int64_t n;
+    int d, dtype;
+    const double *pos, *tvals;
+    void *out;
+    int64_t out_cs, out_rs, out_ps;
+    int32_t *bands;
+    int64_t band_cs, band_rs;
+    const double *spacing;
+    int32_t *nonfinite;
+    unsigned long long *best_d2;
+    unsigned *best_idx;
+};
+
+template <int PASS>
+__global__ void snap_kernel(SnapArgs a) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= a.n) return;
+    double px = a.pos[2 * i], py = a.pos[2 * i + 1];
+    double pxf = dsub(__ddiv_rn(dsub(px, a.x0), a.sx), 0.5);
+    double pyf = dsub(__ddiv_rn(dsub(a.y1, py), a.sy), 0.5);
+    // int(round(x)) on np.float64: round half to even == rint.
+    long long cx = (long long)rint(pxf), cy = (long long)rint(pyf);
+    long long ylo = max(cy - a.ry, (long long)max(0, a.row0));
+    long long yhi = min(cy + a.ry + 1, (long long)a.row1);
+    long long xlo = max(cx - a.rx, 0LL), xhi = min(cx + a.rx + 1, (long long)a.width);
+    for (long long yy = ylo; yy < yhi; ++yy) {
+        double ys = dsub(a.y1, dmul((double)yy + 0.5, a.sy));
+        double ey = dsub(ys, py);
+        double ey2 = dmul(ey, ey);
+        for (long long xx = xlo; xx < xhi; ++xx) {
+            double xs = dadd(a.x0, dmul((double)xx + 0.5, a.sx));
+            double ex = dsub(xs, px);
+            double d2 = dadd(dmul(ex, ex), ey2);
+            if (!(d2 < a.eps)) continue;
+            int64_t lr = yy - a.row0;
+            int64_t pix = lr * a.width + xx;
+            unsigned long long key = (unsigned long long)__double_as_longlong(d2);
+            if (PASS == 0) {
+                atomicMin(&a.best_d2[pix], key);
+            } else if (PASS == 1) {
+                if (a.best_d2[pix] == key) atomicMin(&a.best_idx[pix], (unsigned)i);
+            } else if (PASS == 2) {
+                if (a.best_idx[pix] != (unsigned)i) continue;
+                bool was_bad = false;
+                for (int k = 0; k < a.d; ++k) {
+                    int64_t off = k * a.out_cs + lr * a.out_rs + xx * a.out_ps;
+                    double v = a.tvals[i * a.d + k];
+                    if (a.dtype == MDC_F32) {
+                        float *o = reinterpret_cast<float *>(a.out);
+                        if (!isfinite(o[off])) was_bad = true;
+                        o[off] = (float)v;
+                        v = (double)(float)v;
+                    } else {
+                        double *o = reinterpret_cast<double *>(a.out);
+                        if (!isfinite(o[off])) was_bad = true;
+                        o[off] = v;
+                    }
+                    if (a.bands) a.bands[k * a.band_cs + lr * a.band_rs + xx] = (int32_t)floor(v / a.spacing[k]);
+                }
+                if (was_bad && a.nonfinite) atomicSub(a.nonfinite, 1);
+            } else {
+                a.best_d2[pix] = ~0ULL;
+                a.best_idx[pix] = ~0U;
+            }
+        }
+    }
+}
+
+}  // namespace mdc
+
+using namespace mdc;
+
+extern "C" int mdc_mls_field(const MdcMlsArgs *a, void *stream) {
+    MDC_REQUIRE(a != nullptr, "null args");
+    MDC_REQUIRE(a->variant == MDC_MEAN || a->variant == MDC_AFFINE || a->variant == MDC_RIGID,
+                "variant must be MDC_MEAN, MDC_AFFINE or MDC_RIGID");
+    MDC_REQUIRE(a->dtype == MDC_F32 || a->dtype == MDC_F64, "dtype must be MDC_F32 or MDC_F64");
+    MDC_REQUIRE(a->width > 0 && a->height > 0, "width/height must be positive");
+    MDC_REQUIRE(0 <= a->row0 && a->row0 <= a->row1 && a->row1 <= a->height, "bad row band");
+    MDC_REQUIRE(a->n > 0, "need at least one control");
+    MDC_REQUIRE(a->d >= 1, "need at least one channel");
+    MDC_REQUIRE(a->variant != MDC_RIGID || a->d == 2, "rigid MLS needs exactly 2 channels");
+    MDC_REQUIRE(a->variant != MDC_MEAN || a->axis != nullptr, "mean variant needs axis[]");
+    MDC_REQUIRE(a->pc && a->q && a->qm && a->out, "null device pointer");
+    MDC_REQUIRE(a->bands == nullptr || a->spacing != nullptr, "bands need spacing[]");
+    size_t es = a->dtype == MDC_F32 ? 4 : 8;
+    int chunk = required_chunk(a->dtype, a->d, a->variant);
+    int64_t need = ((a->d + chunk - 1) / chunk) * chunk;
+    MDC_REQUIRE(a->ldq >= need && (a->ldq * es) % 16 == 0,
+                "ldq must cover d rounded up to the channel chunk and be 16-byte aligned");
+    MDC_REQUIRE(((uintptr_t)a->q % 16) == 0 && ((uintptr_t)a->pc % 16) == 0,
+                "q and pc must be 16-byte aligned");
+    KArgs k;
+    k.width = a->width;
+    k.row0 = a->row0;
+    k.nrows = a->row1 - a->row0;
+    k.npix = (int64_t)k.nrows * a->width;
+    k.p_begin = (int64_t)a->row0 * a->width;
+    k.p_end = (int64_t)a->row1 * a->width;
+    k.p_total = (int64_t)a->height * a->width;
+    k.tile0 = 0;
+    k.x0 = a->x0;
+    k.y1 = a->y1;
+    k.sx = a->sx;
+    k.sy = a->sy;
+    k.pmx = a->pmx;
+    k.pmy = a->pmy;
+    k.n = a->n;
+    k.d = a->d;
+    k.ldq = a->ldq;
+    k.alpha = a->alpha;
+    k.reg_eps = a->reg_eps;
+    k.pc = a->pc;
+    k.q = a->q;
+    k.qm = a->qm;
+    k.axis = a->axis;
+    k.out = a->out;
+    k.out_cs = a->out_cs;
+    k.out_rs = a->out_rs;
+    k.out_ps = a->out_ps;
+    k.bands = a->bands;
+    k.band_cs = a->band_cs;
+    k.band_rs = a->band_rs;
+    k.spacing = a->spacing;
+    k.nonfinite = a->nonfinite;
+    if (k.npix == 0) return MDC_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (a->dtype == MDC_F32) {
+        switch (a->variant) {
+            case MDC_MEAN: return dispatch_alpha<float, MDC_MEAN>(k, s);
+            case MDC_AFFINE: return dispatch_alpha<float, MDC_AFFINE>(k, s);
+            default: return dispatch_alpha<float, MDC_RIGID>(k, s);
+        }
+    }
+    switch (a->variant) {
+        case MDC_MEAN: return dispatch_alpha<double, MDC_MEAN>(k, s);
+        case MDC_AFFINE: return dispatch_alpha<double, MDC_AFFINE>(k, s);
+        default: return dispatch_alpha<double, MDC_RIGID>(k, s);
+    }
+}
+
+extern "C" size_t mdc_snap_workspace_bytes(int32_t width, int32_t rows) {
+    return (size_t)width * (size_t)rows * (sizeof(unsigned long long) + sizeof(unsigned));
+}
+
+extern "C" int mdc_mls_snap(const MdcMlsArgs *a, const double *pos, const double *tvals, double eps,
+                            void *workspace, void *stream) {
+    MDC_REQUIRE(a && pos && tvals && workspace, "null pointer");
+    MDC_REQUIRE(eps > 0, "eps must be positive");
+    MDC_REQUIRE(0 <= a->row0 && a->row0 <= a->row1 && a->row1 <= a->height, "bad row band");
+    SnapArgs s;
+    s.width = a->width;
+    s.row0 = a->row0;
+    s.row1 = a->row1;
+    s.height = a->height;
+    s.x0 = a->x0;
+    s.y1 = a->y1;
+    s.sx = a->sx;
+    s.sy = a->sy;
+    s.eps = eps;
+    // field.py:398-399: r = int(ceil(sqrt(eps) / s)) + 1
+    s.rx = (int)ceil(sqrt(eps) / a->sx) + 1;
+    s.ry = (int)ceil(sqrt(eps) / a->sy) + 1;
+    s.n = a->n;
+    s.d = a->d;
+    s.dtype = a->dtype;
+    s.pos = pos;
+    s.tvals = tvals;
+    s.out = a->out;
+    s.out_cs = a->out_cs;
+    s.out_rs = a->out_rs;
+    s.out_ps = a->out_ps;
+    s.bands = a->bands;
+    s.band_cs = a->band_cs;
+    s.band_rs = a->band_rs;
+    s.spacing = a->spacing;
+    s.nonfinite = a->nonfinite;
+    int64_t npix = (int64_t)(a->row1 - a->row0) * a->width;
+    s.best_d2 = reinterpret_cast<unsigned long long *>(workspace);
+    s.best_idx = reinterpret_cast<unsigned *>(s.best_d2 + npix);
+    if (npix == 0 || a->n == 0) return MDC_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    unsigned blocks = (unsigned)((a->n + 127) / 128);
+    snap_kernel<0><<<blocks, 128, 0, st>>>(s);
+    snap_kernel<1><<<blocks, 128, 0, st>>>(s);
+    snap_kernel<2><<<blocks, 128, 0, st>>>(s);
+    snap_kernel<3><<<blocks, 128, 0, st>>>(s);
+    MDC_CHECK_LAUNCH();
+    return MDC_OK;
+}

@@ -1,0 +1,388 @@
+"""Per-pixel moving-least-squares field on the GPU.
+
+Drop-in mirror of the reference's ``field`` module
+(/root/reference/pkg/src/mdcontour/field.py): same dataclasses, defaults,
+validation and exceptions; ``compute_field`` keeps its signature and numpy
+return type (fp64 by default, matching the reference's arithmetic to the
+1e-10 normwise contract).  ``compute_fields`` is the fused entry the
+north-star metric is measured on: d target channels in one launch, fp32 or
+fp64, optional row band (multi-GPU sharding) and fused band epilogue, torch
+CUDA tensors in and out.
+
+All arithmetic runs in libmdc (``mdc_mls_field`` + ``mdc_mls_snap``); only
+the O(N) centring / viewport set-up stays on the host, computed with the same
+numpy expressions as field.py:596-613 so the pixel grid is bit-identical.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import struct
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .dataset import Dataset
+from .projection import expand_bounds
+
+VARIANTS = ("linear", "mean", "affine", "rigid")
+DEFAULT_ALPHA = {"linear": 1.0, "mean": 1.0, "affine": 1.5, "rigid": 1.0}
+ALPHA_RANGE = (0.25, 3.0)
+
+
+class FieldError(Exception):
+    pass
+
+
+class DegenerateRotation(FieldError):
+    """Rigid solve collapsed (zero rotation estimate) at the sample point."""
+
+
+@dataclass(frozen=True)
+class MlsParams:
+    """field.py:52-72."""
+
+    variant: str = "affine"
+    alpha: float | None = None
+    epsilon_dist: float | None = None
+    reg_eps: float = 1e-12
+
+    def __post_init__(self):
+        if self.variant not in VARIANTS:
+            raise ValueError(f"variant must be one of {VARIANTS}, got {self.variant!r}")
+        a = self.resolved_alpha
+        if not 0.1 < a <= 4.0:
+            raise ValueError(f"alpha must be in (0.1, 4.0], got {a}")
+        if self.reg_eps <= 0:
+            raise ValueError("reg_eps must be positive")
+        if self.epsilon_dist is not None and self.epsilon_dist <= 0:
+            raise ValueError("epsilon_dist must be positive")
+
+    @property
+    def resolved_alpha(self) -> float:
+        return DEFAULT_ALPHA[self.variant] if self.alpha is None else self.alpha
+
+
+@dataclass(frozen=True)
+class TargetAssignment:
+    """field.py:75-89."""
+
+    targets: np.ndarray
+    mode: str
+    dims: tuple[str, ...] = ()
+
+    def __post_init__(self):
+        if not np.all(np.isfinite(self.targets)):
+            raise FieldError("target coordinates must be finite")
+
+    @property
+    def active_channels(self) -> int:
+        return 1 if self.mode == "dims" and len(self.dims) == 1 else 2
+
+
+def projection_targets(mesh) -> TargetAssignment:
+    return TargetAssignment(targets=mesh.original_pos.copy(), mode="projection")
+
+
+def dimension_targets(ds: Dataset, dim_a: str, dim_b: str | None = None) -> TargetAssignment:
+    """field.py:96-105."""
+    a = ds.raw_column(dim_a)
+    if dim_b is None:
+        return TargetAssignment(targets=np.column_stack([a, np.zeros_like(a)]), mode="dims", dims=(dim_a,))
+    b = ds.raw_column(dim_b)
+    return TargetAssignment(targets=np.column_stack([a, b]), mode="dims", dims=(dim_a, dim_b))
+
+
+@dataclass(frozen=True)
+class ViewportTransform:
+    """field.py:108-142."""
+
+    x0: float
+    y0: float
+    x1: float
+    y1: float
+    width: int
+    height: int
+
+    @property
+    def units_per_px(self) -> tuple[float, float]:
+        return ((self.x1 - self.x0) / self.width, (self.y1 - self.y0) / self.height)
+
+    def pixel_center_grids(self) -> tuple[np.ndarray, np.ndarray]:
+        sx, sy = self.units_per_px
+        xs = self.x0 + (np.arange(self.width) + 0.5) * sx
+        ys = self.y1 - (np.arange(self.height) + 0.5) * sy
+        return np.meshgrid(xs, ys)
+
+    def to_pixels(self, points: np.ndarray) -> np.ndarray:
+        sx, sy = self.units_per_px
+        px = (points[:, 0] - self.x0) / sx - 0.5
+        py = (self.y1 - points[:, 1]) / sy - 0.5
+        return np.column_stack([px, py])
+
+    @classmethod
+    def fit(cls, points: np.ndarray, width: int, height: int) -> "ViewportTransform":
+        x0, y0, x1, y1 = expand_bounds(points)
+        return cls(x0, y0, x1, y1, width, height)
+
+
+@dataclass
+class CoordinateField:
+    """field.py:145-161."""
+
+    width: int
+    height: int
+    coords: np.ndarray
+    source_positions: np.ndarray
+    transform: ViewportTransform
+    active_channels: int = 2
+
+    def jacobian(self) -> np.ndarray:
+        dy, dx = np.gradient(self.coords, axis=(0, 1))
+        out = np.empty(self.coords.shape[:2] + (2, 2))
+        out[..., 0] = dx
+        out[..., 1] = dy
+        return out
+
+
+def field_gradient(fld: CoordinateField, x: int, y: int) -> np.ndarray:
+    """field.py:164-185."""
+    c = fld.coords
+
+    def diff(axis: int, idx: int, limit: int):
+        if 0 < idx < limit - 1:
+            lo, hi, scale = idx - 1, idx + 1, 0.5
+        else:
+            lo, hi, scale = max(idx - 1, 0), min(idx + 1, limit - 1), 1.0
+        if axis == 0:
+            return scale * (c[y, hi] - c[y, lo])
+        return scale * (c[hi, x] - c[lo, x])
+
+    out = np.empty((2, 2))
+    out[:, 0] = diff(0, x, fld.width)
+    out[:, 1] = diff(1, y, fld.height)
+    return out
+
+
+# ---------------------------------------------------------------------------
+# GPU evaluation
+
+
+_SNAP_WS: dict[int, torch.Tensor] = {}
+
+
+def _snap_workspace(nbytes: int, device: torch.device) -> torch.Tensor:
+    """Per-device scratch for mdc_mls_snap, kept all-0xFF between calls."""
+    key = device.index if device.index is not None else torch.cuda.current_device()
+    ws = _SNAP_WS.get(key)
+    if ws is None or ws.numel() < nbytes:
+        ws = torch.full((max(nbytes, 1),), 255, dtype=torch.uint8, device=device)
+        _SNAP_WS[key] = ws
+    return ws
+
+
+def _ldq(d: int, dtype: int, variant: int) -> int:
+    """Padded target row stride libmdc's stager needs (mirrors mls.cu)."""
+    es = 4 if dtype == _lib.MDC_F32 else 8
+    if variant == _lib.MDC_RIGID:
+        chunk = 2
+    else:
+        cap = 32 if dtype == _lib.MDC_F32 else 16
+        chunk = 1
+        while chunk < d and chunk < cap:
+            chunk *= 2
+    ld = -(-d // chunk) * chunk
+    vec = 16 // es
+    return -(-ld // vec) * vec
+
+
+@dataclass
+class FieldBlock:
+    """Result of ``compute_fields``: device tensors for rows [row0, row1)."""
+
+    values: torch.Tensor            # (d, rows, W) float32/float64
+    bands: torch.Tensor | None      # (d, rows, W) int32
+    transform: ViewportTransform
+    row0: int
+    row1: int
+    nonfinite: torch.Tensor         # () int32 device counter
+
+    def check_finite(self) -> None:
+        if int(self.nonfinite.item()) != 0:
+            raise FieldError("field evaluation produced non-finite coordinates")
+
+
+def _resolve_dtype(dtype) -> int:
+    if dtype in ("f32", "float32", torch.float32, np.float32):
+        return _lib.MDC_F32
+    if dtype in ("f64", "float64", torch.float64, np.float64):
+        return _lib.MDC_F64
+    raise ValueError(f"dtype must be f32 or f64, got {dtype!r}")
+
+
+class MlsProblem:
+    """Host-side set-up of one MLS evaluation (field.py:596-613), reusable
+    across row bands / repeated frames.  Controls live on the device."""
+
+    def __init__(self, positions, targets, variant: str, width: int, height: int,
+                 alpha=None, reg_eps=1e-12, epsilon_dist=None, dtype="f32", axis=None,
+                 device=None):
+        lib = _lib.require_cuda()
+        self.lib = lib
+        if variant not in ("mean", "affine", "rigid"):
+            raise ValueError(f"GPU MLS variant must be mean, affine or rigid, got {variant!r}")
+        positions = np.ascontiguousarray(positions, dtype=np.float64)
+        tvals = np.ascontiguousarray(targets, dtype=np.float64)
+        if tvals.ndim == 1:
+            tvals = tvals[:, None]
+        n, d = tvals.shape
+        if len(positions) != n:
+            raise ValueError("positions and targets disagree on the control count")
+        if variant == "rigid" and d != 2:
+            raise FieldError("rigid MLS needs exactly two target channels")
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        self.variant = variant
+        self.vcode = _lib.VARIANT_CODE[variant]
+        self.dcode = _resolve_dtype(dtype)
+        self.tdtype = torch.float32 if self.dcode == _lib.MDC_F32 else torch.float64
+        self.width, self.height, self.n, self.d = int(width), int(height), n, d
+        self.alpha = DEFAULT_ALPHA[variant] if alpha is None else float(alpha)
+        self.reg_eps = float(reg_eps)
+        self.transform = ViewportTransform.fit(positions, width, height)
+        sx, sy = self.transform.units_per_px
+        self.eps = epsilon_dist if epsilon_dist is not None else (0.25 * max(sx, sy)) ** 2
+        # field.py:607-610 -- identical numpy expressions
+        pm = positions.mean(axis=0)
+        qm = tvals.mean(axis=0)
+        pc = positions - pm
+        qc = tvals - qm
+        self.pm = pm
+        if variant == "mean":
+            ax = np.zeros(d, dtype=np.int32) if axis is None else np.asarray(axis, dtype=np.int32)
+            qk = qc - pc[:, ax]              # _kernels.py:52-67 dq = qc - pc
+        else:
+            ax = np.zeros(d, dtype=np.int32)
+            qk = qc
+        ldq = _ldq(d, self.dcode, self.vcode)
+        qpad = np.zeros((n, ldq), dtype=np.float32 if self.dcode == _lib.MDC_F32 else np.float64)
+        qpad[:, :d] = qk
+        dev = self.device
+        self.pc_t = torch.as_tensor(np.ascontiguousarray(pc)).to(dev)
+        self.q_t = torch.as_tensor(qpad).to(dev)
+        self.qm_t = torch.as_tensor(np.ascontiguousarray(qm)).to(dev)
+        self.axis_t = torch.as_tensor(ax).to(dev)
+        self.pos_t = torch.as_tensor(positions).to(dev)
+        self.tvals_t = torch.as_tensor(tvals).to(dev)
+        self.ldq = ldq
+
+    def args(self, out, out_strides, row0, row1, bands=None, band_strides=(0, 0), spacing=None,
+             nonfinite=None) -> _lib.MdcMlsArgs:
+        t = self.transform
+        sx, sy = t.units_per_px
+        a = _lib.MdcMlsArgs()
+        a.variant, a.dtype = self.vcode, self.dcode
+        a.width, a.height, a.row0, a.row1 = self.width, self.height, int(row0), int(row1)
+        a.n, a.d, a.ldq = self.n, self.d, self.ldq
+        a.x0, a.y1, a.sx, a.sy = t.x0, t.y1, sx, sy
+        a.pmx, a.pmy = float(self.pm[0]), float(self.pm[1])
+        a.alpha, a.reg_eps = self.alpha, self.reg_eps
+        a.pc, a.q, a.qm, a.axis = _lib.ptr(self.pc_t), _lib.ptr(self.q_t), _lib.ptr(self.qm_t), _lib.ptr(self.axis_t)
+        a.out = _lib.ptr(out)
+        a.out_cs, a.out_rs, a.out_ps = (int(s) for s in out_strides)
+        a.bands = _lib.ptr(bands)
+        a.band_cs, a.band_rs = (int(s) for s in band_strides)
+        a.spacing = _lib.ptr(spacing)
+        a.nonfinite = _lib.ptr(nonfinite)
+        return a
+
+    def run(self, a: _lib.MdcMlsArgs, snap: bool = True) -> None:
+        stream = _lib.stream_ptr()
+        _lib.check(self.lib.mdc_mls_field(ctypes.byref(a), stream), "mdc_mls_field")
+        if snap:
+            rows = a.row1 - a.row0
+            ws = _snap_workspace(int(self.lib.mdc_snap_workspace_bytes(self.width, rows)), self.device)
+            _lib.check(self.lib.mdc_mls_snap(ctypes.byref(a), _lib.ptr(self.pos_t), _lib.ptr(self.tvals_t),
+                                             ctypes.c_double(self.eps), _lib.ptr(ws), stream),
+                       "mdc_mls_snap")
+
+
+def compute_fields(positions, targets, params: MlsParams, width: int, height: int,
+                   row_range=None, dtype="f32", band_spacing=None, axis=None,
+                   problem: MlsProblem | None = None) -> FieldBlock:
+    """Fused d-channel MLS: every column of ``targets`` (n, d) is one field.
+
+    Channel k equals channel 0 of the reference's ``compute_field`` for the
+    single-dimension target (targets[:, k], 0) -- exactly what the reference
+    CLI renders once per dimension (cli.py:143-165) -- for mean and affine;
+    rigid takes d == 2 and matches the reference's two channels.
+    ``band_spacing`` (scalar or (d,)) fuses render._band_indices.
+    Returns a FieldBlock of device tensors (rows [row0, row1) only).
+    """
+    if params.variant == "linear":
+        raise FieldError("the linear variant is not on the GPU path yet (SURVEY.md §8f)")
+    prob = problem or MlsProblem(positions, targets, params.variant, width, height,
+                                 alpha=params.resolved_alpha, reg_eps=params.reg_eps,
+                                 epsilon_dist=params.epsilon_dist, dtype=dtype, axis=axis)
+    r0, r1 = (0, height) if row_range is None else (int(row_range[0]), int(row_range[1]))
+    rows = r1 - r0
+    dev = prob.device
+    out = torch.empty((prob.d, rows, width), dtype=prob.tdtype, device=dev)
+    bands = spacing_t = None
+    if band_spacing is not None:
+        sp = np.broadcast_to(np.asarray(band_spacing, dtype=np.float64), (prob.d,)).copy()
+        spacing_t = torch.as_tensor(sp).to(dev)
+        bands = torch.empty((prob.d, rows, width), dtype=torch.int32, device=dev)
+    nonfinite = torch.zeros((), dtype=torch.int32, device=dev)
+    a = prob.args(out, (rows * width, width, 1), r0, r1, bands, (rows * width, width), spacing_t, nonfinite)
+    prob.run(a)
+    return FieldBlock(values=out, bands=bands, transform=prob.transform, row0=r0, row1=r1,
+                      nonfinite=nonfinite)
+
+
+def compute_field(mesh, positions: np.ndarray, targets: TargetAssignment, params: MlsParams,
+                  width: int, height: int, threads: int = 1, dtype="f64") -> CoordinateField:
+    """field.py:582-659 on the GPU.  ``threads`` is accepted for signature
+    compatibility (the GPU result does not depend on it); ``dtype`` selects
+    the fp64 parity mode (default) or the fp32 throughput mode."""
+    if params.variant == "rigid" and targets.active_channels == 1:
+        raise FieldError("rigid MLS is degenerate for single-dimension targets; use mean or affine")
+    if params.variant == "linear":
+        raise FieldError("the linear variant is not on the GPU path yet (SURVEY.md §8f)")
+    positions = np.asarray(positions, dtype=np.float64)
+    tvals = targets.targets.astype(float)
+    prob = MlsProblem(positions, tvals, params.variant, width, height, alpha=params.resolved_alpha,
+                      reg_eps=params.reg_eps, epsilon_dist=params.epsilon_dist, dtype=dtype,
+                      axis=[0, 1])
+    out = torch.empty((height, width, 2), dtype=prob.tdtype, device=prob.device)
+    nonfinite = torch.zeros((), dtype=torch.int32, device=prob.device)
+    a = prob.args(out, (1, 2 * width, 2), 0, height, nonfinite=nonfinite)
+    prob.run(a)
+    coords = out.double().cpu().numpy()
+    if int(nonfinite.item()) != 0 or not np.all(np.isfinite(coords)):
+        raise FieldError("field evaluation produced non-finite coordinates")
+    return CoordinateField(width=width, height=height, coords=coords,
+                           source_positions=np.asarray(positions, dtype=float),
+                           transform=prob.transform, active_channels=targets.active_channels)
+
+
+MAGIC = b"MLSF"
+
+
+def write_field(fld: CoordinateField, path) -> None:
+    """field.py:665-670: magic, u32 width/height, row-major f64 (u, v) pairs."""
+    with open(path, "wb") as fh:
+        fh.write(MAGIC)
+        fh.write(struct.pack("<II", fld.width, fld.height))
+        fh.write(fld.coords.astype("<f8").tobytes())
+
+
+def read_field(path) -> tuple[int, int, np.ndarray]:
+    """field.py:673-679."""
+    with open(path, "rb") as fh:
+        if fh.read(4) != MAGIC:
+            raise FieldError(f"{path}: not a field raster")
+        w, h = struct.unpack("<II", fh.read(8))
+        data = np.frombuffer(fh.read(), dtype="<f8").reshape(h, w, 2)
+    return w, h, data

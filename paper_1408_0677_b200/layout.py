@@ -1,0 +1,257 @@
+"""Planarity-preserving force-directed layout on the GPU.
+
+Drop-in mirror of the reference's ``layout`` module
+(/root/reference/pkg/src/mdcontour/layout.py): ``LayoutParams`` /
+``defaults_for`` / ``LayoutState`` / ``initial_state`` / ``layout_step`` /
+``layout_run`` / ``interpolate_layout`` / ``count_orientation_flips`` keep
+their signatures, defaults and errors.  Each Jacobi step runs in libmdc
+(kd-tree build + warp-cooperative Barnes-Hut + one fused per-vertex
+spring/node-edge/cap/clamp/update kernel, positions double-buffered in HBM);
+``layout_run`` replays a captured CUDA graph per step and moves positions
+across PCIe once per run, not once per step.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .mesh import layout_topology
+
+
+class TOutOfRange(Exception):
+    pass
+
+
+@dataclass(frozen=True)
+class LayoutParams:
+    """layout.py:26-67."""
+
+    repulsion_c: float
+    spring_scale: float
+    desired_edge_d: float
+    softening_eta: float
+    initial_temp: float
+    decay_lambda: float
+    iterations: int = 500
+    bh_theta: float = 0.5
+
+    def __post_init__(self):
+        if self.repulsion_c <= 0 or self.spring_scale <= 0 or self.desired_edge_d <= 0:
+            raise ValueError("force constants must be positive")
+        if self.softening_eta <= 0 or self.initial_temp <= 0 or self.bh_theta <= 0:
+            raise ValueError("softening, temperature, and opening angle must be positive")
+        if not 0.0 < self.decay_lambda < 1.0:
+            raise ValueError("decay_lambda must lie in (0, 1)")
+        if self.iterations < 0:
+            raise ValueError("iterations must be non-negative")
+
+    @classmethod
+    def defaults_for(cls, mesh, iterations: int = 500, **overrides) -> "LayoutParams":
+        d = median_edge_length(mesh)
+        base = dict(
+            repulsion_c=d * d,
+            spring_scale=1.0,
+            desired_edge_d=d,
+            softening_eta=1e-7 * d,
+            initial_temp=d,
+            decay_lambda=0.99,
+            iterations=iterations,
+            bh_theta=0.5,
+        )
+        base.update(overrides)
+        return cls(**base)
+
+
+def median_edge_length(mesh, positions: np.ndarray | None = None) -> float:
+    """layout.py:70-76."""
+    pos = mesh.original_pos if positions is None else positions
+    src = np.repeat(np.arange(mesh.node_count), np.diff(mesh.csr_offsets))
+    dst = mesh.csr_targets
+    keep = src < dst
+    lengths = np.hypot(*(pos[src[keep]] - pos[dst[keep]]).T)
+    return float(np.median(lengths)) if len(lengths) else 1.0
+
+
+@dataclass(frozen=True)
+class LayoutState:
+    mesh: object
+    iteration: int
+    temperature: float
+    relaxed_pos: np.ndarray
+
+
+def temperature_schedule(t0: float, lam: float, k: int) -> np.ndarray:
+    """t_i for i = 0..k-1 by repeated multiplication, exactly as the
+    reference advances ``state.temperature * decay_lambda`` (layout.py:284)."""
+    out = np.empty(k)
+    t = t0
+    for i in range(k):
+        out[i] = t
+        t = t * lam
+    return out
+
+
+LEAF_SIZE = 32  # bhtree.py:74 passes leaf_size=32 on the layout path
+
+
+class LayoutEngine:
+    """Device-resident topology + libmdc plan for one mesh and parameter set."""
+
+    def __init__(self, mesh, params: LayoutParams, device=None, leaf: int = LEAF_SIZE):
+        lib = _lib.require_cuda()
+        self.lib = lib
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        self.params = params
+        self.n = int(mesh.node_count)
+        topo = layout_topology(mesh)
+        dev = self.device
+        self.topo = {k: torch.as_tensor(v).to(dev) for k, v in topo.items()}
+        self.ntri = int(topo["tris"].shape[0])
+        self.pos = torch.empty((self.n, 2), dtype=torch.float64, device=dev)
+        self.ws = torch.empty(int(lib.mdc_layout_workspace_bytes(self.n, leaf)), dtype=torch.uint8, device=dev)
+        self.leaf = leaf
+        self._plans = {}
+        self.temps = None
+
+    def _args(self, dbg=None) -> _lib.MdcLayoutArgs:
+        p = self.params
+        a = _lib.MdcLayoutArgs()
+        a.n, a.ntri, a.leaf = self.n, self.ntri, self.leaf
+        a.c, a.spring, a.dlen = p.repulsion_c, p.spring_scale, p.desired_edge_d
+        a.eta, a.theta = p.softening_eta, p.bh_theta
+        a.csr_off, a.csr_tgt = _lib.ptr(self.topo["csr_off"]), _lib.ptr(self.topo["csr_tgt"])
+        a.tris, a.inc_off, a.inc = _lib.ptr(self.topo["tris"]), _lib.ptr(self.topo["inc_off"]), _lib.ptr(self.topo["inc"])
+        a.pos = _lib.ptr(self.pos)
+        a.workspace, a.workspace_bytes = _lib.ptr(self.ws), self.ws.numel()
+        if dbg is not None:
+            a.dbg_bh, a.dbg_force, a.dbg_scale = (_lib.ptr(t) for t in dbg)
+        return a
+
+    def plan(self, debug: bool = False):
+        key = "dbg" if debug else "run"
+        if key not in self._plans:
+            dbg = None
+            if debug:
+                self.dbg = (torch.empty((self.n, 2), dtype=torch.float64, device=self.device),
+                            torch.empty((self.n, 2), dtype=torch.float64, device=self.device),
+                            torch.empty(self.n, dtype=torch.float64, device=self.device))
+                dbg = self.dbg
+            self._args_keep = a = self._args(dbg)
+            h = ctypes.c_void_p()
+            _lib.check(self.lib.mdc_layout_plan_create(ctypes.byref(a), ctypes.byref(h), _lib.stream_ptr()),
+                       "mdc_layout_plan_create")
+            self._plans[key] = h
+        return self._plans[key]
+
+    def set_positions(self, pos) -> None:
+        self.pos.copy_(torch.as_tensor(np.ascontiguousarray(pos, dtype=np.float64)))
+
+    def run(self, temps: np.ndarray, use_graph: bool = True, debug: bool = False) -> None:
+        """len(temps) steps in place on ``self.pos`` (device)."""
+        k = len(temps)
+        if k == 0:
+            return
+        if self.temps is None or self.temps.numel() < k or debug:
+            self.temps = torch.as_tensor(np.asarray(temps, dtype=np.float64)).to(self.device)
+            # captured graphs bind the temps pointer: drop them with the buffer
+            self._drop("run")
+        else:
+            self.temps[:k].copy_(torch.as_tensor(np.asarray(temps, dtype=np.float64)))
+        h = self.plan(debug)
+        _lib.check(self.lib.mdc_layout_steps(h, k, _lib.ptr(self.temps), int(use_graph and not debug),
+                                             _lib.stream_ptr()), "mdc_layout_steps")
+
+    def repulsion(self, pts: torch.Tensor) -> torch.Tensor:
+        out = torch.empty_like(pts)
+        _lib.check(self.lib.mdc_layout_repulsion(self.plan(), _lib.ptr(pts), _lib.ptr(out), _lib.stream_ptr()),
+                   "mdc_layout_repulsion")
+        return out
+
+    def _drop(self, key):
+        h = self._plans.pop(key, None)
+        if h is not None:
+            self.lib.mdc_layout_plan_destroy(h)
+
+    def __del__(self):
+        try:
+            for key in list(self._plans):
+                self._drop(key)
+        except Exception:
+            pass
+
+
+def _engine(mesh, params: LayoutParams) -> LayoutEngine:
+    """One engine per (mesh, params), cached on the mesh like the reference
+    caches its constraint grouping (layout.py:270-273)."""
+    cache = mesh.__dict__.setdefault("_mdc_layout_engines", {})
+    key = (params.repulsion_c, params.spring_scale, params.desired_edge_d, params.softening_eta,
+           params.bh_theta, torch.cuda.current_device())
+    eng = cache.get(key)
+    if eng is None:
+        eng = LayoutEngine(mesh, params)
+        cache[key] = eng
+    return eng
+
+
+def initial_state(mesh, params: LayoutParams) -> LayoutState:
+    return LayoutState(mesh=mesh, iteration=0, temperature=params.initial_temp,
+                       relaxed_pos=mesh.current_pos.copy())
+
+
+def layout_step(state: LayoutState, params: LayoutParams) -> LayoutState:
+    """layout.py:266-286: one synchronous annealed update from a frozen snapshot."""
+    mesh = state.mesh
+    eng = _engine(mesh, params)
+    eng.set_positions(mesh.current_pos)
+    eng.run(np.array([state.temperature]), use_graph=False)
+    mesh.current_pos = eng.pos.cpu().numpy()
+    return LayoutState(mesh=mesh, iteration=state.iteration + 1,
+                       temperature=state.temperature * params.decay_lambda,
+                       relaxed_pos=mesh.current_pos.copy())
+
+
+def layout_run(mesh, params: LayoutParams) -> LayoutState:
+    """layout.py:298-302: ``params.iterations`` steps, device-resident."""
+    state = initial_state(mesh, params)
+    k = params.iterations
+    if k == 0:
+        return state
+    temps = temperature_schedule(state.temperature, params.decay_lambda, k + 1)
+    eng = _engine(mesh, params)
+    eng.set_positions(mesh.current_pos)
+    eng.run(temps[:k], use_graph=True)
+    mesh.current_pos = eng.pos.cpu().numpy()
+    return LayoutState(mesh=mesh, iteration=k, temperature=float(temps[k]),
+                       relaxed_pos=mesh.current_pos.copy())
+
+
+def layout_debug_step(mesh, pos: np.ndarray, params: LayoutParams, temperature: float):
+    """One step from ``pos`` returning (new_pos, bh, total_force, clamp_s) --
+    the per-component teacher-forced parity hook (layout.py:259-280)."""
+    eng = _engine(mesh, params)
+    eng.set_positions(pos)
+    eng.run(np.array([temperature]), use_graph=False, debug=True)
+    bh, force, s = (t.cpu().numpy() for t in eng.dbg)
+    return eng.pos.cpu().numpy(), bh, force, s
+
+
+def interpolate_layout(state: LayoutState, t: float) -> np.ndarray:
+    """layout.py:305-309."""
+    if not 0.0 <= t <= 1.0:
+        raise TOutOfRange(f"relax parameter must be in [0, 1], got {t}")
+    return (1.0 - t) * state.mesh.original_pos + t * state.relaxed_pos
+
+
+def count_orientation_flips(mesh, positions: np.ndarray) -> int:
+    """layout.py:312-320."""
+    def areas(p):
+        a, b, c = p[mesh.triangles[:, 0]], p[mesh.triangles[:, 1]], p[mesh.triangles[:, 2]]
+        return 0.5 * ((b[:, 0] - a[:, 0]) * (c[:, 1] - a[:, 1]) - (b[:, 1] - a[:, 1]) * (c[:, 0] - a[:, 0]))
+    ref = np.sign(areas(mesh.original_pos))
+    cur = np.sign(areas(positions))
+    return int(np.count_nonzero(ref != cur))

@@ -1,0 +1,244 @@
+"""Triangle-mesh container (CSR + anchored fans) and the layout topology.
+
+``TriMesh`` mirrors the reference's arrays (mesh.py:107-128) so meshes built
+by either package drop into ``layout_step`` / ``compute_field``.  Mesh
+CONSTRUCTION is outside the GPU hot path: the
+``delaunay`` here triangulates with scipy's Qhull and canonicalises exactly
+like the reference's ``_assemble`` (mesh.py:362-416), which yields the same
+arrays as the reference's Bowyer-Watson for points in general position
+(checked against the reference's own meshes in tests/test_mesh.py).
+
+``layout_topology`` derives the int32 device-side topology the layout kernels
+consume (CSR, padded triangles, per-vertex incident (triangle, corner) lists
+in the per-corner bincount order of layout.py:240-255).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+
+class MeshError(Exception):
+    pass
+
+
+class DegenerateInput(MeshError):
+    """All input points collinear: no triangulation exists."""
+
+
+class ZeroAreaTriangle(MeshError):
+    pass
+
+
+def signed_area(a, b, c) -> float:
+    """mesh.py:33-35."""
+    return 0.5 * ((b[0] - a[0]) * (c[1] - a[1]) - (b[1] - a[1]) * (c[0] - a[0]))
+
+
+def limiting_lines(tri, positions):
+    """mesh.py:82-104: midsegment line (point, inward unit normal) per vertex."""
+    a, b, c = (np.asarray(positions[i], dtype=float) for i in tri)
+    if signed_area(a, b, c) == 0.0:
+        raise ZeroAreaTriangle(f"triangle {tuple(tri)} has zero area")
+    verts = (a, b, c)
+    out = []
+    for k in range(3):
+        v = verts[k]
+        m1 = 0.5 * (v + verts[(k + 1) % 3])
+        m2 = 0.5 * (v + verts[(k + 2) % 3])
+        d = m2 - m1
+        n = np.array([-d[1], d[0]])
+        n /= np.linalg.norm(n)
+        if np.dot(n, v - m1) < 0:
+            n = -n
+        out.append((m1, n))
+    return out
+
+
+@dataclass
+class TriMesh:
+    """mesh.py:107-128 field-for-field."""
+
+    node_count: int
+    original_pos: np.ndarray
+    current_pos: np.ndarray
+    csr_offsets: np.ndarray
+    csr_targets: np.ndarray
+    fan_offsets: np.ndarray
+    fan_nodes: np.ndarray
+    triangles: np.ndarray
+    jitter_count: int = 0
+
+    @property
+    def edge_count(self) -> int:
+        return len(self.csr_targets) // 2
+
+    @property
+    def triangle_count(self) -> int:
+        return len(self.triangles)
+
+    def neighbors(self, i: int) -> np.ndarray:
+        return self.csr_targets[self.csr_offsets[i]: self.csr_offsets[i + 1]]
+
+    def signed_areas(self, positions: np.ndarray | None = None) -> np.ndarray:
+        """mesh.py:178-187."""
+        p = self.current_pos if positions is None else positions
+        a = p[self.triangles[:, 0]]
+        b = p[self.triangles[:, 1]]
+        c = p[self.triangles[:, 2]]
+        return 0.5 * ((b[:, 0] - a[:, 0]) * (c[:, 1] - a[:, 1])
+                      - (b[:, 1] - a[:, 1]) * (c[:, 0] - a[:, 0]))
+
+    def hull_nodes(self) -> np.ndarray:
+        e = np.sort(np.concatenate([self.triangles[:, [0, 1]], self.triangles[:, [1, 2]],
+                                    self.triangles[:, [2, 0]]]), axis=1)
+        uniq, cnt = np.unique(e, axis=0, return_counts=True)
+        return np.unique(uniq[cnt == 1].ravel()).astype(np.int64)
+
+
+def assemble(original: np.ndarray, current: np.ndarray, tris: np.ndarray, jitter_count: int = 0) -> TriMesh:
+    """Vectorised restatement of mesh.py:362-416 `_assemble`.
+
+    Canonical triangle order (smallest vertex first, lexsorted), CSR
+    neighbours sorted counter-clockwise by angle at ``original`` (ties by
+    index), fans anchored at each triangle's smallest vertex.
+    """
+    n = len(original)
+    tris = np.asarray(tris, dtype=np.int64).reshape(-1, 3)
+    a, b, c = tris[:, 0], tris[:, 1], tris[:, 2]
+    rot0 = (a <= b) & (a <= c)
+    rot1 = ~rot0 & (b <= a) & (b <= c)
+    canon = np.where(rot0[:, None], tris,
+                     np.where(rot1[:, None], tris[:, [1, 2, 0]], tris[:, [2, 0, 1]]))
+    canon = canon[np.lexsort((canon[:, 2], canon[:, 1], canon[:, 0]))]
+
+    src = np.concatenate([canon[:, 0], canon[:, 0], canon[:, 1], canon[:, 1], canon[:, 2], canon[:, 2]])
+    dst = np.concatenate([canon[:, 1], canon[:, 2], canon[:, 0], canon[:, 2], canon[:, 0], canon[:, 1]])
+    pairs = np.unique(np.stack([src, dst], axis=1), axis=0)
+    src, dst = pairs[:, 0], pairs[:, 1]
+    d = original[dst] - original[src]
+    ang = np.arctan2(d[:, 1], d[:, 0])
+    order = np.lexsort((dst, ang, src))
+    src, dst = src[order], dst[order]
+    csr_offsets = np.zeros(n + 1, dtype=np.int64)
+    np.add.at(csr_offsets, src + 1, 1)
+    csr_offsets = np.cumsum(csr_offsets)
+    csr_targets = dst.astype(np.int64)
+
+    # position of every (i, j) in i's CSR run, for the fan ordering
+    rank = np.arange(len(src)) - csr_offsets[src]
+    key = src * np.int64(n) + dst
+    korder = np.argsort(key)
+    ksorted = key[korder]
+
+    def csr_rank(i, j):
+        return rank[korder[np.searchsorted(ksorted, i * np.int64(n) + j)]]
+
+    anchors, firsts = canon[:, 0], canon[:, 1]
+    fo = np.lexsort((csr_rank(anchors, firsts), anchors))
+    fan_nodes = firsts[fo].astype(np.int64)
+    fan_offsets = np.zeros(n + 1, dtype=np.int64)
+    np.add.at(fan_offsets, anchors + 1, 1)
+    fan_offsets = np.cumsum(fan_offsets)
+    return TriMesh(node_count=n, original_pos=original, current_pos=current,
+                   csr_offsets=csr_offsets, csr_targets=csr_targets, fan_offsets=fan_offsets,
+                   fan_nodes=fan_nodes, triangles=canon.astype(np.int64), jitter_count=jitter_count)
+
+
+def _jitter_duplicates(points: np.ndarray, diag: float, rng: np.random.Generator):
+    """mesh.py:336-359: split near-coincident points with a seeded jitter."""
+    pts = points.copy()
+    tol = 1e-9 * diag
+    amp = 1e-6 * diag
+    moved = 0
+    for _ in range(16):
+        cells: dict[tuple[int, int], int] = {}
+        dup = []
+        for i, (x, y) in enumerate(pts):
+            key = (int(round(x / tol)), int(round(y / tol)))
+            if key in cells:
+                dup.append(i)
+            else:
+                cells[key] = i
+        if not dup:
+            break
+        for i in dup:
+            ang = rng.uniform(0.0, 2.0 * np.pi)
+            r = amp * (0.5 + 0.5 * rng.uniform())
+            pts[i, 0] += r * np.cos(ang)
+            pts[i, 1] += r * np.sin(ang)
+        moved += len(dup)
+    return pts, moved
+
+
+def delaunay(points, seed: int = 0, viewport=None) -> TriMesh:
+    """Delaunay triangulation into a TriMesh (signature of mesh.py:419).
+
+    Preprocessing mirrors the reference (jitter of coincident points,
+    collinearity check); the triangulation itself comes from Qhull.
+    """
+    from scipy.spatial import Delaunay
+
+    if hasattr(points, "positions"):
+        viewport = viewport or points.viewport
+        points = points.positions
+    pts = np.ascontiguousarray(points, dtype=np.float64)
+    if pts.ndim != 2 or pts.shape[1] != 2:
+        raise MeshError("expected an (n, 2) point array")
+    n = len(pts)
+    if n < 3:
+        raise DegenerateInput(f"need at least 3 points, got {n}")
+    if viewport is None:
+        lo, hi = pts.min(axis=0), pts.max(axis=0)
+        ext = np.where(hi > lo, hi - lo, 1.0)
+        diag = float(np.hypot(*(1.1 * ext)))
+    else:
+        diag = float(np.hypot(viewport[2] - viewport[0], viewport[3] - viewport[1]))
+    rng = np.random.default_rng(seed)
+    pts, jitter_count = _jitter_duplicates(pts, diag, rng)
+    d = pts - pts[0]
+    j = int(np.argmax(np.hypot(d[:, 0], d[:, 1])))
+    e = pts[j] - pts[0]
+    if not np.any(e[0] * d[:, 1] - e[1] * d[:, 0]):
+        raise DegenerateInput("all points are collinear")
+    simp = Delaunay(pts).simplices.astype(np.int64)
+    p = pts[simp]
+    area = (p[:, 1, 0] - p[:, 0, 0]) * (p[:, 2, 1] - p[:, 0, 1]) - (p[:, 1, 1] - p[:, 0, 1]) * (p[:, 2, 0] - p[:, 0, 0])
+    simp = np.where((area < 0)[:, None], simp[:, [0, 2, 1]], simp)
+    simp = simp[area != 0]
+    return assemble(pts.copy(), pts.copy(), simp, jitter_count)
+
+
+def layout_topology(mesh) -> dict[str, np.ndarray]:
+    """int32 device topology for the layout kernels.
+
+    csr_off/csr_tgt: the mesh CSR (layout.py:216-231 sums in this order).
+    tris: (T, 4) int32, column 3 padding (16-byte rows).
+    inc_off/inc: per vertex, entries ``triangle << 2 | corner`` sorted by
+    (corner, triangle) == the order in which np.bincount accumulates each
+    corner pass of layout.py:240-255.
+    """
+    n = int(mesh.node_count)
+    tris = np.asarray(mesh.triangles, dtype=np.int64).reshape(-1, 3)
+    t = len(tris)
+    if n >= 2**31 or t >= 2**29:
+        raise MeshError("mesh too large for int32 topology")
+    tri4 = np.zeros((t, 4), dtype=np.int32)
+    tri4[:, :3] = tris
+    vert = tris.T.ravel()                        # corner-major: k*T + t
+    corner = np.repeat(np.arange(3), t)
+    tidx = np.tile(np.arange(t), 3)
+    order = np.lexsort((tidx, corner, vert))     # by vertex, then corner, then triangle
+    inc = ((tidx[order] << 2) | corner[order]).astype(np.int32)
+    inc_off = np.zeros(n + 1, dtype=np.int64)
+    np.add.at(inc_off, vert + 1, 1)
+    inc_off = np.cumsum(inc_off).astype(np.int32)
+    return dict(
+        csr_off=np.asarray(mesh.csr_offsets, dtype=np.int32),
+        csr_tgt=np.asarray(mesh.csr_targets, dtype=np.int32),
+        tris=tri4,
+        inc_off=inc_off,
+        inc=inc,
+    )

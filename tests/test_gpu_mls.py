@@ -1,0 +1,136 @@
+"""MLS field parity on the GPU against the reference's own fields (golden)
+and the CPU oracle.  Tolerances are the north-star contract:
+fp64 <= 1e-10 normwise, fp32 <= 1e-4 normwise, snapped pixels exact, bands
+bit-exact except within eps of a band boundary."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from conftest import normwise
+from helpers import golden_mesh
+
+from paper_1408_0677_b200 import field as F
+
+pytestmark = pytest.mark.gpu
+
+FP64_TOL = 1e-10
+FP32_TOL = 1e-4
+
+
+def _targets(c1, name):
+    tv = c1[f"targets_{name}"]
+    ch = int(c1[f"channels_{name}"])
+    mode = "dims" if name.startswith(("affine_dim", "mean_dim", "rigid_dims", "affine_dims")) else "projection"
+    dims = ("a",) if ch == 1 else (("a", "b") if mode == "dims" else ())
+    return F.TargetAssignment(targets=tv, mode=mode, dims=dims)
+
+
+@pytest.mark.parametrize("dtype,tol", [("f64", FP64_TOL), ("f32", FP32_TOL)])
+def test_compute_field_matches_reference_fields(c1, dtype, tol):
+    m = golden_mesh(c1)
+    pos = c1["field_positions"]
+    W, H = (int(v) for v in c1["field_wh"])
+    worst = {}
+    for name, var, a in zip(c1["field_cases"], c1["field_variants"], c1["field_alphas"]):
+        params = F.MlsParams(variant=str(var), alpha=None if np.isnan(a) else float(a))
+        fld = F.compute_field(m, pos, _targets(c1, name), params, W, H, dtype=dtype)
+        ref = c1[f"field_{name}"]
+        ch = 2
+        errs = [normwise(fld.coords[..., k], ref[..., k]) for k in range(ch) if np.abs(ref[..., k]).max() > 0]
+        worst[name] = max(errs)
+    bad = {k: v for k, v in worst.items() if v > tol}
+    assert not bad, (dtype, bad)
+
+
+def test_snap_pixels_exact(c1):
+    pos = c1["field_positions"]
+    W, H = (int(v) for v in c1["field_wh"])
+    # enlarge the snap radius so many pixels snap; oracle = reference restatement
+    tv = c1["targets_affine_proj"]
+    eps = (2.0 * max(F.ViewportTransform.fit(pos, W, H).units_per_px)) ** 2
+    fld = F.compute_field(golden_mesh(c1), pos, F.TargetAssignment(tv, "projection"),
+                          F.MlsParams(variant="affine", epsilon_dist=eps), W, H)
+    ref = O.compute_field(pos, tv, "affine", W, H, epsilon_dist=eps)
+    # snapped pixels equal exact targets: find them in the oracle output
+    snapped = np.zeros((H, W), bool)
+    for q in tv:
+        snapped |= np.all(ref == q, axis=-1)
+    assert snapped.sum() > 20
+    assert np.array_equal(fld.coords[snapped], ref[snapped])
+    assert normwise(fld.coords, ref) <= FP64_TOL
+
+
+def test_fused_channels_match_per_dim_reference(c1):
+    """compute_fields channel k == reference channel 0 for target (q_k, 0)."""
+    pos = c1["field_positions"]
+    W, H = (int(v) for v in c1["field_wh"])
+    raw = c1["raw"]
+    spacing = np.array([float(c1[f"spacing_affine_dim{k}"]) for k in range(4)])
+    for dtype, tol in (("f64", FP64_TOL), ("f32", FP32_TOL)):
+        blk = F.compute_fields(pos, raw, F.MlsParams("affine"), W, H, dtype=dtype, band_spacing=spacing)
+        blk.check_finite()
+        vals = blk.values.double().cpu().numpy()
+        bands = blk.bands.cpu().numpy()
+        for k in range(4):
+            ref = c1[f"field_affine_dim{k}"][..., 0]
+            assert normwise(vals[k], ref) <= tol, (dtype, k)
+            refb = c1[f"bands_affine_dim{k}"]
+            frac = np.abs(ref / spacing[k] - np.round(ref / spacing[k]))
+            ok = frac > (1e-4 if dtype == "f32" else 1e-9)
+            assert np.array_equal(bands[k][ok], refb[ok]), (dtype, k)
+
+
+def test_fused_mean_channels(c1):
+    pos = c1["field_positions"]
+    W, H = (int(v) for v in c1["field_wh"])
+    blk = F.compute_fields(pos, c1["raw"][:, :1], F.MlsParams("mean"), W, H, dtype="f64")
+    assert normwise(blk.values[0].cpu().numpy(), c1["field_mean_dim0"][..., 0]) <= FP64_TOL
+
+
+def test_row_bands_are_bit_identical_to_full_frame(c1):
+    pos = c1["field_positions"]
+    W, H = (int(v) for v in c1["field_wh"])
+    raw = c1["raw"]
+    full = F.compute_fields(pos, raw, F.MlsParams("affine"), W, H, dtype="f32").values.cpu()
+    parts = []
+    for r0, r1 in ((0, 7), (7, 30), (30, H)):
+        parts.append(F.compute_fields(pos, raw, F.MlsParams("affine"), W, H, dtype="f32",
+                                      row_range=(r0, r1)).values.cpu())
+    assert torch.equal(torch.cat(parts, dim=1), full)
+
+
+def test_deterministic_repeat(c1):
+    pos = c1["field_positions"]
+    W, H = (int(v) for v in c1["field_wh"])
+    a = F.compute_fields(pos, c1["raw"], F.MlsParams("affine"), W, H, dtype="f32").values
+    b = F.compute_fields(pos, c1["raw"], F.MlsParams("affine"), W, H, dtype="f32").values
+    assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("n,d,W,H,alpha", [(2000, 8, 96, 64, 1.5), (3000, 33, 80, 50, 1.5),
+                                           (1500, 5, 64, 64, 1.3), (2500, 3, 70, 40, 1.0)])
+def test_fused_vs_oracle_larger(n, d, W, H, alpha):
+    rng = np.random.default_rng(n + d)
+    pos = rng.normal(0, 3, (n, 2))
+    q = rng.normal(0, 1, (n, d)) + pos[:, :1] * np.arange(d)
+    blk = F.compute_fields(pos, q, F.MlsParams("affine", alpha=alpha), W, H, dtype="f32")
+    blk.check_finite()
+    vals = blk.values.double().cpu().numpy()
+    for k in range(0, d, max(1, d // 4)):
+        tv = np.column_stack([q[:, k], np.zeros(n)])
+        ref = O.compute_field(pos, tv, "affine", W, H, alpha=alpha)[..., 0]
+        assert normwise(vals[k], ref) <= FP32_TOL, k
+
+
+def test_rigid_single_channel_rejected(c1):
+    tv = F.TargetAssignment(targets=c1["targets_affine_dim0"], mode="dims", dims=("a",))
+    with pytest.raises(F.FieldError):
+        F.compute_field(golden_mesh(c1), c1["field_positions"], tv, F.MlsParams("rigid"), 20, 20)
+
+
+def test_g2k_field(g2k):
+    W, H = 40, 30
+    tv = F.TargetAssignment(g2k["targets_affine_dim0"], "dims", ("a",))
+    fld = F.compute_field(golden_mesh(g2k), g2k["field_positions"], tv, F.MlsParams("affine"), W, H)
+    assert normwise(fld.coords[..., 0], g2k["field_affine_dim0"][..., 0]) <= FP64_TOL
