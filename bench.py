@@ -237,6 +237,8 @@ def main():
     ap.add_argument("--no-layout", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--frame", default=None, help="override the raster, WxH (profiling only)")
+    ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -245,6 +247,8 @@ def main():
     cfg = dict(CONFIGS[args.config], id=args.config)
     if args.layout_iters is not None:
         cfg["iters"] = args.layout_iters
+    if args.frame:
+        cfg["W"], cfg["H"] = (int(v) for v in args.frame.lower().split("x"))
 
     if args.impl == "reference":
         run_reference(args, cfg, rank)
@@ -358,37 +362,7 @@ def main():
         raise RuntimeError("non-finite field values")
 
     # ---- e2e through the public API (host buffers in, field out) -----------
-    e2e = None
-    pin_pos = torch.from_numpy(np.ascontiguousarray(positions)).pin_memory()
-    pin_raw = torch.from_numpy(np.ascontiguousarray(raw)).pin_memory()
-    host_out = torch.empty((d, rows, W), dtype=torch.float32).pin_memory()
-    mp = F.MlsParams("affine")
-    ne = max(1, min(args.steps, 3))
-
-    def e2e_step():
-        blk = F.compute_fields(pin_pos.numpy(), pin_raw.numpy(), mp, W, H, row_range=(r0, r1),
-                               dtype="f32", band_spacing=spacing)
-        host_out.copy_(blk.values, non_blocking=True)
-        torch.cuda.current_stream().synchronize()
-        return blk
-
-    blk = e2e_step()
-    blk_prob_tensors = _problem_tensors(positions, raw, W, H)
-    h2d = sum(t.numel() * t.element_size() for t in blk_prob_tensors)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    c0 = time.perf_counter()
-    for _ in range(ne):
-        e2e_step()
-    c1 = time.perf_counter()
-    e_ms = torch.tensor([(c1 - c0) * 1e3 / ne], device=dev)
-    if world > 1:
-        dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
-    e2e = {"value": W * H * d / (e_ms.item() * 1e-3) / 1e6, "unit": UNIT,
-           "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(host_out.numel() * 4),
-           "ms_per_step": e_ms.item()}
-    del blk_prob_tensors
+    e2e = None if args.no_e2e else run_e2e(args, positions, raw, spacing, W, H, d, r0, r1, dev, world)
 
     if rank != 0:
         if world > 1:
@@ -398,13 +372,17 @@ def main():
     # ---- roofline of the dominant kernel --------------------------------
     peaks = measure_peaks(lib, torch)
     pairs = rows * W * cfg["n"]
+    dc = 1
+    while dc < d and dc < 32:
+        dc *= 2
+    chunks = -(-d // dc)
     alg_flops = pairs * (19 + 6 * d)               # SURVEY.md §8d per-pair figure
-    exec_flops = pairs * (30 + 2 * d)              # what the two-pass kernel executes
+    exec_flops = pairs * (18 + 12 * chunks + 2 * d)  # what the two-pass kernel executes
     achieved = alg_flops / (kernel_ms * 1e-3) / 1e12
     peak = peaks["fp32"] / 1e12
     roofline = {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak, "traffic": None,
-                "kernel": "mls_kernel<float, AFFINE, alpha=1.5, DC=32, R=2>",
+                "kernel": f"mls_kernel<float, AFFINE, alpha=1.5, DC={dc}, R=2>",
                 "kernel_ms": kernel_ms, "peak_source": "measured FFMA microbenchmark (mdc_peak_ffma), this run",
                 "executed_tflops": exec_flops / (kernel_ms * 1e-3) / 1e12,
                 "executed_frac": exec_flops / (kernel_ms * 1e-3) / peaks["fp32"],
@@ -437,12 +415,43 @@ def main():
         dist.destroy_process_group()
 
 
-def _problem_tensors(positions, raw, W, H):
-    """The host->device tensors compute_fields uploads per call (for byte counts)."""
-    from paper_1408_0677_b200.field import MlsProblem
+def run_e2e(args, positions, raw, spacing, W, H, d, r0, r1, dev, world):
+    """The same frame through the public API: pinned host inputs -> H2D ->
+    kernels -> D2H of the fp32 field, every step."""
+    import torch
+    import torch.distributed as dist
 
-    p = MlsProblem(positions, raw, "affine", W, H, dtype="f32")
-    return [p.pc_t, p.q_t, p.qm_t, p.axis_t, p.pos_t, p.tvals_t]
+    from paper_1408_0677_b200 import field as F
+
+    rows = r1 - r0
+    pin_pos = torch.from_numpy(np.ascontiguousarray(positions)).pin_memory()
+    pin_raw = torch.from_numpy(np.ascontiguousarray(raw)).pin_memory()
+    host_out = torch.empty((d, rows, W), dtype=torch.float32).pin_memory()
+    mp = F.MlsParams("affine")
+    ne = max(1, min(args.steps, 3))
+    h2d = [0]
+
+    def e2e_step():
+        blk = F.compute_fields(pin_pos.numpy(), pin_raw.numpy(), mp, W, H, row_range=(r0, r1),
+                               dtype="f32", band_spacing=spacing)
+        host_out.copy_(blk.values, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        h2d[0] = blk.h2d_bytes
+
+    e2e_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    c0 = time.perf_counter()
+    for _ in range(ne):
+        e2e_step()
+    c1 = time.perf_counter()
+    e_ms = torch.tensor([(c1 - c0) * 1e3 / ne], device=dev)
+    if world > 1:
+        dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+    return {"value": W * H * d / (e_ms.item() * 1e-3) / 1e6, "unit": UNIT,
+            "h2d_bytes_per_step": int(h2d[0]), "d2h_bytes_per_step": int(host_out.numel() * 4),
+            "ms_per_step": e_ms.item(), "timing": "wall clock, synchronized, max over ranks"}
 
 
 def _auto_spacing(values):

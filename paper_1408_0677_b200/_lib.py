@@ -13,7 +13,7 @@ import os
 import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmdc.so")
+LIB_PATH = os.environ.get("MDC_LIB_PATH") or os.path.join(HERE, "libmdc.so")  # override: A/B experiments only
 
 MDC_MEAN, MDC_AFFINE, MDC_RIGID = 1, 2, 3
 MDC_F32, MDC_F64 = 0, 1

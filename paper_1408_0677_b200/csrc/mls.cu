@@ -100,6 +100,9 @@ __device__ __forceinline__ double weight(double d2, double neg_alpha) {
 
 // ---- tiling --------------------------------------------------------------
 constexpr int NT = 256;  // threads per CTA == controls per shared-memory tile
+#ifndef MDC_MLS_MINB
+#define MDC_MLS_MINB 2  // CTAs per SM the register allocation must allow
+#endif
 
 template <typename T>
 struct V2;
@@ -197,7 +200,7 @@ __device__ __forceinline__ T to_t(double x) {
 // The fused kernel.  VAR: MDC_MEAN / MDC_AFFINE / MDC_RIGID; DC: channels per
 // pass-2 chunk; R: pixels per thread.
 template <typename T, int VAR, int AM, int DC, int R>
-__global__ void __launch_bounds__(NT) mls_kernel(KArgs a) {
+__global__ void __launch_bounds__(NT, MDC_MLS_MINB) mls_kernel(KArgs a) {
     using T2 = typename V2<T>::type;
     constexpr int QE = Stager<T, DC>::QV * 16 / (int)sizeof(T);  // padded channels per control
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -518,11 +521,12 @@ static int dispatch_dc(const KArgs &k, cudaStream_t s) {
     if (d <= 2) return launch_t<T, VAR, AM, 2, R>(k, s);
     if (d <= 4) return launch_t<T, VAR, AM, 4, R>(k, s);
     if (d <= 8) return launch_t<T, VAR, AM, 8, R>(k, s);
-    if (F32) {
+    if constexpr (F32) {
         if (d <= 16) return launch_t<T, VAR, AM, 16, R>(k, s);
         return launch_t<T, VAR, AM, 32, R>(k, s);
+    } else {
+        return launch_t<T, VAR, AM, 16, R>(k, s);
     }
-    return launch_t<T, VAR, AM, 16, R>(k, s);
 }
 
 template <typename T, int VAR>

@@ -208,10 +208,17 @@ class FieldBlock:
     row0: int
     row1: int
     nonfinite: torch.Tensor         # () int32 device counter
+    h2d_bytes: int = 0              # host->device bytes this call uploaded
 
     def check_finite(self) -> None:
         if int(self.nonfinite.item()) != 0:
             raise FieldError("field evaluation produced non-finite coordinates")
+
+
+def _h2d(arr: np.ndarray, device: torch.device) -> torch.Tensor:
+    """Host -> device through a pinned staging buffer (async on the current stream)."""
+    t = torch.from_numpy(np.ascontiguousarray(arr))
+    return t.pin_memory().to(device, non_blocking=True)
 
 
 def _resolve_dtype(dtype) -> int:
@@ -269,12 +276,14 @@ class MlsProblem:
         qpad = np.zeros((n, ldq), dtype=np.float32 if self.dcode == _lib.MDC_F32 else np.float64)
         qpad[:, :d] = qk
         dev = self.device
-        self.pc_t = torch.as_tensor(np.ascontiguousarray(pc)).to(dev)
-        self.q_t = torch.as_tensor(qpad).to(dev)
-        self.qm_t = torch.as_tensor(np.ascontiguousarray(qm)).to(dev)
-        self.axis_t = torch.as_tensor(ax).to(dev)
-        self.pos_t = torch.as_tensor(positions).to(dev)
-        self.tvals_t = torch.as_tensor(tvals).to(dev)
+        self.pc_t = _h2d(pc, dev)
+        self.q_t = _h2d(qpad, dev)
+        self.qm_t = _h2d(qm, dev)
+        self.axis_t = _h2d(ax, dev)
+        self.pos_t = _h2d(positions, dev)
+        self.tvals_t = _h2d(tvals, dev)
+        self.h2d_bytes = sum(t.numel() * t.element_size() for t in
+                             (self.pc_t, self.q_t, self.qm_t, self.axis_t, self.pos_t, self.tvals_t))
         self.ldq = ldq
 
     def args(self, out, out_strides, row0, row1, bands=None, band_strides=(0, 0), spacing=None,
@@ -332,13 +341,14 @@ def compute_fields(positions, targets, params: MlsParams, width: int, height: in
     bands = spacing_t = None
     if band_spacing is not None:
         sp = np.broadcast_to(np.asarray(band_spacing, dtype=np.float64), (prob.d,)).copy()
-        spacing_t = torch.as_tensor(sp).to(dev)
+        spacing_t = _h2d(sp, dev)
         bands = torch.empty((prob.d, rows, width), dtype=torch.int32, device=dev)
     nonfinite = torch.zeros((), dtype=torch.int32, device=dev)
     a = prob.args(out, (rows * width, width, 1), r0, r1, bands, (rows * width, width), spacing_t, nonfinite)
     prob.run(a)
+    h2d = 0 if problem is not None else prob.h2d_bytes + (spacing_t.numel() * 8 if spacing_t is not None else 0)
     return FieldBlock(values=out, bands=bands, transform=prob.transform, row0=r0, row1=r1,
-                      nonfinite=nonfinite)
+                      nonfinite=nonfinite, h2d_bytes=h2d)
 
 
 def compute_field(mesh, positions: np.ndarray, targets: TargetAssignment, params: MlsParams,
