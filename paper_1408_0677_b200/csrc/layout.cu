@@ -20,6 +20,7 @@
 // reference's order.
 #include <math.h>
 
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 #include <algorithm>
 #include <vector>
@@ -40,6 +41,13 @@ struct TreeShape {
     std::vector<int32_t> seg_lo, seg_hi, seg_node, seg_split;
     // per depth L (0..max_depth): nodes created at that depth
     std::vector<int32_t> nd_off, nd_list;
+    // leaves in left-to-right order and each node's contiguous leaf range
+    std::vector<int32_t> leaves, leaf_lo, leaf_hi;
+    // BH task split: the nodes at depth cut (left to right) each become an
+    // independent traversal task; task_path holds their cut ancestors and
+    // task_first marks the task that owns an ancestor's monopole.
+    int cut = 0, ntask = 1;
+    std::vector<int32_t> task_node, task_path, task_first;
 };
 
 static int32_t shape_build(TreeShape &t, int32_t lo, int32_t hi, int d) {
@@ -74,6 +82,45 @@ static void make_shape(TreeShape &t, int64_t n, int leaf) {
     t.nd_list.resize(nn);
     std::vector<int32_t> fill(t.nd_off.begin(), t.nd_off.end() - 1);
     for (int i = 0; i < nn; ++i) t.nd_list[fill[t.depth[i]]++] = i;  // preorder ids ascending == lo ascending per depth
+    // leaves by lo; a node's leaves are the contiguous run with lo in [lo, hi)
+    for (int i = 0; i < nn; ++i)
+        if (t.left[i] < 0) t.leaves.push_back(i);
+    std::sort(t.leaves.begin(), t.leaves.end(), [&](int32_t a, int32_t b) { return t.lo[a] < t.lo[b]; });
+    t.leaf_lo.resize(nn);
+    t.leaf_hi.resize(nn);
+    {
+        std::vector<int32_t> llo(t.leaves.size());
+        for (size_t k = 0; k < t.leaves.size(); ++k) llo[k] = t.lo[t.leaves[k]];
+        for (int i = 0; i < nn; ++i) {
+            t.leaf_lo[i] = (int32_t)(std::lower_bound(llo.begin(), llo.end(), t.lo[i]) - llo.begin());
+            t.leaf_hi[i] = (int32_t)(std::lower_bound(llo.begin(), llo.end(), t.hi[i]) - llo.begin());
+        }
+    }
+    // BH task split at the deepest depth <= 4 above every leaf
+    {
+        int min_leaf_depth = t.max_depth;
+        for (int i = 0; i < nn; ++i)
+            if (t.left[i] < 0) min_leaf_depth = std::min(min_leaf_depth, t.depth[i]);
+        t.cut = std::min(4, min_leaf_depth);
+        for (int i = 0; i < nn; ++i)
+            if (t.depth[i] == t.cut) t.task_node.push_back(i);
+        std::sort(t.task_node.begin(), t.task_node.end(), [&](int32_t a, int32_t b) { return t.lo[a] < t.lo[b]; });
+        t.ntask = (int)t.task_node.size();
+        std::vector<int32_t> parent(nn, -1);
+        for (int i = 0; i < nn; ++i)
+            if (t.left[i] >= 0) parent[t.left[i]] = parent[t.right[i]] = i;
+        t.task_path.assign((size_t)t.ntask * (t.cut > 0 ? t.cut : 1), -1);
+        t.task_first.assign(t.task_path.size(), 0);
+        for (int k = 0; k < t.ntask; ++k) {
+            int u = t.task_node[k];
+            for (int dd = t.cut - 1; dd >= 0; --dd) {
+                u = parent[u];
+                t.task_path[(size_t)k * t.cut + dd] = u;
+                // leftmost depth-cut descendant of u == the task whose node has lo == lo(u)
+                t.task_first[(size_t)k * t.cut + dd] = t.lo[t.task_node[k]] == t.lo[u] ? 1 : 0;
+            }
+        }
+    }
     // frontier per level L = nodes with depth == L, plus leaves with depth < L
     t.seg_off.assign(1, 0);
     for (int L = 0; L < t.max_depth; ++L) {
@@ -108,7 +155,15 @@ struct Carver {
 struct DevTree {
     int32_t *lo, *hi, *left, *right, *axis;
     int32_t *seg_lo, *seg_hi, *seg_node, *seg_split, *nd_list;
+    int32_t *leaves, *leaf_lo, *leaf_hi;
+    int32_t *seg_off, *nd_off;
+    int32_t *task_node, *task_path, *task_first;
+    int cut, ntask;
+    double *part;       // ntask x n x 2 partial BH forces
     double *com, *mass, *size, *bmin, *bmax;
+    double *leaf_sum;   // 2 per leaf
+    double *spts;       // points in leaf (perm) order, n x 2
+    int nleaves;
 };
 
 struct Buffers {
@@ -147,6 +202,21 @@ static size_t carve(Buffers &b, char *base, const TreeShape &s) {
     b.t.seg_hi = c.take<int32_t>(ns);
     b.t.seg_node = c.take<int32_t>(ns);
     b.t.seg_split = c.take<int32_t>(ns);
+    size_t nl = s.leaves.size() ? s.leaves.size() : 1;
+    b.t.seg_off = c.take<int32_t>(s.seg_off.size() + 1);
+    b.t.task_node = c.take<int32_t>(s.task_node.size() + 1);
+    b.t.task_path = c.take<int32_t>(s.task_path.size() + 1);
+    b.t.task_first = c.take<int32_t>(s.task_first.size() + 1);
+    b.t.cut = s.cut;
+    b.t.ntask = s.ntask;
+    b.t.part = c.take<double>(2 * (size_t)s.ntask * (size_t)(n > 0 ? n : 1));
+    b.t.nd_off = c.take<int32_t>(s.nd_off.size() + 1);
+    b.t.leaves = c.take<int32_t>(nl);
+    b.t.leaf_lo = c.take<int32_t>(nn);
+    b.t.leaf_hi = c.take<int32_t>(nn);
+    b.t.leaf_sum = c.take<double>(2 * nl);
+    b.t.spts = c.take<double>(2 * (size_t)(n > 0 ? n : 1));
+    b.t.nleaves = (int)s.leaves.size();
     b.t.com = c.take<double>(2 * nn);
     b.t.mass = c.take<double>(nn);
     b.t.size = c.take<double>(nn);
@@ -162,7 +232,7 @@ static size_t carve(Buffers &b, char *base, const TreeShape &s) {
     b.ys[0] = c.take<int32_t>(n);
     b.ys[1] = c.take<int32_t>(n);
     b.flag = c.take<int32_t>(n);
-    b.blocksum = c.take<int32_t>((n + SCAN_BLOCK - 1) / SCAN_BLOCK + 1);
+    b.blocksum = c.take<int32_t>(std::max<int64_t>((n + SCAN_BLOCK - 1) / SCAN_BLOCK + 1, 1024));
     b.pos_b = c.take<double>(2 * n);
     b.bh = c.take<double>(2 * n);
     b.ctr = c.take<int32_t>(4);
@@ -328,15 +398,19 @@ __global__ void partition_kernel(int64_t n, DevTree t, int seg0, int nseg, const
     On[dest] = id;
 }
 
-// Centroids: one warp per node sums its perm range (mean, bhtree.py:46).
-__global__ void com_kernel(const double *pts, DevTree t, int nnodes, const int32_t *perm) {
+// Centroids (mean, bhtree.py:46), deterministic two-level sum: one warp per
+// leaf sums its points (and gathers them into leaf order for the traversal),
+// then one warp per node sums its contiguous run of leaf sums.
+__global__ void leaf_sum_kernel(const double *pts, DevTree t, const int32_t *perm) {
     int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     int lane = threadIdx.x & 31;
-    if (w >= nnodes) return;
-    int lo = t.lo[w], hi = t.hi[w];
+    if (w >= t.nleaves) return;
+    int node = t.leaves[w];
+    int lo = t.lo[node], hi = t.hi[node];
     double sx = 0.0, sy = 0.0;
     for (int k = lo + lane; k < hi; k += 32) {
         double2 p = reinterpret_cast<const double2 *>(pts)[perm[k]];
+        reinterpret_cast<double2 *>(t.spts)[k] = p;
         sx += p.x;
         sy += p.y;
     }
@@ -346,9 +420,202 @@ __global__ void com_kernel(const double *pts, DevTree t, int nnodes, const int32
         sy += __shfl_xor_sync(0xffffffffu, sy, o);
     }
     if (lane == 0) {
-        double m = (double)(hi - lo);
+        t.leaf_sum[2 * w] = sx;
+        t.leaf_sum[2 * w + 1] = sy;
+    }
+}
+
+__global__ void com_kernel(DevTree t, int nnodes) {
+    int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    if (w >= nnodes) return;
+    int l0 = t.leaf_lo[w], l1 = t.leaf_hi[w];
+    double sx = 0.0, sy = 0.0;
+    for (int k = l0 + lane; k < l1; k += 32) {
+        sx += t.leaf_sum[2 * k];
+        sy += t.leaf_sum[2 * k + 1];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        sx += __shfl_xor_sync(0xffffffffu, sx, o);
+        sy += __shfl_xor_sync(0xffffffffu, sy, o);
+    }
+    if (lane == 0) {
+        double m = (double)(t.hi[w] - t.lo[w]);
         t.com[2 * w] = sx / m;
         t.com[2 * w + 1] = sy / m;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// The whole level walk as ONE cooperative kernel (grid-wide syncs between
+// phases) instead of ~6 launches per level: per level
+//   phase 1  node stats for this depth; left-flags through each splitting
+//            segment's primary run
+//   phase 2  per-block counts of the other run's flags        (grid sync)
+//   phase 3  global exclusive prefix of those flags           (grid sync)
+//   phase 4  stable partition of the other run, copy the rest (grid sync)
+// then leaf sums + leaf-order gather, and centroids.
+namespace cg = cooperative_groups;
+constexpr int BUILD_THREADS = 256;
+
+struct BuildArgs {
+    const double *pts;
+    int64_t n;
+    DevTree t;
+    int max_depth, nnodes;
+    int32_t *xs0, *xs1, *ys0, *ys1;
+    int32_t *flag, *oflag, *prefix, *blocksum;
+};
+
+__device__ __forceinline__ void stats_for(const BuildArgs &a, int node, const int32_t *X, const int32_t *Y) {
+    const DevTree &t = a.t;
+    int lo = t.lo[node], hi = t.hi[node];
+    double xmin = a.pts[2 * X[lo]], xmax = a.pts[2 * X[hi - 1]];
+    double ymin = a.pts[2 * Y[lo] + 1], ymax = a.pts[2 * Y[hi - 1] + 1];
+    t.bmin[2 * node] = xmin;
+    t.bmin[2 * node + 1] = ymin;
+    t.bmax[2 * node] = xmax;
+    t.bmax[2 * node + 1] = ymax;
+    double ex = xmax - xmin, ey = ymax - ymin;
+    t.size[node] = hypot(ex, ey);
+    t.mass[node] = (double)(hi - lo);
+    t.axis[node] = ey > ex ? 1 : 0;
+}
+
+__global__ void __launch_bounds__(BUILD_THREADS) build_levels_kernel(BuildArgs a) {
+    cg::grid_group grid = cg::this_grid();
+    typedef cub::BlockReduce<int, BUILD_THREADS> BR;
+    typedef cub::BlockScan<int, BUILD_THREADS> BS;
+    __shared__ union {
+        typename BR::TempStorage r;
+        typename BS::TempStorage s;
+    } tmp;
+    __shared__ int s_carry;
+    const DevTree &t = a.t;
+    const int64_t n = a.n;
+    const int G = gridDim.x, tid = threadIdx.x;
+    const int64_t gtid = (int64_t)blockIdx.x * BUILD_THREADS + tid, gsz = (int64_t)G * BUILD_THREADS;
+    const int64_t chunk = (((n + G - 1) / G) + BUILD_THREADS - 1) / BUILD_THREADS * BUILD_THREADS;
+    const int64_t c_lo = min((int64_t)blockIdx.x * chunk, n), c_hi = min(c_lo + chunk, n);
+    int32_t *X = a.xs0, *Y = a.ys0, *Xn = a.xs1, *Yn = a.ys1;
+    for (int L = 0; L <= a.max_depth; ++L) {
+        // ---- phase 1
+        const int d0 = t.nd_off[L], dn = t.nd_off[L + 1] - d0;
+        for (int64_t e = gtid; e < dn; e += gsz) stats_for(a, t.nd_list[d0 + e], X, Y);
+        if (L == a.max_depth) break;
+        const int seg0 = t.seg_off[L], nseg = t.seg_off[L + 1] - seg0;
+        for (int64_t k = gtid; k < n; k += gsz) {
+            int s = seg0 + find_seg(t.seg_lo + seg0, nseg, (int)k);
+            if (!t.seg_split[s]) continue;
+            int lo = t.seg_lo[s], hi = t.seg_hi[s];
+            double ex = a.pts[2 * X[hi - 1]] - a.pts[2 * X[lo]];
+            double ey = a.pts[2 * Y[hi - 1] + 1] - a.pts[2 * Y[lo] + 1];
+            const int32_t *P = ey > ex ? Y : X;
+            a.flag[P[k]] = (k - lo) < (hi - lo) / 2 ? 1 : 0;
+        }
+        grid.sync();
+        // ---- phase 2: other-run flags, per-block counts over this block's chunk
+        int cnt = 0;
+        for (int64_t k = c_lo + tid; k < c_hi; k += BUILD_THREADS) {
+            int s = seg0 + find_seg(t.seg_lo + seg0, nseg, (int)k);
+            int v = 0;
+            if (t.seg_split[s]) {
+                const int32_t *O = t.axis[t.seg_node[s]] ? X : Y;
+                v = a.flag[O[k]];
+            }
+            a.oflag[k] = v;
+            cnt += v;
+        }
+        cnt = BR(tmp.r).Sum(cnt);
+        if (tid == 0) a.blocksum[blockIdx.x] = cnt;
+        grid.sync();
+        // ---- phase 3: global exclusive prefix
+        int base = 0;
+        for (int b = tid; b < (int)blockIdx.x; b += BUILD_THREADS) base += a.blocksum[b];
+        __syncthreads();
+        base = BR(tmp.r).Sum(base);
+        if (tid == 0) s_carry = base;
+        __syncthreads();
+        for (int64_t b0 = c_lo; b0 < c_hi; b0 += BUILD_THREADS) {
+            int64_t k = b0 + tid;
+            int v = k < c_hi ? a.oflag[k] : 0, ex, agg;
+            BS(tmp.s).ExclusiveSum(v, ex, agg);
+            if (k < c_hi) a.prefix[k] = s_carry + ex;
+            __syncthreads();
+            if (tid == 0) s_carry += agg;
+            __syncthreads();
+        }
+        grid.sync();
+        // ---- phase 4: stable partition
+        for (int64_t k = gtid; k < n; k += gsz) {
+            int s = seg0 + find_seg(t.seg_lo + seg0, nseg, (int)k);
+            if (!t.seg_split[s]) {
+                Xn[k] = X[k];
+                Yn[k] = Y[k];
+                continue;
+            }
+            int lo = t.seg_lo[s], hi = t.seg_hi[s];
+            int mid = (hi - lo) / 2;
+            int ax = t.axis[t.seg_node[s]];
+            const int32_t *P = ax ? Y : X;
+            const int32_t *O = ax ? X : Y;
+            int32_t *Pn = ax ? Yn : Xn;
+            int32_t *On = ax ? Xn : Yn;
+            Pn[k] = P[k];
+            int id = O[k];
+            int left_before = a.prefix[k] - a.prefix[lo];
+            int dest = a.flag[id] ? lo + left_before : lo + mid + ((int)k - lo - left_before);
+            On[dest] = id;
+        }
+        grid.sync();
+        int32_t *tx = X, *ty = Y;
+        X = Xn;
+        Y = Yn;
+        Xn = tx;
+        Yn = ty;
+    }
+    // leaf sums + gather into leaf order (warp per leaf)
+    const int lane = tid & 31;
+    const int64_t gw = gtid >> 5, nw = gsz >> 5;
+    for (int64_t w = gw; w < t.nleaves; w += nw) {
+        int node = t.leaves[w];
+        int lo = t.lo[node], hi = t.hi[node];
+        double sx = 0.0, sy = 0.0;
+        for (int k = lo + lane; k < hi; k += 32) {
+            double2 p = reinterpret_cast<const double2 *>(a.pts)[X[k]];
+            reinterpret_cast<double2 *>(t.spts)[k] = p;
+            sx += p.x;
+            sy += p.y;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            sx += __shfl_xor_sync(0xffffffffu, sx, o);
+            sy += __shfl_xor_sync(0xffffffffu, sy, o);
+        }
+        if (lane == 0) {
+            t.leaf_sum[2 * w] = sx;
+            t.leaf_sum[2 * w + 1] = sy;
+        }
+    }
+    grid.sync();
+    for (int64_t w = gw; w < a.nnodes; w += nw) {
+        int l0 = t.leaf_lo[w], l1 = t.leaf_hi[w];
+        double sx = 0.0, sy = 0.0;
+        for (int k = l0 + lane; k < l1; k += 32) {
+            sx += t.leaf_sum[2 * k];
+            sy += t.leaf_sum[2 * k + 1];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            sx += __shfl_xor_sync(0xffffffffu, sx, o);
+            sy += __shfl_xor_sync(0xffffffffu, sy, o);
+        }
+        if (lane == 0) {
+            double m = (double)(t.hi[w] - t.lo[w]);
+            t.com[2 * w] = sx / m;
+            t.com[2 * w + 1] = sy / m;
+        }
     }
 }
 
@@ -357,97 +624,150 @@ __global__ void com_kernel(const double *pts, DevTree t, int nnodes, const int32
 constexpr int BH_WARPS = 4;
 constexpr int BH_STACK = 64;
 
-__global__ void __launch_bounds__(BH_WARPS * 32) bh_kernel(const double *pts, int64_t n, DevTree t,
-                                                           const int32_t *perm, double c,
-                                                           double eta, double theta, double *out) {
+// fp64 reciprocal / reciprocal square root: MUFU seed + two Newton steps
+// (relative error ~1 ulp; the reference's IEEE division/sqrt agree to ~1e-16,
+// far inside the 1e-12 per-step contract).  The opening criterion keeps the
+// IEEE sqrt so every far/near decision matches the reference bit for bit.
+__device__ __forceinline__ double rcp_nr(double x) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    double e = fma(-x, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-x, r, 1.0);
+    return fma(r, e, r);
+}
+__device__ __forceinline__ double rsqrt_nr(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    double h = 0.5 * x;
+    double e = fma(-h * y, y, 0.5);
+    y = fma(y, e, y);
+    e = fma(-h * y, y, 0.5);
+    return fma(y, e, y);
+}
+
+__device__ __forceinline__ bool far_node(const DevTree &t, int node, double xi, double yi, double theta) {
+    double gx = t.bmin[2 * node] - xi;
+    if (gx < 0.0) gx = xi - t.bmax[2 * node];
+    if (gx < 0.0) gx = 0.0;
+    double gy = t.bmin[2 * node + 1] - yi;
+    if (gy < 0.0) gy = yi - t.bmax[2 * node + 1];
+    if (gy < 0.0) gy = 0.0;
+    double box_dist = __dsqrt_rn(__dadd_rn(__dmul_rn(gx, gx), __dmul_rn(gy, gy)));
+    return t.size[node] < __dmul_rn(theta, box_dist);
+}
+
+__device__ __forceinline__ void monopole(const DevTree &t, int node, double xi, double yi, double c,
+                                         double eta, double &fx, double &fy) {
+    double dx = xi - t.com[2 * node], dy = yi - t.com[2 * node + 1];
+    double r2 = dx * dx + dy * dy;
+    double r = r2 * rsqrt_nr(r2);
+    double coef = c * t.mass[node] * rcp_nr(r * r * r + eta);
+    fx = fma(coef, dx, fx);
+    fy = fma(coef, dy, fy);
+}
+
+// grid.x: groups of BH_WARPS warps (32 leaf-order points each); grid.y: task.
+// A task re-checks its cut ancestors per lane (an accepted ancestor's
+// monopole is added by exactly one task), then walks its subtree.  The set of
+// interactions per point is exactly the reference's; partial sums per task
+// are combined in task order by the consumer.
+__global__ void __launch_bounds__(BH_WARPS * 32) bh_kernel(int64_t n, DevTree t, double c, double eta,
+                                                           double theta) {
     __shared__ int s_node[BH_WARPS][BH_STACK];
     __shared__ unsigned s_mask[BH_WARPS][BH_STACK];
     const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int task = blockIdx.y;
     const int64_t k = ((int64_t)blockIdx.x * BH_WARPS + wib) * 32 + lane;
     const bool valid = k < n;
-    const int i = valid ? perm[k] : 0;
     double xi = 0.0, yi = 0.0;
     if (valid) {
-        double2 p = reinterpret_cast<const double2 *>(pts)[i];
+        double2 p = reinterpret_cast<const double2 *>(t.spts)[k];
         xi = p.x;
         yi = p.y;
     }
     double fx = 0.0, fy = 0.0;
-    unsigned m0 = __ballot_sync(0xffffffffu, valid);
-    if (m0 == 0) return;
-    int sp = 0;
-    if (lane == 0) {
-        s_node[wib][0] = 0;
-        s_mask[wib][0] = m0;
+    bool act = valid;
+    for (int dd = 0; dd < t.cut; ++dd) {
+        int a = t.task_path[task * t.cut + dd];
+        if (act && far_node(t, a, xi, yi, theta)) {
+            act = false;
+            if (t.task_first[task * t.cut + dd]) monopole(t, a, xi, yi, c, eta, fx, fy);
+        }
     }
-    sp = 1;
-    __syncwarp();
-    while (sp > 0) {
-        --sp;
-        int node = s_node[wib][sp];
-        unsigned mask = s_mask[wib][sp];
+    unsigned m0 = __ballot_sync(0xffffffffu, act);
+    if (m0) {
+        if (lane == 0) {
+            s_node[wib][0] = t.task_node[task];
+            s_mask[wib][0] = m0;
+        }
+        int sp = 1;
         __syncwarp();
-        bool act = (mask >> lane) & 1u;
-        if (t.left[node] < 0) {
-            int lo = t.lo[node], cnt = t.hi[node] - lo;
-            for (int base = 0; base < cnt; base += 32) {
-                int kk = base + lane;
-                int jid = -1;
-                double xj = 0.0, yj = 0.0;
-                if (kk < cnt) {
-                    jid = perm[lo + kk];
-                    double2 p = reinterpret_cast<const double2 *>(pts)[jid];
-                    xj = p.x;
-                    yj = p.y;
-                }
-                int m = min(32, cnt - base);
-                for (int q = 0; q < m; ++q) {
-                    int j = __shfl_sync(0xffffffffu, jid, q);
-                    double px = __shfl_sync(0xffffffffu, xj, q);
-                    double py = __shfl_sync(0xffffffffu, yj, q);
-                    if (act && j != i) {
-                        double dx = xi - px, dy = yi - py;
+        const double2 *sp2 = reinterpret_cast<const double2 *>(t.spts);
+        while (sp > 0) {
+            --sp;
+            int node = s_node[wib][sp];
+            unsigned mask = s_mask[wib][sp];
+            __syncwarp();
+            bool on = (mask >> lane) & 1u;
+            if (t.left[node] < 0) {
+                // Leaf: pairwise sum over its points (_kernels.py:194-205).  The
+                // self term is exactly +0 (dx = dy = 0, w finite since eta > 0),
+                // so no j != i test is needed -- coincident distinct points
+                // also contribute 0 in the reference.
+                if (on) {
+                    int lo = t.lo[node], hi = t.hi[node];
+#pragma unroll 4
+                    for (int q = lo; q < hi; ++q) {
+                        double2 pj = __ldg(sp2 + q);
+                        double dx = xi - pj.x, dy = yi - pj.y;
                         double r2 = dx * dx + dy * dy;
-                        double w = c / (r2 * sqrt(r2) + eta);
-                        fx += w * dx;
-                        fy += w * dy;
+                        double y = r2 > 0.0 ? rsqrt_nr(r2) : 0.0;
+                        double w = c * rcp_nr(r2 * (r2 * y) + eta);
+                        fx = fma(w, dx, fx);
+                        fy = fma(w, dy, fy);
                     }
                 }
+                continue;
             }
-            continue;
-        }
-        bool open = false;
-        if (act) {
-            double gx = t.bmin[2 * node] - xi;
-            if (gx < 0.0) gx = xi - t.bmax[2 * node];
-            if (gx < 0.0) gx = 0.0;
-            double gy = t.bmin[2 * node + 1] - yi;
-            if (gy < 0.0) gy = yi - t.bmax[2 * node + 1];
-            if (gy < 0.0) gy = 0.0;
-            double box_dist = sqrt(gx * gx + gy * gy);
-            if (t.size[node] < theta * box_dist) {
-                double dx = xi - t.com[2 * node], dy = yi - t.com[2 * node + 1];
-                double r = sqrt(dx * dx + dy * dy);
-                double coef = c * t.mass[node] / (r * r * r + eta);
-                fx += coef * dx;
-                fy += coef * dy;
-            } else {
-                open = true;
+            bool open = false;
+            if (on) {
+                if (far_node(t, node, xi, yi, theta))
+                    monopole(t, node, xi, yi, c, eta, fx, fy);
+                else
+                    open = true;
             }
-        }
-        unsigned om = __ballot_sync(0xffffffffu, open);
-        if (om) {
-            if (lane == 0) {
-                s_node[wib][sp] = t.left[node];
-                s_mask[wib][sp] = om;
-                s_node[wib][sp + 1] = t.right[node];
-                s_mask[wib][sp + 1] = om;
+            unsigned om = __ballot_sync(0xffffffffu, open);
+            if (om) {
+                if (lane == 0) {
+                    s_node[wib][sp] = t.left[node];
+                    s_mask[wib][sp] = om;
+                    s_node[wib][sp + 1] = t.right[node];
+                    s_mask[wib][sp + 1] = om;
+                }
+                sp += 2;
+                __syncwarp();
             }
-            sp += 2;
-            __syncwarp();
         }
     }
-    if (valid) reinterpret_cast<double2 *>(out)[i] = make_double2(fx, fy);
+    if (valid) reinterpret_cast<double2 *>(t.part)[(size_t)task * n + k] = make_double2(fx, fy);
+}
+
+// Combine the task partials (task order) into out[i] by point id.
+__device__ __forceinline__ double2 bh_total(const DevTree &t, int64_t n, int64_t k) {
+    double fx = 0.0, fy = 0.0;
+    for (int task = 0; task < t.ntask; ++task) {
+        double2 v = reinterpret_cast<const double2 *>(t.part)[(size_t)task * n + k];
+        fx += v.x;
+        fy += v.y;
+    }
+    return make_double2(fx, fy);
+}
+
+__global__ void bh_combine_kernel(int64_t n, DevTree t, const int32_t *perm, double *out) {
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    reinterpret_cast<double2 *>(out)[perm[k]] = bh_total(t, n, k);
 }
 
 // ---------------------------------------------------------------------------
@@ -580,6 +900,7 @@ struct MdcLayoutPlan {
     cudaGraphExec_t graph[2] = {nullptr, nullptr};
     cudaStream_t cap_stream = nullptr;
     const double *graph_temps = nullptr;
+    int build_blocks = 0;
 };
 
 namespace mdc {
@@ -598,32 +919,24 @@ static int build_tree(MdcLayoutPlan *p, const double *pts, cudaStream_t s, const
     bytes = b.cub_bytes;
     MDC_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(b.cub_tmp, bytes, b.ky, b.ky_out, b.ids, b.ys[0],
                                                    (int)n, 0, 64, s));
-    int cur = 0;
-    int nsb = (int)((n + SCAN_BLOCK - 1) / SCAN_BLOCK);
-    int32_t *prefix = reinterpret_cast<int32_t *>(b.kx);  // kx is free after the sort
-    for (int L = 0; L <= sh.max_depth; ++L) {
-        int c0 = sh.nd_off[L], cnt = sh.nd_off[L + 1] - c0;
-        if (cnt > 0) {
-            node_stats_kernel<<<(cnt + 127) / 128, 128, 0, s>>>(pts, b.t, b.t.nd_list + c0, cnt,
-                                                                b.xs[cur], b.ys[cur]);
-            MDC_CHECK_LAUNCH();
-        }
-        if (L == sh.max_depth) break;
-        int seg0 = sh.seg_off[L], nseg = sh.seg_off[L + 1] - seg0;
-        flag_kernel<<<nb, 256, 0, s>>>(n, b.t, seg0, nseg, b.xs[cur], b.ys[cur], b.flag);
-        blocksum_kernel<<<nsb, SCAN_BLOCK, 0, s>>>(n, b.t, seg0, nseg, b.xs[cur], b.ys[cur], b.flag,
-                                                   b.blocksum);
-        blockscan_kernel<<<1, SCAN_BLOCK, 0, s>>>(nsb, b.blocksum);
-        scatter_kernel<<<nsb, SCAN_BLOCK, 0, s>>>(n, b.t, seg0, nseg, b.xs[cur], b.ys[cur], b.flag,
-                                                  b.blocksum, b.xs[cur ^ 1], b.ys[cur ^ 1], prefix);
-        partition_kernel<<<nb, 256, 0, s>>>(n, b.t, seg0, nseg, b.xs[cur], b.ys[cur], b.flag, prefix,
-                                            b.xs[cur ^ 1], b.ys[cur ^ 1]);
-        MDC_CHECK_LAUNCH();
-        cur ^= 1;
-    }
-    int nn = (int)sh.lo.size();
-    com_kernel<<<(nn * 32 + 255) / 256, 256, 0, s>>>(pts, b.t, nn, b.xs[cur]);
-    MDC_CHECK_LAUNCH();
+    BuildArgs ba;
+    ba.pts = pts;
+    ba.n = n;
+    ba.t = b.t;
+    ba.max_depth = sh.max_depth;
+    ba.nnodes = (int)sh.lo.size();
+    ba.xs0 = b.xs[0];
+    ba.xs1 = b.xs[1];
+    ba.ys0 = b.ys[0];
+    ba.ys1 = b.ys[1];
+    ba.flag = b.flag;
+    ba.oflag = reinterpret_cast<int32_t *>(b.kx_out);  // free after the sorts
+    ba.prefix = reinterpret_cast<int32_t *>(b.kx);
+    ba.blocksum = b.blocksum;
+    void *kargs[] = {&ba};
+    MDC_CHECK_CUDA(cudaLaunchCooperativeKernel((const void *)build_levels_kernel, dim3(p->build_blocks),
+                                               dim3(BUILD_THREADS), kargs, 0, s));
+    int cur = sh.max_depth & 1;
     *perm_out = b.xs[cur];
     return MDC_OK;
 }
@@ -634,8 +947,9 @@ static int run_bh(MdcLayoutPlan *p, const double *pts, double *out, cudaStream_t
     if (rc) return rc;
     int64_t n = p->shape.n;
     int64_t warps = (n + 31) / 32;
-    bh_kernel<<<(unsigned)((warps + BH_WARPS - 1) / BH_WARPS), BH_WARPS * 32, 0, s>>>(
-        pts, n, p->b.t, perm, p->a.c, p->a.eta, p->a.theta, out);
+    dim3 grid((unsigned)((warps + BH_WARPS - 1) / BH_WARPS), (unsigned)p->shape.ntask);
+    bh_kernel<<<grid, BH_WARPS * 32, 0, s>>>(n, p->b.t, p->a.c, p->a.eta, p->a.theta);
+    bh_combine_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, p->b.t, perm, out);
     MDC_CHECK_LAUNCH();
     return MDC_OK;
 }
@@ -716,10 +1030,27 @@ extern "C" int mdc_layout_plan_create(const MdcLayoutArgs *a, MdcLayoutPlan **pl
     rc |= up(p->b.t.seg_hi, sh.seg_hi);
     rc |= up(p->b.t.seg_node, sh.seg_node);
     rc |= up(p->b.t.seg_split, sh.seg_split);
+    rc |= up(p->b.t.leaves, sh.leaves);
+    rc |= up(p->b.t.seg_off, sh.seg_off);
+    rc |= up(p->b.t.task_node, sh.task_node);
+    rc |= up(p->b.t.task_path, sh.task_path);
+    rc |= up(p->b.t.task_first, sh.task_first);
+    rc |= up(p->b.t.nd_off, sh.nd_off);
+    rc |= up(p->b.t.leaf_lo, sh.leaf_lo);
+    rc |= up(p->b.t.leaf_hi, sh.leaf_hi);
     (void)nn;
     if (rc) {
         delete p;
         return MDC_ECUDA;
+    }
+    {
+        int dev = 0, sms = 0, per_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, build_levels_kernel, BUILD_THREADS, 0);
+        int want = (int)((p->shape.n + BUILD_THREADS - 1) / BUILD_THREADS);
+        p->build_blocks = std::max(1, std::min(std::max(1, per_sm) * sms, want));
+        if (p->build_blocks > 1024) p->build_blocks = 1024;  // blocksum capacity below
     }
     // host vectors must outlive the async copies
     cudaError_t e = cudaStreamSynchronize(s);
