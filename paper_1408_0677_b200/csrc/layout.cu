@@ -160,6 +160,8 @@ struct DevTree {
     int32_t *task_node, *task_path, *task_first;
     int cut, ntask;
     double *part;       // ntask x n x 2 partial BH forces
+    double4 *geo;       // per node: {bmin.x, bmin.y, bmax.x, bmax.y}, {com.x, com.y, size, mass}
+    int4 *topo;         // per node: {lo, hi, left, right}
     double *com, *mass, *size, *bmin, *bmax;
     double *leaf_sum;   // 2 per leaf
     double *spts;       // points in leaf (perm) order, n x 2
@@ -210,6 +212,8 @@ static size_t carve(Buffers &b, char *base, const TreeShape &s) {
     b.t.cut = s.cut;
     b.t.ntask = s.ntask;
     b.t.part = c.take<double>(2 * (size_t)s.ntask * (size_t)(n > 0 ? n : 1));
+    b.t.geo = c.take<double4>(2 * nn);
+    b.t.topo = c.take<int4>(nn);
     b.t.nd_off = c.take<int32_t>(s.nd_off.size() + 1);
     b.t.leaves = c.take<int32_t>(nl);
     b.t.leaf_lo = c.take<int32_t>(nn);
@@ -613,8 +617,12 @@ __global__ void __launch_bounds__(BUILD_THREADS) build_levels_kernel(BuildArgs a
         }
         if (lane == 0) {
             double m = (double)(t.hi[w] - t.lo[w]);
-            t.com[2 * w] = sx / m;
-            t.com[2 * w + 1] = sy / m;
+            double cx = sx / m, cy = sy / m;
+            t.com[2 * w] = cx;
+            t.com[2 * w + 1] = cy;
+            t.geo[2 * w] = make_double4(t.bmin[2 * w], t.bmin[2 * w + 1], t.bmax[2 * w], t.bmax[2 * w + 1]);
+            t.geo[2 * w + 1] = make_double4(cx, cy, t.size[w], t.mass[w]);
+            t.topo[w] = make_int4(t.lo[w], t.hi[w], t.left[w], t.right[w]);
         }
     }
 }
@@ -624,45 +632,42 @@ __global__ void __launch_bounds__(BUILD_THREADS) build_levels_kernel(BuildArgs a
 constexpr int BH_WARPS = 4;
 constexpr int BH_STACK = 64;
 
-// fp64 reciprocal / reciprocal square root: MUFU seed + two Newton steps
-// (relative error ~1 ulp; the reference's IEEE division/sqrt agree to ~1e-16,
-// far inside the 1e-12 per-step contract).  The opening criterion keeps the
-// IEEE sqrt so every far/near decision matches the reference bit for bit.
+// fp64 reciprocal / reciprocal square root: MUFU seed + one third-order
+// correction each (seed error e ~ 2^-22 -> O(e^3) ~ 2^-66, i.e. ~1 ulp after
+// rounding).  The reference's IEEE division/sqrt agree to ~1e-16, far inside
+// the 1e-12 per-step contract.  The opening criterion keeps the IEEE sqrt so
+// every far/near decision matches the reference bit for bit.
 __device__ __forceinline__ double rcp_nr(double x) {
     double r;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-    double e = fma(-x, r, 1.0);
-    r = fma(r, e, r);
-    e = fma(-x, r, 1.0);
-    return fma(r, e, r);
+    double e = fma(-x, r, 1.0);      // r = (1 - e)/x
+    return fma(r, fma(e, e, e), r);  // r (1 + e + e^2)
 }
 __device__ __forceinline__ double rsqrt_nr(double x) {
     double y;
     asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-    double h = 0.5 * x;
-    double e = fma(-h * y, y, 0.5);
-    y = fma(y, e, y);
-    e = fma(-h * y, y, 0.5);
-    return fma(y, e, y);
+    double e = fma(-x * y, y, 1.0);                 // y = (1 - e)^(1/2) / sqrt(x)
+    return fma(y * e, fma(0.375, e, 0.5), y);       // y (1 + e/2 + 3e^2/8)
 }
 
-__device__ __forceinline__ bool far_node(const DevTree &t, int node, double xi, double yi, double theta) {
-    double gx = t.bmin[2 * node] - xi;
-    if (gx < 0.0) gx = xi - t.bmax[2 * node];
+__device__ __forceinline__ bool far_node(const double4 g0, double size, double xi, double yi, double theta) {
+    double gx = g0.x - xi;
+    if (gx < 0.0) gx = xi - g0.z;
     if (gx < 0.0) gx = 0.0;
-    double gy = t.bmin[2 * node + 1] - yi;
-    if (gy < 0.0) gy = yi - t.bmax[2 * node + 1];
+    double gy = g0.y - yi;
+    if (gy < 0.0) gy = yi - g0.w;
     if (gy < 0.0) gy = 0.0;
     double box_dist = __dsqrt_rn(__dadd_rn(__dmul_rn(gx, gx), __dmul_rn(gy, gy)));
-    return t.size[node] < __dmul_rn(theta, box_dist);
+    return size < __dmul_rn(theta, box_dist);
 }
 
-__device__ __forceinline__ void monopole(const DevTree &t, int node, double xi, double yi, double c,
-                                         double eta, double &fx, double &fy) {
-    double dx = xi - t.com[2 * node], dy = yi - t.com[2 * node + 1];
+// Accumulates mass * (x_i - com) / (r^3 + eta); the caller scales by c once.
+__device__ __forceinline__ void monopole(const double4 g1, double xi, double yi, double eta, double &fx,
+                                         double &fy) {
+    double dx = xi - g1.x, dy = yi - g1.y;
     double r2 = dx * dx + dy * dy;
     double r = r2 * rsqrt_nr(r2);
-    double coef = c * t.mass[node] * rcp_nr(r * r * r + eta);
+    double coef = g1.w * rcp_nr(r * r * r + eta);
     fx = fma(coef, dx, fx);
     fy = fma(coef, dy, fy);
 }
@@ -690,9 +695,10 @@ __global__ void __launch_bounds__(BH_WARPS * 32) bh_kernel(int64_t n, DevTree t,
     bool act = valid;
     for (int dd = 0; dd < t.cut; ++dd) {
         int a = t.task_path[task * t.cut + dd];
-        if (act && far_node(t, a, xi, yi, theta)) {
+        double4 g0 = t.geo[2 * a], g1 = t.geo[2 * a + 1];
+        if (act && far_node(g0, g1.z, xi, yi, theta)) {
             act = false;
-            if (t.task_first[task * t.cut + dd]) monopole(t, a, xi, yi, c, eta, fx, fy);
+            if (t.task_first[task * t.cut + dd]) monopole(g1, xi, yi, eta, fx, fy);
         }
     }
     unsigned m0 = __ballot_sync(0xffffffffu, act);
@@ -710,20 +716,20 @@ __global__ void __launch_bounds__(BH_WARPS * 32) bh_kernel(int64_t n, DevTree t,
             unsigned mask = s_mask[wib][sp];
             __syncwarp();
             bool on = (mask >> lane) & 1u;
-            if (t.left[node] < 0) {
+            int4 tp = t.topo[node];
+            if (tp.z < 0) {
                 // Leaf: pairwise sum over its points (_kernels.py:194-205).  The
-                // self term is exactly +0 (dx = dy = 0, w finite since eta > 0),
-                // so no j != i test is needed -- coincident distinct points
-                // also contribute 0 in the reference.
+                // self term is exactly +0 (dx = dy = 0; r2 is floored so the
+                // weight stays finite), so no j != i test is needed --
+                // coincident distinct points also contribute 0 in the reference.
                 if (on) {
-                    int lo = t.lo[node], hi = t.hi[node];
 #pragma unroll 4
-                    for (int q = lo; q < hi; ++q) {
+                    for (int q = tp.x; q < tp.y; ++q) {
                         double2 pj = __ldg(sp2 + q);
                         double dx = xi - pj.x, dy = yi - pj.y;
-                        double r2 = dx * dx + dy * dy;
-                        double y = r2 > 0.0 ? rsqrt_nr(r2) : 0.0;
-                        double w = c * rcp_nr(r2 * (r2 * y) + eta);
+                        double r2 = fmax(dx * dx + dy * dy, 1e-300);
+                        double y = rsqrt_nr(r2);
+                        double w = rcp_nr(r2 * (r2 * y) + eta);
                         fx = fma(w, dx, fx);
                         fy = fma(w, dy, fy);
                     }
@@ -732,17 +738,18 @@ __global__ void __launch_bounds__(BH_WARPS * 32) bh_kernel(int64_t n, DevTree t,
             }
             bool open = false;
             if (on) {
-                if (far_node(t, node, xi, yi, theta))
-                    monopole(t, node, xi, yi, c, eta, fx, fy);
+                double4 g0 = t.geo[2 * node], g1 = t.geo[2 * node + 1];
+                if (far_node(g0, g1.z, xi, yi, theta))
+                    monopole(g1, xi, yi, eta, fx, fy);
                 else
                     open = true;
             }
             unsigned om = __ballot_sync(0xffffffffu, open);
             if (om) {
                 if (lane == 0) {
-                    s_node[wib][sp] = t.left[node];
+                    s_node[wib][sp] = tp.z;
                     s_mask[wib][sp] = om;
-                    s_node[wib][sp + 1] = t.right[node];
+                    s_node[wib][sp + 1] = tp.w;
                     s_mask[wib][sp + 1] = om;
                 }
                 sp += 2;
@@ -750,7 +757,7 @@ __global__ void __launch_bounds__(BH_WARPS * 32) bh_kernel(int64_t n, DevTree t,
             }
         }
     }
-    if (valid) reinterpret_cast<double2 *>(t.part)[(size_t)task * n + k] = make_double2(fx, fy);
+    if (valid) reinterpret_cast<double2 *>(t.part)[(size_t)task * n + k] = make_double2(c * fx, c * fy);
 }
 
 // Combine the task partials (task order) into out[i] by point id.
