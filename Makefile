@@ -13,6 +13,9 @@ build/%.o: $(PKG)/csrc/%.cu $(PKG)/csrc/common.cuh include/mdc.h
 	@mkdir -p build
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
+# the seam kernels mirror numba's operation order: no FMA contraction
+build/seam.o: NVFLAGS += -fmad=false
+
 $(PKG)/libmdc.so: $(OBJ)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJ)
 

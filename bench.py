@@ -304,7 +304,9 @@ def main():
     W, H, d = cfg["W"], cfg["H"], cfg["d"]
     spacing = np.array([_auto_spacing(raw[:, k]) for k in range(d)])
     prob = MlsProblem(positions, raw, "affine", W, H, dtype="f32")
-    r0, r1 = rank * H // world, (rank + 1) * H // world
+    from paper_1408_0677_b200.shard import broadcast_controls, row_band
+
+    r0, r1 = row_band(rank, world, H)
     rows = r1 - r0
     out = torch.empty((d, rows, W), dtype=torch.float32, device=dev)
     bands = torch.empty((d, rows, W), dtype=torch.int32, device=dev)
@@ -319,9 +321,7 @@ def main():
     kev = []
 
     def frame(timed):
-        if world > 1:
-            for tsr in ctrl:  # point data broadcast once per frame (NVLink)
-                dist.broadcast(tsr, src=0)
+        broadcast_controls(ctrl, src=0)  # point data once per frame (NCCL / NVLink)
         flush.fill_(1)
         nonfinite.zero_()
         if timed:

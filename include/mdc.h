@@ -114,6 +114,29 @@ MDC_API size_t mdc_snap_workspace_bytes(int32_t width, int32_t rows);
 MDC_API int mdc_mls_snap(const MdcMlsArgs *a, const double *pos, const double *tvals, double eps,
                  void *workspace, void *stream);
 
+/* One-to-one seam replacements of the reference's numba kernels (same
+ * arguments and out-parameter convention as _kernels.py, DEVICE pointers,
+ * fp64, the reference's own operation order).  npix pixels at (vx, vy),
+ * n controls, out is npix x 2.
+ *   mdc_mean_field   <- _kernels.mean_field   (_kernels.py:52-67)
+ *   mdc_affine_field <- _kernels.affine_field (_kernels.py:70-124)
+ *   mdc_rigid_field  <- _kernels.rigid_field  (_kernels.py:127-175)
+ *   mdc_bh_forces    <- _kernels.bh_forces    (_kernels.py:178-230), int64
+ *                       flat kd-tree arrays exactly as bhtree.KdTree holds them */
+MDC_API int mdc_mean_field(int64_t npix, const double *vx, const double *vy, int64_t n, const double *px,
+                           const double *py, const double *dqx, const double *dqy, double alpha,
+                           double *out, void *stream);
+MDC_API int mdc_affine_field(int64_t npix, const double *vx, const double *vy, int64_t n, const double *px,
+                             const double *py, const double *qx, const double *qy, double alpha,
+                             double reg_eps, double *out, void *stream);
+MDC_API int mdc_rigid_field(int64_t npix, const double *vx, const double *vy, int64_t n, const double *px,
+                            const double *py, const double *qx, const double *qy, double alpha, double *out,
+                            void *stream);
+MDC_API int mdc_bh_forces(int64_t n, const double *points, const int64_t *perm, const int64_t *lo,
+                          const int64_t *hi, const int64_t *left, const int64_t *right, const double *com,
+                          const double *mass, const double *size, const double *bmin, const double *bmax,
+                          double c, double eta, double theta, double *out, void *stream);
+
 /* ------------------------------------------------------------------------ */
 /* Constrained layout (layout.py:266-302).
  *
