@@ -9,7 +9,7 @@ OBJ := $(patsubst $(PKG)/csrc/%.cu,build/%.o,$(SRC))
 
 all: $(PKG)/libmdc.so oracle
 
-build/%.o: $(PKG)/csrc/%.cu $(PKG)/csrc/common.cuh include/mdc.h
+build/%.o: $(PKG)/csrc/%.cu $(wildcard $(PKG)/csrc/*.cuh) include/mdc.h
 	@mkdir -p build
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 

@@ -239,6 +239,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--frame", default=None, help="override the raster, WxH (profiling only)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-tc", action="store_true", help="force the SIMT MLS kernel (A/B)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -303,7 +304,7 @@ def main():
 
     W, H, d = cfg["W"], cfg["H"], cfg["d"]
     spacing = np.array([_auto_spacing(raw[:, k]) for k in range(d)])
-    prob = MlsProblem(positions, raw, "affine", W, H, dtype="f32")
+    prob = MlsProblem(positions, raw, "affine", W, H, dtype="f32", tensor_cores=not args.no_tc)
     from paper_1408_0677_b200.shard import broadcast_controls, row_band
 
     r0, r1 = row_band(rank, world, H)

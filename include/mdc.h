@@ -98,9 +98,18 @@ typedef struct MdcMlsArgs {
     int64_t band_cs, band_rs;
     const double *spacing;
     int32_t *nonfinite;
+    /* tensor-core path (fp32 affine, d >= 8): scratch for the pre-arranged
+     * hi/lo target image, mdc_mls_workspace_bytes(a) bytes; NULL or too small
+     * selects the SIMT kernel.  flags: MDC_FLAG_NO_TC forces SIMT. */
+    int32_t flags;
+    void *workspace;
+    size_t workspace_bytes;
 } MdcMlsArgs;
 
+#define MDC_FLAG_NO_TC 1
+
 MDC_API int mdc_mls_field(const MdcMlsArgs *a, void *stream);
+MDC_API size_t mdc_mls_workspace_bytes(const MdcMlsArgs *a);
 
 /* Snap (field.py:388-412): pixels of rows [row0,row1) whose centre lies at
  * squared distance < eps from control i (un-centred positions, fp64 decisions

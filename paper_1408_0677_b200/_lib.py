@@ -17,6 +17,7 @@ LIB_PATH = os.environ.get("MDC_LIB_PATH") or os.path.join(HERE, "libmdc.so")  # 
 
 MDC_MEAN, MDC_AFFINE, MDC_RIGID = 1, 2, 3
 MDC_F32, MDC_F64 = 0, 1
+MDC_FLAG_NO_TC = 1
 VARIANT_CODE = {"mean": MDC_MEAN, "affine": MDC_AFFINE, "rigid": MDC_RIGID}
 
 _c_i32 = ctypes.c_int32
@@ -41,6 +42,9 @@ class MdcMlsArgs(ctypes.Structure):
         ("band_cs", _c_i64), ("band_rs", _c_i64),
         ("spacing", _vp),
         ("nonfinite", _vp),
+        ("flags", _c_i32),
+        ("workspace", _vp),
+        ("workspace_bytes", ctypes.c_size_t),
     ]
 
 
@@ -63,6 +67,7 @@ SIGNATURES = {
     "mdc_version": (ctypes.c_int, []),
     "mdc_num_sms": (ctypes.c_int, []),
     "mdc_mls_field": (ctypes.c_int, [ctypes.POINTER(MdcMlsArgs), _vp]),
+    "mdc_mls_workspace_bytes": (ctypes.c_size_t, [ctypes.POINTER(MdcMlsArgs)]),
     "mdc_snap_workspace_bytes": (ctypes.c_size_t, [_c_i32, _c_i32]),
     "mdc_mls_snap": (ctypes.c_int, [ctypes.POINTER(MdcMlsArgs), _vp, _vp, _c_d, _vp, _vp]),
     "mdc_layout_workspace_bytes": (ctypes.c_size_t, [_c_i64, _c_i32]),

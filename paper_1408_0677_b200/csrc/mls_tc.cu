@@ -1,0 +1,399 @@
+// mls_tc.cu -- affine MLS with the pass-2 contraction on the 5th-gen tensor
+// cores (tcgen05, kind::tf32, 3xTF32 split, accumulators in TMEM).
+//
+// Same mathematics as mls.cu (SURVEY.md §8a M6'; reference _kernels.py:70-124):
+//   pass 1 (SIMT, fp32 FMA pipe): 6 pixel-local moments -> c = A_reg^{-1} e0
+//   pass 2: F[p, k] = sum_j G[p, j] Q[j, k],  G[p, j] = w_pj (c0 + c1 dx + c2 dy)
+// Pass 2 is a dense (pixels x N) . (N x d) contraction (north_star: "tensor
+// cores ... only for the global-support weight case").  The SIMT threads only
+// evaluate G (one weight per pair) and store it, split hi + lo, straight into
+// shared memory in the UMMA K-major core-matrix layout; one elected thread
+// issues tcgen05.mma (M = 128 pixels, N = channels, K = 8 controls) x 3
+// (hi*hi + hi*lo + lo*hi, ~fp32-accurate) per K step, accumulating in TMEM.
+// A two-stage ring (mbarrier armed by tcgen05.commit) overlaps the tensor
+// core with the SIMT evaluation of the next tile.  The target block Q is
+// pre-arranged once per call into the same core-matrix layout (hi/lo), so its
+// tiles are plain contiguous cp.async copies.
+//
+// Tile geometry: CTA = 256 threads = 256 pixels (two M=128 MMA tiles), K-tile
+// = 16 controls; 3 CTAs per SM.
+#include "mls_common.cuh"
+
+namespace mdc {
+namespace tc {
+
+constexpr int TPB = 256;          // threads == pixels per CTA
+constexpr int KT = 16;            // controls per K tile
+constexpr int STAGES = 2;
+constexpr int A_SBO = (KT / 4) * 128;                  // bytes between 8-row core-matrix groups
+constexpr int A_HALF = (TPB / 8) * A_SBO;              // one of hi/lo: 256 rows x KT
+constexpr int A_STAGE = 2 * A_HALF;
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// UMMA shared-memory descriptor, K-major, no swizzle ("interleave"):
+// ((8, m), 2) : ((16 B, SBO), LBO) -- 8-row x 16-byte core matrices.
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    return (uint64_t)((saddr & 0x3FFFF) >> 4) | ((uint64_t)(lbo >> 4) << 16) | ((uint64_t)(sbo >> 4) << 32) |
+           ((uint64_t)1 << 46);  // version 1 (Blackwell); base offset 0; SWIZZLE_NONE
+}
+
+// Instruction descriptor: D f32, A/B tf32, both K-major, M = 128, N = n.
+__host__ __device__ constexpr uint32_t idesc_tf32(int n) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ uint32_t tf32_hi_bits(float x) {
+    // round-to-nearest (ties away) to the 10-bit tf32 mantissa
+    return (__float_as_uint(x) + 0x1000u) & 0xFFFFE000u;
+}
+
+// byte offset of (row m, k) in a K-major core-matrix tile with SBO = A_SBO
+__device__ __forceinline__ uint32_t cm_off(int m, int k) {
+    return (uint32_t)((m >> 3) * A_SBO + (k >> 2) * 128 + (m & 7) * 16 + (k & 3) * 4);
+}
+
+// ---------------------------------------------------------------------------
+// Q -> tiled core-matrix image, hi/lo split.  img[(chunk * ntiles + t)][hi|lo]
+// each half = NC rows (channels) x KT controls = NC * 64 bytes.
+__global__ void q_image_kernel(const float *q, int64_t n, int ldq, int d, int nc, int nchunk, int64_t ntiles,
+                               float *img) {
+    int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int64_t total = (int64_t)nchunk * ntiles * nc * KT;
+    if (e >= total) return;
+    int k = (int)(e % KT);
+    int64_t r = e / KT;
+    int ch = (int)(r % nc);
+    r /= nc;
+    int64_t t = r % ntiles;
+    int chunk = (int)(r / ntiles);
+    int64_t j = t * KT + k;
+    int gch = chunk * nc + ch;
+    float v = (j < n && gch < d) ? q[j * ldq + gch] : 0.0f;
+    float hi = __uint_as_float(tf32_hi_bits(v));
+    float lo = v - hi;
+    size_t tile_bytes = (size_t)nc * 64;
+    char *base = reinterpret_cast<char *>(img) + ((size_t)chunk * ntiles + t) * 2 * tile_bytes;
+    uint32_t off = (uint32_t)((ch >> 3) * A_SBO + (k >> 2) * 128 + (ch & 7) * 16 + (k & 3) * 4);
+    *reinterpret_cast<float *>(base + off) = hi;
+    *reinterpret_cast<float *>(base + tile_bytes + off) = lo;
+}
+
+template <int AM, int NC>
+__global__ void __launch_bounds__(TPB, 3) mls_tc_kernel(KArgs a, const float *qimg, int64_t ntiles, int nchunk) {
+    constexpr int B_HALF = NC * 64;
+    constexpr int B_STAGE = 2 * B_HALF;
+    constexpr int TMEM_COLS = (2 * NC <= 32) ? 32 : (2 * NC <= 64 ? 64 : (2 * NC <= 128 ? 128 : 256));
+    extern __shared__ __align__(128) unsigned char smem[];
+    unsigned char *sA = smem;                                  // STAGES x A_STAGE
+    unsigned char *sB = sA + STAGES * A_STAGE;                 // STAGES x B_STAGE
+    float2 *sxy = reinterpret_cast<float2 *>(sB + STAGES * B_STAGE);  // TPB controls
+    uint64_t *bar = reinterpret_cast<uint64_t *>(sxy + TPB);   // STAGES mma-done barriers
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar + STAGES);
+
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const int64_t tile_base = (a.tile0 + blockIdx.x) * (int64_t)TPB;
+    const float neg_alpha = (float)(-a.alpha);
+
+    if (tid == 0) {
+        for (int s = 0; s < STAGES; ++s) mbar_init(&bar[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "n"(TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = *tmem_slot;
+
+    // pixel + tile-local frame (identical to mls.cu: global tile alignment)
+    double ox, oy;
+    {
+        int64_t mid = tile_base + TPB / 2;
+        if (mid >= a.p_total) mid = a.p_total - 1;
+        pixel_xy(a, mid, ox, oy);
+    }
+    int64_t p = tile_base + tid;
+    const bool active = p >= a.p_begin && p < a.p_end;
+    if (!active) p = p < a.p_begin ? a.p_begin : a.p_end - 1;
+    double vxg, vyg;
+    pixel_xy(a, p, vxg, vyg);
+    const float vx = (float)(vxg - ox), vy = (float)(vyg - oy);
+    const int64_t n = a.n;
+    const int64_t nxy = (n + TPB - 1) / TPB;
+
+    auto stage_xy = [&](int64_t r) {
+        int64_t j = r * TPB + tid;
+        double rx = 0.0, ry = 0.0;
+        if (j < n) {
+            double2 v = reinterpret_cast<const double2 *>(a.pc)[j];
+            rx = v.x;
+            ry = v.y;
+        }
+        __syncthreads();
+        sxy[tid] = make_float2((float)(rx - ox), (float)(ry - oy));
+        __syncthreads();
+    };
+
+    // ---------------- pass 1: moments (SIMT) ----------------
+    float sw = 0.f, mx = 0.f, my = 0.f, sxx = 0.f, sxy_ = 0.f, syy = 0.f;
+    for (int64_t r = 0; r < nxy; ++r) {
+        stage_xy(r);
+        const int cnt = (int)min((int64_t)TPB, n - r * TPB);
+        const float4 *s4 = reinterpret_cast<const float4 *>(sxy);
+        int j = 0;
+#pragma unroll 4
+        for (; j + 1 < cnt; j += 2) {
+            float4 pp = s4[j >> 1];
+            {
+                float dx = pp.x - vx, dy = pp.y - vy;
+                float w = weight<AM>(dx * dx + dy * dy, neg_alpha);
+                float wdx = w * dx, wdy = w * dy;
+                sw += w; mx += wdx; my += wdy;
+                sxx += wdx * dx; sxy_ += wdx * dy; syy += wdy * dy;
+            }
+            {
+                float dx = pp.z - vx, dy = pp.w - vy;
+                float w = weight<AM>(dx * dx + dy * dy, neg_alpha);
+                float wdx = w * dx, wdy = w * dy;
+                sw += w; mx += wdx; my += wdy;
+                sxx += wdx * dx; sxy_ += wdx * dy; syy += wdy * dy;
+            }
+        }
+        if (j < cnt) {
+            float2 pp = sxy[j];
+            float dx = pp.x - vx, dy = pp.y - vy;
+            float w = weight<AM>(dx * dx + dy * dy, neg_alpha);
+            float wdx = w * dx, wdy = w * dy;
+            sw += w; mx += wdx; my += wdy;
+            sxx += wdx * dx; sxy_ += wdx * dy; syy += wdy * dy;
+        }
+    }
+    float c0, c1, c2;
+    {
+        double s = sw, m0 = mx, m1 = my;
+        double a00 = (double)sxx - m0 * m0 / s;
+        double a01 = (double)sxy_ - m0 * m1 / s;
+        double a11 = (double)syy - m1 * m1 / s;
+        double reg = a.reg_eps * (a00 + a11);
+        a00 += reg;
+        a11 += reg;
+        double det = a00 * a11 - a01 * a01;
+        double u0 = (a11 * m0 - a01 * m1) / det;
+        double u1 = (a00 * m1 - a01 * m0) / det;
+        c0 = (float)(1.0 / s + (m0 * u0 + m1 * u1) / (s * s));
+        c1 = (float)(-u0 / s);
+        c2 = (float)(-u1 / s);
+    }
+
+    // ---------------- pass 2: G tiles -> tcgen05 ----------------
+    const uint32_t idesc = idesc_tf32(NC);
+    const int mrow = tid;  // row of this thread's pixel in the CTA's 256-row A tile
+    bool bad = false;
+    uint32_t tiles_done = 0;  // global count of issued K tiles (ring position)
+    for (int chunk = 0; chunk < nchunk; ++chunk) {
+        const char *qchunk = reinterpret_cast<const char *>(qimg) + (size_t)chunk * ntiles * B_STAGE;
+        for (int64_t t = 0; t < ntiles; ++t) {
+            const int64_t j0 = t * KT;
+            if ((j0 % TPB) == 0) stage_xy(j0 / TPB);
+            const uint32_t ring = tiles_done + (uint32_t)t;
+            const int s = ring & 1;
+            if (ring >= STAGES) mbar_wait(&bar[s], ((ring - STAGES) >> 1) & 1);
+            // B tile: contiguous copy of the pre-arranged hi|lo image
+            unsigned char *bs = sB + s * B_STAGE;
+            const char *src = qchunk + (size_t)t * B_STAGE;
+            for (int c = tid; c < B_STAGE / 16; c += TPB) cp_async16(bs + c * 16, src + c * 16);
+            cp_async_commit();
+            // G for 16 controls, stored hi / lo in core-matrix layout
+            unsigned char *as = sA + s * A_STAGE;
+            const int jl0 = (int)(j0 % TPB);
+#pragma unroll
+            for (int q4 = 0; q4 < KT / 4; ++q4) {
+                const float4 *s4 = reinterpret_cast<const float4 *>(sxy + jl0 + q4 * 4);
+                float g[4];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    float4 pp = s4[h];
+                    float dx = pp.x - vx, dy = pp.y - vy;
+                    float w = weight<AM>(dx * dx + dy * dy, neg_alpha);
+                    g[2 * h] = w * (c0 + c1 * dx + c2 * dy);
+                    dx = pp.z - vx;
+                    dy = pp.w - vy;
+                    w = weight<AM>(dx * dx + dy * dy, neg_alpha);
+                    g[2 * h + 1] = w * (c0 + c1 * dx + c2 * dy);
+                }
+                uint4 hi, lo;
+                uint32_t *hp = &hi.x, *lp = &lo.x;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    float ge = (j0 + q4 * 4 + e < n) ? g[e] : 0.0f;
+                    uint32_t hb = tf32_hi_bits(ge);
+                    hp[e] = hb;
+                    lp[e] = __float_as_uint(ge - __uint_as_float(hb));
+                }
+                const uint32_t off = cm_off(mrow, q4 * 4);
+                *reinterpret_cast<uint4 *>(as + off) = hi;
+                *reinterpret_cast<uint4 *>(as + A_HALF + off) = lo;
+            }
+            cp_async_wait<0>();
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncthreads();
+            if (tid == 0) {
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                const uint32_t a_hi = smem_u32(as), a_lo = smem_u32(as + A_HALF);
+                const uint32_t b_hi = smem_u32(bs), b_lo = smem_u32(bs + B_HALF);
+#pragma unroll
+                for (int mt = 0; mt < 2; ++mt) {
+                    const uint32_t dcol = tmem + mt * NC;
+                    const uint32_t moff = mt * (128 / 8) * A_SBO;
+#pragma unroll
+                    for (int ks = 0; ks < KT / 8; ++ks) {
+                        const uint32_t koff = ks * 256;
+                        const uint32_t acc = (t > 0 || ks > 0) ? 1u : 0u;
+                        uint64_t dah = umma_desc(a_hi + moff + koff, 128, A_SBO);
+                        uint64_t dal = umma_desc(a_lo + moff + koff, 128, A_SBO);
+                        uint64_t dbh = umma_desc(b_hi + koff, 128, A_SBO);
+                        uint64_t dbl = umma_desc(b_lo + koff, 128, A_SBO);
+                        mma_tf32(dcol, dah, dbh, idesc, acc);
+                        mma_tf32(dcol, dah, dbl, idesc, 1u);
+                        mma_tf32(dcol, dal, dbh, idesc, 1u);
+                    }
+                }
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                 smem_u32(&bar[s]))
+                             : "memory");
+            }
+        }
+        tiles_done += (uint32_t)ntiles;
+        // wait for this chunk's last MMAs, then drain TMEM
+        {
+            const uint32_t last = tiles_done - 1;
+            mbar_wait(&bar[last & 1], (last >> 1) & 1);
+        }
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+        const uint32_t col0 = tmem + (warp >> 2) * NC;
+        const int64_t row = p / a.width;
+        const int64_t col = p - row * a.width;
+        const int64_t lr = row - a.row0;
+#pragma unroll
+        for (int c8 = 0; c8 < NC / 8; ++c8) {
+            uint32_t v[8];
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                : "r"(lane_base + col0 + c8 * 8));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            if (active) {
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    const int ch = chunk * NC + c8 * 8 + e;
+                    if (ch < a.d) {
+                        float f = (float)((double)__uint_as_float(v[e]) + a.qm[ch]);
+                        reinterpret_cast<float *>(a.out)[ch * a.out_cs + lr * a.out_rs + col * a.out_ps] = f;
+                        if (!isfinite(f)) bad = true;
+                        if (a.bands)
+                            a.bands[ch * a.band_cs + lr * a.band_rs + col] = (int32_t)floor((double)f / a.spacing[ch]);
+                    }
+                }
+            }
+        }
+        // TMEM is re-used by the next chunk: every warp must have drained it
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;");
+    }
+    if (a.nonfinite && active && bad) atomicAdd(a.nonfinite, 1);
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS));
+}
+
+template <int NC>
+static size_t tc_smem_bytes() {
+    return STAGES * (size_t)A_STAGE + STAGES * (size_t)(2 * NC * 64) + TPB * sizeof(float2) +
+           STAGES * sizeof(uint64_t) + 16;
+}
+
+static int pick_nc(int d) { return d <= 16 ? 16 : (d <= 32 ? 32 : 64); }
+
+}  // namespace tc
+
+size_t mls_tc_workspace_bytes(int d, int64_t n) {
+    int nc = tc::pick_nc(d);
+    int nchunk = (d + nc - 1) / nc;
+    int64_t ntiles = (n + tc::KT - 1) / tc::KT;
+    return (size_t)nchunk * ntiles * 2 * nc * 64 + 256;
+}
+
+template <int AM, int NC>
+static int launch_tc_nc(const KArgs &k, void *ws, cudaStream_t s) {
+    using namespace tc;
+    const int nchunk = (k.d + NC - 1) / NC;
+    const int64_t ntiles = (k.n + KT - 1) / KT;
+    float *img = reinterpret_cast<float *>(ws);
+    int64_t total = (int64_t)nchunk * ntiles * NC * KT;
+    q_image_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(reinterpret_cast<const float *>(k.q), k.n,
+                                                                   k.ldq, k.d, NC, nchunk, ntiles, img);
+    auto fn = mls_tc_kernel<AM, NC>;
+    size_t smem = tc_smem_bytes<NC>();
+    static bool attr = false;
+    if (!attr) {
+        MDC_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    KArgs kk = k;
+    kk.tile0 = kk.p_begin / TPB;
+    int64_t blocks = (kk.p_end + TPB - 1) / TPB - kk.tile0;
+    if (blocks > 0) fn<<<(unsigned)blocks, TPB, smem, s>>>(kk, img, ntiles, nchunk);
+    MDC_CHECK_LAUNCH();
+    return MDC_OK;
+}
+
+template <int AM>
+static int launch_tc_am(const KArgs &k, void *ws, cudaStream_t s) {
+    switch (tc::pick_nc(k.d)) {
+        case 16: return launch_tc_nc<AM, 16>(k, ws, s);
+        case 32: return launch_tc_nc<AM, 32>(k, ws, s);
+        default: return launch_tc_nc<AM, 64>(k, ws, s);
+    }
+}
+
+int launch_mls_tc(const KArgs &k, void *ws, cudaStream_t s) {
+    switch (alpha_mode(k.alpha)) {
+        case A_ONE: return launch_tc_am<A_ONE>(k, ws, s);
+        case A_THREE_HALVES: return launch_tc_am<A_THREE_HALVES>(k, ws, s);
+        case A_HALF: return launch_tc_am<A_HALF>(k, ws, s);
+        case A_TWO: return launch_tc_am<A_TWO>(k, ws, s);
+        default: return launch_tc_am<A_GENERIC>(k, ws, s);
+    }
+}
+
+}  // namespace mdc

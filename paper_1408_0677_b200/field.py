@@ -235,7 +235,7 @@ class MlsProblem:
 
     def __init__(self, positions, targets, variant: str, width: int, height: int,
                  alpha=None, reg_eps=1e-12, epsilon_dist=None, dtype="f32", axis=None,
-                 device=None):
+                 device=None, tensor_cores: bool = True):
         lib = _lib.require_cuda()
         self.lib = lib
         if variant not in ("mean", "affine", "rigid"):
@@ -285,6 +285,8 @@ class MlsProblem:
         self.h2d_bytes = sum(t.numel() * t.element_size() for t in
                              (self.pc_t, self.q_t, self.qm_t, self.axis_t, self.pos_t, self.tvals_t))
         self.ldq = ldq
+        self.flags = 0 if tensor_cores else _lib.MDC_FLAG_NO_TC
+        self._ws = None
 
     def args(self, out, out_strides, row0, row1, bands=None, band_strides=(0, 0), spacing=None,
              nonfinite=None) -> _lib.MdcMlsArgs:
@@ -304,6 +306,12 @@ class MlsProblem:
         a.band_cs, a.band_rs = (int(s) for s in band_strides)
         a.spacing = _lib.ptr(spacing)
         a.nonfinite = _lib.ptr(nonfinite)
+        a.flags = self.flags
+        need = int(self.lib.mdc_mls_workspace_bytes(ctypes.byref(a)))
+        if need:
+            if self._ws is None or self._ws.numel() < need:
+                self._ws = torch.empty(need, dtype=torch.uint8, device=self.device)
+            a.workspace, a.workspace_bytes = _lib.ptr(self._ws), self._ws.numel()
         return a
 
     def run(self, a: _lib.MdcMlsArgs, snap: bool = True) -> None:
@@ -319,7 +327,7 @@ class MlsProblem:
 
 def compute_fields(positions, targets, params: MlsParams, width: int, height: int,
                    row_range=None, dtype="f32", band_spacing=None, axis=None,
-                   problem: MlsProblem | None = None) -> FieldBlock:
+                   problem: MlsProblem | None = None, tensor_cores: bool = True) -> FieldBlock:
     """Fused d-channel MLS: every column of ``targets`` (n, d) is one field.
 
     Channel k equals channel 0 of the reference's ``compute_field`` for the
@@ -333,7 +341,8 @@ def compute_fields(positions, targets, params: MlsParams, width: int, height: in
         raise FieldError("the linear variant is not on the GPU path yet (SURVEY.md §8f)")
     prob = problem or MlsProblem(positions, targets, params.variant, width, height,
                                  alpha=params.resolved_alpha, reg_eps=params.reg_eps,
-                                 epsilon_dist=params.epsilon_dist, dtype=dtype, axis=axis)
+                                 epsilon_dist=params.epsilon_dist, dtype=dtype, axis=axis,
+                                 tensor_cores=tensor_cores)
     r0, r1 = (0, height) if row_range is None else (int(row_range[0]), int(row_range[1]))
     rows = r1 - r0
     dev = prob.device

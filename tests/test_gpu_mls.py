@@ -134,3 +134,35 @@ def test_g2k_field(g2k):
     tv = F.TargetAssignment(g2k["targets_affine_dim0"], "dims", ("a",))
     fld = F.compute_field(golden_mesh(g2k), g2k["field_positions"], tv, F.MlsParams("affine"), W, H)
     assert normwise(fld.coords[..., 0], g2k["field_affine_dim0"][..., 0]) <= FP64_TOL
+
+
+@pytest.mark.parametrize("n,d,W,H,alpha", [(3000, 32, 96, 64, 1.5), (2000, 8, 64, 40, 1.0),
+                                           (2500, 16, 70, 48, 1.3), (1800, 40, 64, 64, 1.5),
+                                           (1000, 70, 48, 40, 2.0), (777, 24, 50, 30, 0.5)])
+def test_tensor_core_path_vs_oracle_and_simt(n, d, W, H, alpha):
+    """tcgen05 3xTF32 pass 2 (fp32 affine, d >= 8) against the fp64 oracle at
+    the fp32 contract and against the SIMT kernel."""
+    rng = np.random.default_rng(n * 7 + d)
+    pos = rng.normal(0, 3, (n, 2))
+    q = rng.normal(0, 1, (n, d)) + np.sin(pos[:, :1] * np.arange(1, d + 1) * 0.3)
+    params = F.MlsParams("affine", alpha=alpha)
+    tc = F.compute_fields(pos, q, params, W, H, dtype="f32", tensor_cores=True)
+    simt = F.compute_fields(pos, q, params, W, H, dtype="f32", tensor_cores=False)
+    tc.check_finite()
+    vt = tc.values.double().cpu().numpy()
+    vs = simt.values.double().cpu().numpy()
+    for k in sorted({0, d // 2, d - 1}):
+        tv = np.column_stack([q[:, k], np.zeros(n)])
+        ref = O.compute_field(pos, tv, "affine", W, H, alpha=alpha)[..., 0]
+        assert normwise(vt[k], ref) <= FP32_TOL, (k, normwise(vt[k], ref))
+        assert normwise(vt[k], vs[k]) <= FP32_TOL
+
+
+def test_tensor_core_row_bands_bit_identical(c1):
+    pos = c1["field_positions"]
+    W, H = (int(v) for v in c1["field_wh"])
+    raw = np.tile(c1["raw"], (1, 4))  # 16 channels -> TC path
+    full = F.compute_fields(pos, raw, F.MlsParams("affine"), W, H, dtype="f32").values.cpu()
+    parts = [F.compute_fields(pos, raw, F.MlsParams("affine"), W, H, dtype="f32", row_range=rr).values.cpu()
+             for rr in ((0, 5), (5, 33), (33, H))]
+    assert torch.equal(torch.cat(parts, dim=1), full)
