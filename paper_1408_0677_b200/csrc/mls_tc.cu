@@ -104,27 +104,59 @@ __global__ void q_image_kernel(const float *q, int64_t n, int ldq, int d, int nc
     *reinterpret_cast<float *>(base + tile_bytes + off) = lo;
 }
 
+// Warp roles: warps 0..7 (256 threads, one pixel each) evaluate moments and
+// G tiles; warp 8 is the producer/issuer: lane 0 waits for a full stage
+// (8 warp arrivals + the bulk-copied Q tile's bytes), issues the MMAs and
+// commits them to the stage's "empty" barrier.  No block-wide barrier per
+// K tile; compute warps only wait when the ring wraps onto a stage whose
+// MMAs are still in flight.
+constexpr int CWARPS = TPB / 32;        // compute warps
+constexpr int THREADS = TPB + 32;       // + one issuer warp
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void compute_bar_sync() {  // named barrier over the 256 compute threads
+    asm volatile("bar.sync 1, %0;" ::"n"(TPB) : "memory");
+}
+
 template <int AM, int NC>
-__global__ void __launch_bounds__(TPB, 3) mls_tc_kernel(KArgs a, const float *qimg, int64_t ntiles, int nchunk) {
+__global__ void __launch_bounds__(THREADS, 3) mls_tc_kernel(KArgs a, const float *qimg, int64_t ntiles, int nchunk) {
     constexpr int B_HALF = NC * 64;
     constexpr int B_STAGE = 2 * B_HALF;
     constexpr int TMEM_COLS = (2 * NC <= 32) ? 32 : (2 * NC <= 64 ? 64 : (2 * NC <= 128 ? 128 : 256));
     extern __shared__ __align__(128) unsigned char smem[];
-    unsigned char *sA = smem;                                  // STAGES x A_STAGE
-    unsigned char *sB = sA + STAGES * A_STAGE;                 // STAGES x B_STAGE
+    unsigned char *sA = smem;                                          // STAGES x A_STAGE
+    unsigned char *sB = sA + STAGES * A_STAGE;                         // STAGES x B_STAGE
     float2 *sxy = reinterpret_cast<float2 *>(sB + STAGES * B_STAGE);  // TPB controls
-    uint64_t *bar = reinterpret_cast<uint64_t *>(sxy + TPB);   // STAGES mma-done barriers
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar + STAGES);
+    uint64_t *full = reinterpret_cast<uint64_t *>(sxy + TPB);         // STAGES: G + Q ready
+    uint64_t *empty = full + STAGES;                                   // STAGES: MMAs retired
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(empty + STAGES);
 
-    const int tid = threadIdx.x, warp = tid >> 5;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const bool issuer = warp == CWARPS;
     const int64_t tile_base = (a.tile0 + blockIdx.x) * (int64_t)TPB;
     const float neg_alpha = (float)(-a.alpha);
 
     if (tid == 0) {
-        for (int s = 0; s < STAGES; ++s) mbar_init(&bar[s], 1);
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], CWARPS + 1);  // 8 compute-warp arrivals + 1 expect_tx arrival
+            mbar_init(&empty[s], 1);          // tcgen05.commit
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 0) {
+    if (issuer) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                      "n"(TMEM_COLS));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -133,213 +165,228 @@ __global__ void __launch_bounds__(TPB, 3) mls_tc_kernel(KArgs a, const float *qi
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tmem = *tmem_slot;
+    const uint32_t idesc = idesc_tf32(NC);
 
-    // pixel + tile-local frame (identical to mls.cu: global tile alignment)
-    double ox, oy;
-    {
-        int64_t mid = tile_base + TPB / 2;
-        if (mid >= a.p_total) mid = a.p_total - 1;
-        pixel_xy(a, mid, ox, oy);
-    }
-    int64_t p = tile_base + tid;
-    const bool active = p >= a.p_begin && p < a.p_end;
-    if (!active) p = p < a.p_begin ? a.p_begin : a.p_end - 1;
-    double vxg, vyg;
-    pixel_xy(a, p, vxg, vyg);
-    const float vx = (float)(vxg - ox), vy = (float)(vyg - oy);
-    const int64_t n = a.n;
-    const int64_t nxy = (n + TPB - 1) / TPB;
-
-    auto stage_xy = [&](int64_t r) {
-        int64_t j = r * TPB + tid;
-        double rx = 0.0, ry = 0.0;
-        if (j < n) {
-            double2 v = reinterpret_cast<const double2 *>(a.pc)[j];
-            rx = v.x;
-            ry = v.y;
+    if (issuer) {
+        // ------------------------------ MMA issuer --------------------------
+        if (lane == 0) {
+            uint32_t ring = 0;
+            for (int chunk = 0; chunk < nchunk; ++chunk) {
+                for (int64_t t = 0; t < ntiles; ++t, ++ring) {
+                    const int s = ring & 1;
+                    mbar_wait(&full[s], (ring >> 1) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+                    unsigned char *as = sA + s * A_STAGE;
+                    unsigned char *bs = sB + s * B_STAGE;
+                    const uint32_t a_hi = smem_u32(as), a_lo = smem_u32(as + A_HALF);
+                    const uint32_t b_hi = smem_u32(bs), b_lo = smem_u32(bs + B_HALF);
+#pragma unroll
+                    for (int mt = 0; mt < 2; ++mt) {
+                        const uint32_t dcol = tmem + mt * NC;
+                        const uint32_t moff = mt * (128 / 8) * A_SBO;
+#pragma unroll
+                        for (int kk = 0; kk < KT / 8; ++kk) {
+                            const uint32_t koff = kk * 256;
+                            const uint32_t acc = (t > 0 || kk > 0) ? 1u : 0u;
+                            const uint64_t dah = umma_desc(a_hi + moff + koff, 128, A_SBO);
+                            const uint64_t dal = umma_desc(a_lo + moff + koff, 128, A_SBO);
+                            const uint64_t dbh = umma_desc(b_hi + koff, 128, A_SBO);
+                            const uint64_t dbl = umma_desc(b_lo + koff, 128, A_SBO);
+                            mma_tf32(dcol, dah, dbh, idesc, acc);
+                            mma_tf32(dcol, dah, dbl, idesc, 1u);
+                            mma_tf32(dcol, dal, dbh, idesc, 1u);
+                        }
+                    }
+                    asm volatile(
+                        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                            smem_u32(&empty[s]))
+                        : "memory");
+                }
+            }
         }
-        __syncthreads();
-        sxy[tid] = make_float2((float)(rx - ox), (float)(ry - oy));
-        __syncthreads();
-    };
+        __syncwarp();
+    } else {
+        // ------------------------------ compute warps ------------------------
+        double ox, oy;
+        {
+            int64_t mid = tile_base + TPB / 2;
+            if (mid >= a.p_total) mid = a.p_total - 1;
+            pixel_xy(a, mid, ox, oy);
+        }
+        int64_t p = tile_base + tid;
+        const bool active = p >= a.p_begin && p < a.p_end;
+        if (!active) p = p < a.p_begin ? a.p_begin : a.p_end - 1;
+        double vxg, vyg;
+        pixel_xy(a, p, vxg, vyg);
+        const float vx = (float)(vxg - ox), vy = (float)(vyg - oy);
+        const int64_t n = a.n;
+        const int64_t nxy = (n + TPB - 1) / TPB;
 
-    // ---------------- pass 1: moments (SIMT) ----------------
-    float sw = 0.f, mx = 0.f, my = 0.f, sxx = 0.f, sxy_ = 0.f, syy = 0.f;
-    for (int64_t r = 0; r < nxy; ++r) {
-        stage_xy(r);
-        const int cnt = (int)min((int64_t)TPB, n - r * TPB);
-        const float4 *s4 = reinterpret_cast<const float4 *>(sxy);
-        int j = 0;
+        // Controls past n are parked far away (weight underflows to 0, G
+        // stays finite) and their Q rows are zero: full tiles, no masking.
+        auto stage_xy = [&](int64_t r) {
+            int64_t j = r * TPB + tid;
+            float2 v = make_float2(1e18f, 1e18f);
+            if (j < n) {
+                double2 d = reinterpret_cast<const double2 *>(a.pc)[j];
+                v = make_float2((float)(d.x - ox), (float)(d.y - oy));
+            }
+            compute_bar_sync();
+            sxy[tid] = v;
+            compute_bar_sync();
+        };
+
+        // ---------------- pass 1: moments (SIMT) ----------------
+        float sw = 0.f, mx = 0.f, my = 0.f, sxx = 0.f, sxy_ = 0.f, syy = 0.f;
+        for (int64_t r = 0; r < nxy; ++r) {
+            stage_xy(r);
+            const int cnt = (int)min((int64_t)TPB, n - r * TPB);
+            const float4 *s4 = reinterpret_cast<const float4 *>(sxy);
+            int j = 0;
 #pragma unroll 4
-        for (; j + 1 < cnt; j += 2) {
-            float4 pp = s4[j >> 1];
-            {
+            for (; j + 1 < cnt; j += 2) {
+                float4 pp = s4[j >> 1];
+                {
+                    float dx = pp.x - vx, dy = pp.y - vy;
+                    float w = weight<AM>(dx * dx + dy * dy, neg_alpha);
+                    float wdx = w * dx, wdy = w * dy;
+                    sw += w; mx += wdx; my += wdy;
+                    sxx += wdx * dx; sxy_ += wdx * dy; syy += wdy * dy;
+                }
+                {
+                    float dx = pp.z - vx, dy = pp.w - vy;
+                    float w = weight<AM>(dx * dx + dy * dy, neg_alpha);
+                    float wdx = w * dx, wdy = w * dy;
+                    sw += w; mx += wdx; my += wdy;
+                    sxx += wdx * dx; sxy_ += wdx * dy; syy += wdy * dy;
+                }
+            }
+            if (j < cnt) {
+                float2 pp = sxy[j];
                 float dx = pp.x - vx, dy = pp.y - vy;
                 float w = weight<AM>(dx * dx + dy * dy, neg_alpha);
                 float wdx = w * dx, wdy = w * dy;
                 sw += w; mx += wdx; my += wdy;
                 sxx += wdx * dx; sxy_ += wdx * dy; syy += wdy * dy;
             }
-            {
-                float dx = pp.z - vx, dy = pp.w - vy;
-                float w = weight<AM>(dx * dx + dy * dy, neg_alpha);
-                float wdx = w * dx, wdy = w * dy;
-                sw += w; mx += wdx; my += wdy;
-                sxx += wdx * dx; sxy_ += wdx * dy; syy += wdy * dy;
-            }
         }
-        if (j < cnt) {
-            float2 pp = sxy[j];
-            float dx = pp.x - vx, dy = pp.y - vy;
-            float w = weight<AM>(dx * dx + dy * dy, neg_alpha);
-            float wdx = w * dx, wdy = w * dy;
-            sw += w; mx += wdx; my += wdy;
-            sxx += wdx * dx; sxy_ += wdx * dy; syy += wdy * dy;
-        }
-    }
-    float c0, c1, c2;
-    {
-        double s = sw, m0 = mx, m1 = my;
-        double a00 = (double)sxx - m0 * m0 / s;
-        double a01 = (double)sxy_ - m0 * m1 / s;
-        double a11 = (double)syy - m1 * m1 / s;
-        double reg = a.reg_eps * (a00 + a11);
-        a00 += reg;
-        a11 += reg;
-        double det = a00 * a11 - a01 * a01;
-        double u0 = (a11 * m0 - a01 * m1) / det;
-        double u1 = (a00 * m1 - a01 * m0) / det;
-        c0 = (float)(1.0 / s + (m0 * u0 + m1 * u1) / (s * s));
-        c1 = (float)(-u0 / s);
-        c2 = (float)(-u1 / s);
-    }
-
-    // ---------------- pass 2: G tiles -> tcgen05 ----------------
-    const uint32_t idesc = idesc_tf32(NC);
-    const int mrow = tid;  // row of this thread's pixel in the CTA's 256-row A tile
-    bool bad = false;
-    uint32_t tiles_done = 0;  // global count of issued K tiles (ring position)
-    for (int chunk = 0; chunk < nchunk; ++chunk) {
-        const char *qchunk = reinterpret_cast<const char *>(qimg) + (size_t)chunk * ntiles * B_STAGE;
-        for (int64_t t = 0; t < ntiles; ++t) {
-            const int64_t j0 = t * KT;
-            if ((j0 % TPB) == 0) stage_xy(j0 / TPB);
-            const uint32_t ring = tiles_done + (uint32_t)t;
-            const int s = ring & 1;
-            if (ring >= STAGES) mbar_wait(&bar[s], ((ring - STAGES) >> 1) & 1);
-            // B tile: contiguous copy of the pre-arranged hi|lo image
-            unsigned char *bs = sB + s * B_STAGE;
-            const char *src = qchunk + (size_t)t * B_STAGE;
-            for (int c = tid; c < B_STAGE / 16; c += TPB) cp_async16(bs + c * 16, src + c * 16);
-            cp_async_commit();
-            // G for 16 controls, stored hi / lo in core-matrix layout
-            unsigned char *as = sA + s * A_STAGE;
-            const int jl0 = (int)(j0 % TPB);
-#pragma unroll
-            for (int q4 = 0; q4 < KT / 4; ++q4) {
-                const float4 *s4 = reinterpret_cast<const float4 *>(sxy + jl0 + q4 * 4);
-                float g[4];
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    float4 pp = s4[h];
-                    float dx = pp.x - vx, dy = pp.y - vy;
-                    float w = weight<AM>(dx * dx + dy * dy, neg_alpha);
-                    g[2 * h] = w * (c0 + c1 * dx + c2 * dy);
-                    dx = pp.z - vx;
-                    dy = pp.w - vy;
-                    w = weight<AM>(dx * dx + dy * dy, neg_alpha);
-                    g[2 * h + 1] = w * (c0 + c1 * dx + c2 * dy);
-                }
-                uint4 hi, lo;
-                uint32_t *hp = &hi.x, *lp = &lo.x;
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    float ge = (j0 + q4 * 4 + e < n) ? g[e] : 0.0f;
-                    uint32_t hb = tf32_hi_bits(ge);
-                    hp[e] = hb;
-                    lp[e] = __float_as_uint(ge - __uint_as_float(hb));
-                }
-                const uint32_t off = cm_off(mrow, q4 * 4);
-                *reinterpret_cast<uint4 *>(as + off) = hi;
-                *reinterpret_cast<uint4 *>(as + A_HALF + off) = lo;
-            }
-            cp_async_wait<0>();
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            __syncthreads();
-            if (tid == 0) {
-                asm volatile("tcgen05.fence::after_thread_sync;");
-                const uint32_t a_hi = smem_u32(as), a_lo = smem_u32(as + A_HALF);
-                const uint32_t b_hi = smem_u32(bs), b_lo = smem_u32(bs + B_HALF);
-#pragma unroll
-                for (int mt = 0; mt < 2; ++mt) {
-                    const uint32_t dcol = tmem + mt * NC;
-                    const uint32_t moff = mt * (128 / 8) * A_SBO;
-#pragma unroll
-                    for (int ks = 0; ks < KT / 8; ++ks) {
-                        const uint32_t koff = ks * 256;
-                        const uint32_t acc = (t > 0 || ks > 0) ? 1u : 0u;
-                        uint64_t dah = umma_desc(a_hi + moff + koff, 128, A_SBO);
-                        uint64_t dal = umma_desc(a_lo + moff + koff, 128, A_SBO);
-                        uint64_t dbh = umma_desc(b_hi + koff, 128, A_SBO);
-                        uint64_t dbl = umma_desc(b_lo + koff, 128, A_SBO);
-                        mma_tf32(dcol, dah, dbh, idesc, acc);
-                        mma_tf32(dcol, dah, dbl, idesc, 1u);
-                        mma_tf32(dcol, dal, dbh, idesc, 1u);
-                    }
-                }
-                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                                 smem_u32(&bar[s]))
-                             : "memory");
-            }
-        }
-        tiles_done += (uint32_t)ntiles;
-        // wait for this chunk's last MMAs, then drain TMEM
+        float c0, c1, c2;
         {
-            const uint32_t last = tiles_done - 1;
-            mbar_wait(&bar[last & 1], (last >> 1) & 1);
+            double s = sw, m0 = mx, m1 = my;
+            double a00 = (double)sxx - m0 * m0 / s;
+            double a01 = (double)sxy_ - m0 * m1 / s;
+            double a11 = (double)syy - m1 * m1 / s;
+            double reg = a.reg_eps * (a00 + a11);
+            a00 += reg;
+            a11 += reg;
+            double det = a00 * a11 - a01 * a01;
+            double u0 = (a11 * m0 - a01 * m1) / det;
+            double u1 = (a00 * m1 - a01 * m0) / det;
+            c0 = (float)(1.0 / s + (m0 * u0 + m1 * u1) / (s * s));
+            c1 = (float)(-u0 / s);
+            c2 = (float)(-u1 / s);
         }
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
-        const uint32_t col0 = tmem + (warp >> 2) * NC;
+
+        // ---------------- pass 2: G tiles -> ring -> tcgen05 ----------------
+        bool bad = false;
+        uint32_t ring = 0;
         const int64_t row = p / a.width;
         const int64_t col = p - row * a.width;
         const int64_t lr = row - a.row0;
+        for (int chunk = 0; chunk < nchunk; ++chunk) {
+            const char *qchunk = reinterpret_cast<const char *>(qimg) + (size_t)chunk * ntiles * B_STAGE;
+            for (int64_t t = 0; t < ntiles; ++t, ++ring) {
+                const int tin = (int)(t & (TPB / KT - 1));
+                if (tin == 0) stage_xy(t / (TPB / KT));
+                const int s = ring & 1;
+                if (ring >= STAGES) mbar_wait(&empty[s], ((ring - STAGES) >> 1) & 1);
+                unsigned char *as = sA + s * A_STAGE;
+                if (tid == 0) {  // Q tile: one bulk copy, completion counted on full[s]
+                    mbar_arrive_tx(&full[s], B_STAGE);
+                    bulk_g2s(sB + s * B_STAGE, qchunk + (size_t)t * B_STAGE, B_STAGE, &full[s]);
+                }
+                const int jl0 = tin * KT;
 #pragma unroll
-        for (int c8 = 0; c8 < NC / 8; ++c8) {
-            uint32_t v[8];
-            asm volatile(
-                "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
-                : "r"(lane_base + col0 + c8 * 8));
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            if (active) {
+                for (int q4 = 0; q4 < KT / 4; ++q4) {
+                    const float4 *s4 = reinterpret_cast<const float4 *>(sxy + jl0 + q4 * 4);
+                    float g[4];
 #pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    const int ch = chunk * NC + c8 * 8 + e;
-                    if (ch < a.d) {
-                        float f = (float)((double)__uint_as_float(v[e]) + a.qm[ch]);
-                        reinterpret_cast<float *>(a.out)[ch * a.out_cs + lr * a.out_rs + col * a.out_ps] = f;
-                        if (!isfinite(f)) bad = true;
-                        if (a.bands)
-                            a.bands[ch * a.band_cs + lr * a.band_rs + col] = (int32_t)floor((double)f / a.spacing[ch]);
+                    for (int h = 0; h < 2; ++h) {
+                        float4 pp = s4[h];
+                        float dx = pp.x - vx, dy = pp.y - vy;
+                        float w = weight<AM>(dx * dx + dy * dy, neg_alpha);
+                        g[2 * h] = w * (c0 + c1 * dx + c2 * dy);
+                        dx = pp.z - vx;
+                        dy = pp.w - vy;
+                        w = weight<AM>(dx * dx + dy * dy, neg_alpha);
+                        g[2 * h + 1] = w * (c0 + c1 * dx + c2 * dy);
+                    }
+                    uint4 hi, lo;
+                    uint32_t *hp = &hi.x, *lp = &lo.x;
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        uint32_t hb = tf32_hi_bits(g[e]);
+                        hp[e] = hb;
+                        lp[e] = __float_as_uint(g[e] - __uint_as_float(hb));
+                    }
+                    const uint32_t off = cm_off(tid, q4 * 4);
+                    *reinterpret_cast<uint4 *>(as + off) = hi;
+                    *reinterpret_cast<uint4 *>(as + A_HALF + off) = lo;
+                }
+                // make this warp's generic-proxy stores visible to the tensor core
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&full[s]);
+            }
+            // drain: the chunk's last MMAs retire in order
+            {
+                const uint32_t last = ring - 1;
+                mbar_wait(&empty[last & 1], (last >> 1) & 1);
+            }
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+            const uint32_t col0 = tmem + (warp >> 2) * NC;
+#pragma unroll
+            for (int c8 = 0; c8 < NC / 8; ++c8) {
+                uint32_t v[8];
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                    : "r"(lane_base + col0 + c8 * 8));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (active) {
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        const int ch = chunk * NC + c8 * 8 + e;
+                        if (ch < a.d) {
+                            float f = (float)((double)__uint_as_float(v[e]) + a.qm[ch]);
+                            reinterpret_cast<float *>(a.out)[ch * a.out_cs + lr * a.out_rs + col * a.out_ps] = f;
+                            if (!isfinite(f)) bad = true;
+                            if (a.bands)
+                                a.bands[ch * a.band_cs + lr * a.band_rs + col] =
+                                    (int32_t)floor((double)f / a.spacing[ch]);
+                        }
                     }
                 }
             }
+            // TMEM is re-used by the next chunk's first MMA, which the issuer
+            // only starts after every compute warp has arrived on that tile
+            // (i.e. after these tcgen05.ld completed).
+            asm volatile("tcgen05.fence::before_thread_sync;");
         }
-        // TMEM is re-used by the next chunk: every warp must have drained it
-        asm volatile("tcgen05.fence::before_thread_sync;");
-        __syncthreads();
-        asm volatile("tcgen05.fence::after_thread_sync;");
+        if (a.nonfinite && active && bad) atomicAdd(a.nonfinite, 1);
     }
-    if (a.nonfinite && active && bad) atomicAdd(a.nonfinite, 1);
     __syncthreads();
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS));
+    if (issuer) {
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS));
+    }
 }
 
 template <int NC>
 static size_t tc_smem_bytes() {
     return STAGES * (size_t)A_STAGE + STAGES * (size_t)(2 * NC * 64) + TPB * sizeof(float2) +
-           STAGES * sizeof(uint64_t) + 16;
+           2 * STAGES * sizeof(uint64_t) + 16;
 }
 
 static int pick_nc(int d) { return d <= 16 ? 16 : (d <= 32 ? 32 : 64); }
@@ -372,7 +419,7 @@ static int launch_tc_nc(const KArgs &k, void *ws, cudaStream_t s) {
     KArgs kk = k;
     kk.tile0 = kk.p_begin / TPB;
     int64_t blocks = (kk.p_end + TPB - 1) / TPB - kk.tile0;
-    if (blocks > 0) fn<<<(unsigned)blocks, TPB, smem, s>>>(kk, img, ntiles, nchunk);
+    if (blocks > 0) fn<<<(unsigned)blocks, THREADS, smem, s>>>(kk, img, ntiles, nchunk);
     MDC_CHECK_LAUNCH();
     return MDC_OK;
 }
