@@ -23,8 +23,17 @@ namespace mdc {
 namespace tc {
 
 constexpr int TPB = 256;          // threads == pixels per CTA
-constexpr int KT = 16;            // controls per K tile
-constexpr int STAGES = 2;
+#ifndef MDC_TC_KT
+#define MDC_TC_KT 16
+#endif
+#ifndef MDC_TC_STAGES
+#define MDC_TC_STAGES 2
+#endif
+#ifndef MDC_TC_MINB
+#define MDC_TC_MINB 3
+#endif
+constexpr int KT = MDC_TC_KT;          // controls per K tile (multiple of 8 = tcgen05 tf32 K)
+constexpr int STAGES = MDC_TC_STAGES;  // ring depth
 constexpr int A_SBO = (KT / 4) * 128;                  // bytes between 8-row core-matrix groups
 constexpr int A_HALF = (TPB / 8) * A_SBO;              // one of hi/lo: 256 rows x KT
 constexpr int A_STAGE = 2 * A_HALF;
@@ -80,7 +89,7 @@ __device__ __forceinline__ uint32_t cm_off(int m, int k) {
 
 // ---------------------------------------------------------------------------
 // Q -> tiled core-matrix image, hi/lo split.  img[(chunk * ntiles + t)][hi|lo]
-// each half = NC rows (channels) x KT controls = NC * 64 bytes.
+// each half = NC rows (channels) x KT controls = NC * KT * 4 bytes.
 __global__ void q_image_kernel(const float *q, int64_t n, int ldq, int d, int nc, int nchunk, int64_t ntiles,
                                float *img) {
     int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -97,7 +106,7 @@ __global__ void q_image_kernel(const float *q, int64_t n, int ldq, int d, int nc
     float v = (j < n && gch < d) ? q[j * ldq + gch] : 0.0f;
     float hi = __uint_as_float(tf32_hi_bits(v));
     float lo = v - hi;
-    size_t tile_bytes = (size_t)nc * 64;
+    size_t tile_bytes = (size_t)nc * KT * 4;
     char *base = reinterpret_cast<char *>(img) + ((size_t)chunk * ntiles + t) * 2 * tile_bytes;
     uint32_t off = (uint32_t)((ch >> 3) * A_SBO + (k >> 2) * 128 + (ch & 7) * 16 + (k & 3) * 4);
     *reinterpret_cast<float *>(base + off) = hi;
@@ -132,8 +141,8 @@ __device__ __forceinline__ void compute_bar_sync() {  // named barrier over the 
 }
 
 template <int AM, int NC>
-__global__ void __launch_bounds__(THREADS, 3) mls_tc_kernel(KArgs a, const float *qimg, int64_t ntiles, int nchunk) {
-    constexpr int B_HALF = NC * 64;
+__global__ void __launch_bounds__(THREADS, MDC_TC_MINB) mls_tc_kernel(KArgs a, const float *qimg, int64_t ntiles, int nchunk) {
+    constexpr int B_HALF = NC * KT * 4;
     constexpr int B_STAGE = 2 * B_HALF;
     constexpr int TMEM_COLS = (2 * NC <= 32) ? 32 : (2 * NC <= 64 ? 64 : (2 * NC <= 128 ? 128 : 256));
     extern __shared__ __align__(128) unsigned char smem[];
@@ -173,8 +182,8 @@ __global__ void __launch_bounds__(THREADS, 3) mls_tc_kernel(KArgs a, const float
             uint32_t ring = 0;
             for (int chunk = 0; chunk < nchunk; ++chunk) {
                 for (int64_t t = 0; t < ntiles; ++t, ++ring) {
-                    const int s = ring & 1;
-                    mbar_wait(&full[s], (ring >> 1) & 1);
+                    const int s = ring % STAGES;
+                    mbar_wait(&full[s], (ring / STAGES) & 1);
                     asm volatile("tcgen05.fence::after_thread_sync;");
                     unsigned char *as = sA + s * A_STAGE;
                     unsigned char *bs = sB + s * B_STAGE;
@@ -224,17 +233,21 @@ __global__ void __launch_bounds__(THREADS, 3) mls_tc_kernel(KArgs a, const float
 
         // Controls past n are parked far away (weight underflows to 0, G
         // stays finite) and their Q rows are zero: full tiles, no masking.
-        auto stage_xy = [&](int64_t r) {
+        // Positions of round r+1 are fetched while round r is being used.
+        double2 pre = make_double2(0.0, 0.0);
+        auto fetch_xy = [&](int64_t r) {
             int64_t j = r * TPB + tid;
-            float2 v = make_float2(1e18f, 1e18f);
-            if (j < n) {
-                double2 d = reinterpret_cast<const double2 *>(a.pc)[j];
-                v = make_float2((float)(d.x - ox), (float)(d.y - oy));
-            }
+            pre = j < n ? reinterpret_cast<const double2 *>(a.pc)[j] : make_double2(1e300, 1e300);
+        };
+        auto stage_xy = [&](int64_t r) {
+            float2 v = pre.x == 1e300 ? make_float2(1e18f, 1e18f)
+                                      : make_float2((float)(pre.x - ox), (float)(pre.y - oy));
             compute_bar_sync();
             sxy[tid] = v;
             compute_bar_sync();
+            fetch_xy(r + 1 < nxy ? r + 1 : 0);
         };
+        fetch_xy(0);
 
         // ---------------- pass 1: moments (SIMT) ----------------
         float sw = 0.f, mx = 0.f, my = 0.f, sxx = 0.f, sxy_ = 0.f, syy = 0.f;
@@ -298,8 +311,8 @@ __global__ void __launch_bounds__(THREADS, 3) mls_tc_kernel(KArgs a, const float
             for (int64_t t = 0; t < ntiles; ++t, ++ring) {
                 const int tin = (int)(t & (TPB / KT - 1));
                 if (tin == 0) stage_xy(t / (TPB / KT));
-                const int s = ring & 1;
-                if (ring >= STAGES) mbar_wait(&empty[s], ((ring - STAGES) >> 1) & 1);
+                const int s = ring % STAGES;
+                if (ring >= STAGES) mbar_wait(&empty[s], ((ring - STAGES) / STAGES) & 1);
                 unsigned char *as = sA + s * A_STAGE;
                 if (tid == 0) {  // Q tile: one bulk copy, completion counted on full[s]
                     mbar_arrive_tx(&full[s], B_STAGE);
@@ -341,7 +354,7 @@ __global__ void __launch_bounds__(THREADS, 3) mls_tc_kernel(KArgs a, const float
             // drain: the chunk's last MMAs retire in order
             {
                 const uint32_t last = ring - 1;
-                mbar_wait(&empty[last & 1], (last >> 1) & 1);
+                mbar_wait(&empty[last % STAGES], (last / STAGES) & 1);
             }
             asm volatile("tcgen05.fence::after_thread_sync;");
             const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
@@ -385,7 +398,7 @@ __global__ void __launch_bounds__(THREADS, 3) mls_tc_kernel(KArgs a, const float
 
 template <int NC>
 static size_t tc_smem_bytes() {
-    return STAGES * (size_t)A_STAGE + STAGES * (size_t)(2 * NC * 64) + TPB * sizeof(float2) +
+    return STAGES * (size_t)A_STAGE + STAGES * (size_t)(2 * NC * KT * 4) + TPB * sizeof(float2) +
            2 * STAGES * sizeof(uint64_t) + 16;
 }
 
@@ -397,7 +410,7 @@ size_t mls_tc_workspace_bytes(int d, int64_t n) {
     int nc = tc::pick_nc(d);
     int nchunk = (d + nc - 1) / nc;
     int64_t ntiles = (n + tc::KT - 1) / tc::KT;
-    return (size_t)nchunk * ntiles * 2 * nc * 64 + 256;
+    return (size_t)nchunk * ntiles * 2 * nc * tc::KT * 4 + 256;
 }
 
 template <int AM, int NC>
