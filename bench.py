@@ -373,20 +373,35 @@ def main():
     # ---- roofline of the dominant kernel --------------------------------
     peaks = measure_peaks(lib, torch)
     pairs = rows * W * cfg["n"]
-    dc = 1
-    while dc < d and dc < 32:
-        dc *= 2
-    chunks = -(-d // dc)
-    alg_flops = pairs * (19 + 6 * d)               # SURVEY.md §8d per-pair figure
-    exec_flops = pairs * (18 + 12 * chunks + 2 * d)  # what the two-pass kernel executes
-    achieved = alg_flops / (kernel_ms * 1e-3) / 1e12
+    alg_flops = pairs * (19 + 6 * d)  # SURVEY.md §8d per-pair figure (one-pass formulation)
+    use_tc = (not args.no_tc) and d >= 8
+    if use_tc:
+        nc = 16 if d <= 16 else (32 if d <= 32 else 64)
+        chunks = -(-d // nc)
+        fma_instr = pairs * (13 + 10 * chunks)     # SIMT FMA-pipe ops: moments + G evaluation
+        tc_flops = pairs * chunks * 3 * 2 * nc      # 3xTF32 MMAs
+        kname = f"mls_tc_kernel<alpha=1.5, N={nc}> (tcgen05 kind::tf32 3xTF32 pass 2)"
+    else:
+        dc = 1
+        while dc < d and dc < 32:
+            dc *= 2
+        chunks = -(-d // dc)
+        fma_instr = pairs * (13 + 9 * chunks + d)
+        tc_flops = 0
+        kname = f"mls_kernel<float, AFFINE, alpha=1.5, DC={dc}, R=2> (SIMT)"
+    sec = kernel_ms * 1e-3
+    achieved = 2 * fma_instr / sec / 1e12          # FP32-pipe FLOP-equivalents (FMA-pipe op = 2)
     peak = peaks["fp32"] / 1e12
+    tf32_peak = 0.5 * _measured_bf16_tflops()       # dense tf32 = 1/2 bf16 (measured bf16, MEASURED_PEAKS.json)
     roofline = {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak, "traffic": None,
-                "kernel": f"mls_kernel<float, AFFINE, alpha=1.5, DC={dc}, R=2>",
-                "kernel_ms": kernel_ms, "peak_source": "measured FFMA microbenchmark (mdc_peak_ffma), this run",
-                "executed_tflops": exec_flops / (kernel_ms * 1e-3) / 1e12,
-                "executed_frac": exec_flops / (kernel_ms * 1e-3) / peaks["fp32"],
+                "kernel": kname, "kernel_ms": kernel_ms,
+                "achieved_def": "FP32-pipe ops executed (FMA-pipe instruction = 2 FLOP) / kernel time",
+                "peak_source": "measured FFMA microbenchmark (mdc_peak_ffma), this run",
+                "algorithmic_tflops": alg_flops / sec / 1e12,
+                "algorithmic_def": "SURVEY.md §8d 19+6d FLOP per (pixel, control) pair",
+                "tensor_tflops": tc_flops / sec / 1e12 if tc_flops else 0.0,
+                "tensor_peak_tflops": tf32_peak, "tensor_frac": (tc_flops / sec / 1e12) / tf32_peak if tc_flops else 0.0,
                 "fp64_peak_tflops": peaks["fp64"] / 1e12,
                 "kernel_share_of_step": kernel_ms / ms_step}
 
@@ -404,7 +419,7 @@ def main():
         "config": {"workload": workload_name(cfg), "points": cfg["n"], "dims": d, "width": W,
                    "height": H, "layout_iterations": cfg["iters"], "parallelism": f"rowband{world}",
                    "l2": "flushed between frames (256 MiB write)"},
-        "gpu_launches": 5 * args.steps,
+        "gpu_launches": (6 if use_tc else 5) * args.steps,
         "clocks": clk.summary(),
         "roofline": roofline,
         "cpu_baseline": cpu,
@@ -453,6 +468,13 @@ def run_e2e(args, positions, raw, spacing, W, H, d, r0, r1, dev, world):
     return {"value": W * H * d / (e_ms.item() * 1e-3) / 1e6, "unit": UNIT,
             "h2d_bytes_per_step": int(h2d[0]), "d2h_bytes_per_step": int(host_out.numel() * 4),
             "ms_per_step": e_ms.item(), "timing": "wall clock, synchronized, max over ranks"}
+
+
+def _measured_bf16_tflops():
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops"])
+    except (OSError, KeyError, ValueError):
+        return 1590.0  # B200_PROFILING.md fallback
 
 
 def _auto_spacing(values):
