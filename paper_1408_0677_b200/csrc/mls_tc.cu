@@ -15,14 +15,19 @@
 // pre-arranged once per call into the same core-matrix layout (hi/lo), so its
 // tiles are plain contiguous cp.async copies.
 //
-// Tile geometry: CTA = 256 threads = 256 pixels (two M=128 MMA tiles), K-tile
-// = 16 controls; 3 CTAs per SM.
+// Tile geometry (A/B-tuned): CTA = 128 pixels (one M = 128 MMA tile) + an
+// issuer warp, K tile = 16 controls, 2-stage ring, 5 CTAs per SM.
 #include "mls_common.cuh"
 
 namespace mdc {
 namespace tc {
 
-constexpr int TPB = 256;          // threads == pixels per CTA
+#ifndef MDC_TC_TPB
+#define MDC_TC_TPB 128
+#endif
+constexpr int TPB = MDC_TC_TPB;   // compute threads == pixels per CTA (multiple of 128)
+constexpr int MT = TPB / 128;     // M = 128 MMA tiles per CTA
+constexpr int XYR = 256;          // controls per position staging round
 #ifndef MDC_TC_KT
 #define MDC_TC_KT 16
 #endif
@@ -30,12 +35,12 @@ constexpr int TPB = 256;          // threads == pixels per CTA
 #define MDC_TC_STAGES 2
 #endif
 #ifndef MDC_TC_MINB
-#define MDC_TC_MINB 3
+#define MDC_TC_MINB 5
 #endif
 constexpr int KT = MDC_TC_KT;          // controls per K tile (multiple of 8 = tcgen05 tf32 K)
 constexpr int STAGES = MDC_TC_STAGES;  // ring depth
 constexpr int A_SBO = (KT / 4) * 128;                  // bytes between 8-row core-matrix groups
-constexpr int A_HALF = (TPB / 8) * A_SBO;              // one of hi/lo: 256 rows x KT
+constexpr int A_HALF = (TPB / 8) * A_SBO;              // one of hi/lo: TPB rows x KT
 constexpr int A_STAGE = 2 * A_HALF;
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -144,12 +149,14 @@ template <int AM, int NC>
 __global__ void __launch_bounds__(THREADS, MDC_TC_MINB) mls_tc_kernel(KArgs a, const float *qimg, int64_t ntiles, int nchunk) {
     constexpr int B_HALF = NC * KT * 4;
     constexpr int B_STAGE = 2 * B_HALF;
-    constexpr int TMEM_COLS = (2 * NC <= 32) ? 32 : (2 * NC <= 64 ? 64 : (2 * NC <= 128 ? 128 : 256));
+    constexpr int COLS = MT * NC;
+    constexpr int TMEM_COLS = COLS <= 32 ? 32 : (COLS <= 64 ? 64 : (COLS <= 128 ? 128 : 256));
+    constexpr int PER = XYR / TPB;  // staged controls per thread per round
     extern __shared__ __align__(128) unsigned char smem[];
     unsigned char *sA = smem;                                          // STAGES x A_STAGE
     unsigned char *sB = sA + STAGES * A_STAGE;                         // STAGES x B_STAGE
-    float2 *sxy = reinterpret_cast<float2 *>(sB + STAGES * B_STAGE);  // TPB controls
-    uint64_t *full = reinterpret_cast<uint64_t *>(sxy + TPB);         // STAGES: G + Q ready
+    float2 *sxy = reinterpret_cast<float2 *>(sB + STAGES * B_STAGE);  // 2 x XYR controls
+    uint64_t *full = reinterpret_cast<uint64_t *>(sxy + 2 * XYR);     // STAGES: G + Q ready
     uint64_t *empty = full + STAGES;                                   // STAGES: MMAs retired
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(empty + STAGES);
 
@@ -160,7 +167,7 @@ __global__ void __launch_bounds__(THREADS, MDC_TC_MINB) mls_tc_kernel(KArgs a, c
 
     if (tid == 0) {
         for (int s = 0; s < STAGES; ++s) {
-            mbar_init(&full[s], CWARPS + 1);  // 8 compute-warp arrivals + 1 expect_tx arrival
+            mbar_init(&full[s], CWARPS + 1);  // compute-warp arrivals + 1 expect_tx arrival
             mbar_init(&empty[s], 1);          // tcgen05.commit
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -180,6 +187,9 @@ __global__ void __launch_bounds__(THREADS, MDC_TC_MINB) mls_tc_kernel(KArgs a, c
         // ------------------------------ MMA issuer --------------------------
         if (lane == 0) {
             uint32_t ring = 0;
+#ifdef MDC_TC_PASS1_ONLY
+            nchunk = 0;
+#endif
             for (int chunk = 0; chunk < nchunk; ++chunk) {
                 for (int64_t t = 0; t < ntiles; ++t, ++ring) {
                     const int s = ring % STAGES;
@@ -190,7 +200,7 @@ __global__ void __launch_bounds__(THREADS, MDC_TC_MINB) mls_tc_kernel(KArgs a, c
                     const uint32_t a_hi = smem_u32(as), a_lo = smem_u32(as + A_HALF);
                     const uint32_t b_hi = smem_u32(bs), b_lo = smem_u32(bs + B_HALF);
 #pragma unroll
-                    for (int mt = 0; mt < 2; ++mt) {
+                    for (int mt = 0; mt < MT; ++mt) {
                         const uint32_t dcol = tmem + mt * NC;
                         const uint32_t moff = mt * (128 / 8) * A_SBO;
 #pragma unroll
@@ -229,32 +239,47 @@ __global__ void __launch_bounds__(THREADS, MDC_TC_MINB) mls_tc_kernel(KArgs a, c
         pixel_xy(a, p, vxg, vyg);
         const float vx = (float)(vxg - ox), vy = (float)(vyg - oy);
         const int64_t n = a.n;
-        const int64_t nxy = (n + TPB - 1) / TPB;
+        const int64_t nxy = (n + XYR - 1) / XYR;
 
-        // Controls past n are parked far away (weight underflows to 0, G
-        // stays finite) and their Q rows are zero: full tiles, no masking.
-        // Positions of round r+1 are fetched while round r is being used.
-        double2 pre = make_double2(0.0, 0.0);
-        auto fetch_xy = [&](int64_t r) {
-            int64_t j = r * TPB + tid;
-            pre = j < n ? reinterpret_cast<const double2 *>(a.pc)[j] : make_double2(1e300, 1e300);
+        // Control positions stream through a double-buffered staging area,
+        // one named barrier per round.  Controls past n are parked far away
+        // (weight underflows to 0, G stays finite) and their Q rows are zero:
+        // full tiles, no masking.
+        double2 pre[PER];
+        auto fetch = [&](int64_t r) {
+#pragma unroll
+            for (int e = 0; e < PER; ++e) {
+                int64_t j = r * XYR + e * TPB + tid;
+                pre[e] = (r < nxy && j < n) ? reinterpret_cast<const double2 *>(a.pc)[j] : make_double2(1e300, 1e300);
+            }
         };
-        auto stage_xy = [&](int64_t r) {
-            float2 v = pre.x == 1e300 ? make_float2(1e18f, 1e18f)
-                                      : make_float2((float)(pre.x - ox), (float)(pre.y - oy));
-            compute_bar_sync();
-            sxy[tid] = v;
-            compute_bar_sync();
-            fetch_xy(r + 1 < nxy ? r + 1 : 0);
+        auto store = [&](int64_t r) {
+            float2 *buf = sxy + (r & 1) * XYR;
+#pragma unroll
+            for (int e = 0; e < PER; ++e)
+                buf[e * TPB + tid] = pre[e].x == 1e300 ? make_float2(1e18f, 1e18f)
+                                                       : make_float2((float)(pre[e].x - ox), (float)(pre[e].y - oy));
         };
-        fetch_xy(0);
+        auto xy_init = [&]() {
+            compute_bar_sync();
+            fetch(0);
+            store(0);
+            fetch(1);
+        };
+        auto xy_step = [&](int64_t r) {  // make round r readable, stage r + 1, prefetch r + 2
+            compute_bar_sync();
+            if (r + 1 < nxy) store(r + 1);
+            fetch(r + 2);
+        };
 
         // ---------------- pass 1: moments (SIMT) ----------------
         float sw = 0.f, mx = 0.f, my = 0.f, sxx = 0.f, sxy_ = 0.f, syy = 0.f;
+        xy_init();
         for (int64_t r = 0; r < nxy; ++r) {
-            stage_xy(r);
-            const int cnt = (int)min((int64_t)TPB, n - r * TPB);
-            const float4 *s4 = reinterpret_cast<const float4 *>(sxy);
+            xy_step(r);
+            const float2 *buf = sxy + (r & 1) * XYR;
+            const int cnt = (int)min((int64_t)XYR, n - r * XYR);
+            const float4 *s4 = reinterpret_cast<const float4 *>(buf);
             int j = 0;
 #pragma unroll 4
             for (; j + 1 < cnt; j += 2) {
@@ -275,7 +300,7 @@ __global__ void __launch_bounds__(THREADS, MDC_TC_MINB) mls_tc_kernel(KArgs a, c
                 }
             }
             if (j < cnt) {
-                float2 pp = sxy[j];
+                float2 pp = buf[j];
                 float dx = pp.x - vx, dy = pp.y - vy;
                 float w = weight<AM>(dx * dx + dy * dy, neg_alpha);
                 float wdx = w * dx, wdy = w * dy;
@@ -301,16 +326,23 @@ __global__ void __launch_bounds__(THREADS, MDC_TC_MINB) mls_tc_kernel(KArgs a, c
         }
 
         // ---------------- pass 2: G tiles -> ring -> tcgen05 ----------------
+#ifdef MDC_TC_PASS1_ONLY
+        if (c0 == 12345.f) a.nonfinite[0] = 1;  // keep pass 1 alive
+        nchunk = 0;
+#endif
         bool bad = false;
         uint32_t ring = 0;
         const int64_t row = p / a.width;
         const int64_t col = p - row * a.width;
         const int64_t lr = row - a.row0;
+        constexpr int TPR = XYR / KT;  // K tiles per staging round
         for (int chunk = 0; chunk < nchunk; ++chunk) {
             const char *qchunk = reinterpret_cast<const char *>(qimg) + (size_t)chunk * ntiles * B_STAGE;
+            xy_init();
             for (int64_t t = 0; t < ntiles; ++t, ++ring) {
-                const int tin = (int)(t & (TPB / KT - 1));
-                if (tin == 0) stage_xy(t / (TPB / KT));
+                const int tin = (int)(t % TPR);
+                const int64_t round = t / TPR;
+                if (tin == 0) xy_step(round);
                 const int s = ring % STAGES;
                 if (ring >= STAGES) mbar_wait(&empty[s], ((ring - STAGES) / STAGES) & 1);
                 unsigned char *as = sA + s * A_STAGE;
@@ -318,10 +350,10 @@ __global__ void __launch_bounds__(THREADS, MDC_TC_MINB) mls_tc_kernel(KArgs a, c
                     mbar_arrive_tx(&full[s], B_STAGE);
                     bulk_g2s(sB + s * B_STAGE, qchunk + (size_t)t * B_STAGE, B_STAGE, &full[s]);
                 }
-                const int jl0 = tin * KT;
+                const float2 *buf = sxy + (round & 1) * XYR + tin * KT;
 #pragma unroll
                 for (int q4 = 0; q4 < KT / 4; ++q4) {
-                    const float4 *s4 = reinterpret_cast<const float4 *>(sxy + jl0 + q4 * 4);
+                    const float4 *s4 = reinterpret_cast<const float4 *>(buf + q4 * 4);
                     float g[4];
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
@@ -398,7 +430,7 @@ __global__ void __launch_bounds__(THREADS, MDC_TC_MINB) mls_tc_kernel(KArgs a, c
 
 template <int NC>
 static size_t tc_smem_bytes() {
-    return STAGES * (size_t)A_STAGE + STAGES * (size_t)(2 * NC * KT * 4) + TPB * sizeof(float2) +
+    return STAGES * (size_t)A_STAGE + STAGES * (size_t)(2 * NC * KT * 4) + 2 * XYR * sizeof(float2) +
            2 * STAGES * sizeof(uint64_t) + 16;
 }
 
