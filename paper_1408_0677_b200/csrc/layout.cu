@@ -452,6 +452,42 @@ __global__ void com_kernel(DevTree t, int nnodes) {
 }
 
 // ---------------------------------------------------------------------------
+// Small-n sort: one CTA per axis sorts all (key, id) pairs in shared memory
+// (cub::BlockRadixSort, stable -> ties by id), one launch for both axes,
+// instead of 2 x ~10 device-wide radix passes.
+constexpr int BSORT_THREADS = 512;
+constexpr int BSORT_ITEMS = 24;
+constexpr int BSORT_MAX = BSORT_THREADS * BSORT_ITEMS;  // 12288 points
+
+__global__ void __launch_bounds__(BSORT_THREADS) block_sort_kernel(const double *pts, int n, int32_t *xs,
+                                                                   int32_t *ys) {
+    typedef cub::BlockRadixSort<unsigned long long, BSORT_THREADS, BSORT_ITEMS, int32_t> BRS;
+    extern __shared__ __align__(16) unsigned char bsort_smem[];
+    typename BRS::TempStorage &tmp = *reinterpret_cast<typename BRS::TempStorage *>(bsort_smem);
+    const int axis = blockIdx.x;
+    unsigned long long keys[BSORT_ITEMS];
+    int32_t vals[BSORT_ITEMS];
+#pragma unroll
+    for (int e = 0; e < BSORT_ITEMS; ++e) {
+        int i = threadIdx.x * BSORT_ITEMS + e;  // blocked arrangement keeps input (id) order for stability
+        if (i < n) {
+            keys[e] = order_key(pts[2 * i + axis]);
+            vals[e] = i;
+        } else {
+            keys[e] = ~0ULL;  // after every real key (real keys never reach all-ones: NaN excluded)
+            vals[e] = INT32_MAX;
+        }
+    }
+    BRS(tmp).Sort(keys, vals);
+    int32_t *out = axis ? ys : xs;
+#pragma unroll
+    for (int e = 0; e < BSORT_ITEMS; ++e) {
+        int i = threadIdx.x * BSORT_ITEMS + e;
+        if (i < n) out[i] = vals[e];
+    }
+}
+
+// ---------------------------------------------------------------------------
 // The whole level walk as ONE cooperative kernel (grid-wide syncs between
 // phases) instead of ~6 launches per level: per level
 //   phase 1  node stats for this depth; left-flags through each splitting
@@ -461,7 +497,9 @@ __global__ void com_kernel(DevTree t, int nnodes) {
 //   phase 4  stable partition of the other run, copy the rest (grid sync)
 // then leaf sums + leaf-order gather, and centroids.
 namespace cg = cooperative_groups;
-constexpr int BUILD_THREADS = 256;
+constexpr int BUILD_THREADS = 256;   // cooperative (multi-CTA) walk
+constexpr int BUILD_SINGLE_THREADS = 1024;
+constexpr int64_t BUILD_SINGLE_MAX = 2048;  // one CTA walks the tree up to this n (A/B: slower at 10k)
 
 struct BuildArgs {
     const double *pts;
@@ -487,10 +525,21 @@ __device__ __forceinline__ void stats_for(const BuildArgs &a, int node, const in
     t.axis[node] = ey > ex ? 1 : 0;
 }
 
-__global__ void __launch_bounds__(BUILD_THREADS) build_levels_kernel(BuildArgs a) {
-    cg::grid_group grid = cg::this_grid();
+// SINGLE = one CTA does the whole walk (small n): block barriers instead of
+// grid-wide ones, same code otherwise.
+template <int NTH, bool SINGLE>
+__global__ void __launch_bounds__(NTH) build_levels_kernel(BuildArgs a) {
+    constexpr int BUILD_THREADS = NTH;
     typedef cub::BlockReduce<int, BUILD_THREADS> BR;
     typedef cub::BlockScan<int, BUILD_THREADS> BS;
+    struct Sync {
+        __device__ void sync() const {
+            if constexpr (SINGLE)
+                __syncthreads();
+            else
+                cg::this_grid().sync();
+        }
+    } grid;
     __shared__ union {
         typename BR::TempStorage r;
         typename BS::TempStorage s;
@@ -727,7 +776,9 @@ __global__ void __launch_bounds__(BH_WARPS * 32) bh_kernel(int64_t n, DevTree t,
                     for (int q = tp.x; q < tp.y; ++q) {
                         double2 pj = __ldg(sp2 + q);
                         double dx = xi - pj.x, dy = yi - pj.y;
-                        double r2 = fmax(dx * dx + dy * dy, 1e-300);
+                        // + 1e-300 keeps the self term finite (r2 = 0) and is
+                        // absorbed exactly by any r2 > ~1e-284.
+                        double r2 = fma(dx, dx, fma(dy, dy, 1e-300));
                         double y = rsqrt_nr(r2);
                         double w = rcp_nr(r2 * (r2 * y) + eta);
                         fx = fma(w, dx, fx);
@@ -918,14 +969,27 @@ static int build_tree(MdcLayoutPlan *p, const double *pts, cudaStream_t s, const
     Buffers &b = p->b;
     int64_t n = sh.n;
     int nb = (int)((n + 255) / 256);
-    keys_kernel<<<nb, 256, 0, s>>>(pts, n, b.kx, b.ky, b.ids);
-    MDC_CHECK_LAUNCH();
-    size_t bytes = b.cub_bytes;
-    MDC_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(b.cub_tmp, bytes, b.kx, b.kx_out, b.ids, b.xs[0],
-                                                   (int)n, 0, 64, s));
-    bytes = b.cub_bytes;
-    MDC_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(b.cub_tmp, bytes, b.ky, b.ky_out, b.ids, b.ys[0],
-                                                   (int)n, 0, 64, s));
+    if (n <= BSORT_MAX) {
+        size_t smem = sizeof(typename cub::BlockRadixSort<unsigned long long, BSORT_THREADS, BSORT_ITEMS,
+                                                           int32_t>::TempStorage);
+        static bool attr = false;
+        if (!attr) {
+            MDC_CHECK_CUDA(cudaFuncSetAttribute(block_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)smem));
+            attr = true;
+        }
+        block_sort_kernel<<<2, BSORT_THREADS, smem, s>>>(pts, (int)n, b.xs[0], b.ys[0]);
+        MDC_CHECK_LAUNCH();
+    } else {
+        keys_kernel<<<nb, 256, 0, s>>>(pts, n, b.kx, b.ky, b.ids);
+        MDC_CHECK_LAUNCH();
+        size_t bytes = b.cub_bytes;
+        MDC_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(b.cub_tmp, bytes, b.kx, b.kx_out, b.ids, b.xs[0],
+                                                       (int)n, 0, 64, s));
+        bytes = b.cub_bytes;
+        MDC_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(b.cub_tmp, bytes, b.ky, b.ky_out, b.ids, b.ys[0],
+                                                       (int)n, 0, 64, s));
+    }
     BuildArgs ba;
     ba.pts = pts;
     ba.n = n;
@@ -940,9 +1004,14 @@ static int build_tree(MdcLayoutPlan *p, const double *pts, cudaStream_t s, const
     ba.oflag = reinterpret_cast<int32_t *>(b.kx_out);  // free after the sorts
     ba.prefix = reinterpret_cast<int32_t *>(b.kx);
     ba.blocksum = b.blocksum;
-    void *kargs[] = {&ba};
-    MDC_CHECK_CUDA(cudaLaunchCooperativeKernel((const void *)build_levels_kernel, dim3(p->build_blocks),
-                                               dim3(BUILD_THREADS), kargs, 0, s));
+    if (n <= BUILD_SINGLE_MAX) {
+        build_levels_kernel<BUILD_SINGLE_THREADS, true><<<1, BUILD_SINGLE_THREADS, 0, s>>>(ba);
+        MDC_CHECK_LAUNCH();
+    } else {
+        void *kargs[] = {&ba};
+        MDC_CHECK_CUDA(cudaLaunchCooperativeKernel((const void *)build_levels_kernel<BUILD_THREADS, false>,
+                                                   dim3(p->build_blocks), dim3(BUILD_THREADS), kargs, 0, s));
+    }
     int cur = sh.max_depth & 1;
     *perm_out = b.xs[cur];
     return MDC_OK;
@@ -1054,7 +1123,8 @@ extern "C" int mdc_layout_plan_create(const MdcLayoutArgs *a, MdcLayoutPlan **pl
         int dev = 0, sms = 0, per_sm = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, build_levels_kernel, BUILD_THREADS, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, build_levels_kernel<BUILD_THREADS, false>,
+                                                      BUILD_THREADS, 0);
         int want = (int)((p->shape.n + BUILD_THREADS - 1) / BUILD_THREADS);
         p->build_blocks = std::max(1, std::min(std::max(1, per_sm) * sms, want));
         if (p->build_blocks > 1024) p->build_blocks = 1024;  // blocksum capacity below
