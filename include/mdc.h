@@ -123,6 +123,33 @@ MDC_API size_t mdc_snap_workspace_bytes(int32_t width, int32_t rows);
 MDC_API int mdc_mls_snap(const MdcMlsArgs *a, const double *pos, const double *tvals, double eps,
                  void *workspace, void *stream);
 
+/* Isocontour rendering (render.py:91-148): per image, band shading and/or
+ * anti-aliased contour lines with np.gradient gradients, fp64 compositing,
+ * RGBA8 out (images x H x W x 4).  An image is `channels` planes (1: the
+ * CLI's per-dimension render; 2: a two-channel field, bands summed and
+ * coverage maxed over channels).  Plane (img, c) element (r, x) lives at
+ * values[img*img_stride + c*cs + r*rs + x*ps].  colormap: ncolors x 4 fp64
+ * already divided by 255 (render.py:78-82).  Optional coverage (float, images
+ * x H x W) receives line_coverage.  Full frames (np.gradient needs the
+ * neighbouring rows). */
+#define MDC_RENDER_CONTOUR 0
+#define MDC_RENDER_DISCRETE 1
+#define MDC_RENDER_DISCRETE_CONTOUR 2
+typedef struct MdcRenderArgs {
+    int32_t mode, dtype, width, height, nimg, channels;
+    const void *values;
+    int64_t img_stride, cs, rs, ps;
+    const double *spacing;
+    double line_width_px;
+    int32_t line_color[4], background[4];
+    const double *colormap;
+    int32_t ncolors;
+    uint8_t *out;
+    float *coverage;
+} MdcRenderArgs;
+MDC_API int mdc_render(const MdcRenderArgs *a, void *stream);
+
+/* ------------------------------------------------------------------------ */
 /* One-to-one seam replacements of the reference's numba kernels (same
  * arguments and out-parameter convention as _kernels.py, DEVICE pointers,
  * fp64, the reference's own operation order).  npix pixels at (vx, vy),

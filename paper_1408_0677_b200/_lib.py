@@ -61,6 +61,22 @@ class MdcLayoutArgs(ctypes.Structure):
     ]
 
 
+class MdcRenderArgs(ctypes.Structure):
+    _fields_ = [
+        ("mode", _c_i32), ("dtype", _c_i32), ("width", _c_i32), ("height", _c_i32),
+        ("nimg", _c_i32), ("channels", _c_i32),
+        ("values", _vp),
+        ("img_stride", _c_i64), ("cs", _c_i64), ("rs", _c_i64), ("ps", _c_i64),
+        ("spacing", _vp),
+        ("line_width_px", _c_d),
+        ("line_color", _c_i32 * 4), ("background", _c_i32 * 4),
+        ("colormap", _vp),
+        ("ncolors", _c_i32),
+        ("out", _vp),
+        ("coverage", _vp),
+    ]
+
+
 # Every symbol include/mdc.h declares, with its ctypes signature.
 SIGNATURES = {
     "mdc_last_error": (ctypes.c_char_p, []),
@@ -79,6 +95,7 @@ SIGNATURES = {
     "mdc_layout_kdtree": (ctypes.c_int, [_vp, _vp] + [_vp] * 10 + [_vp]),
     "mdc_pca_workspace_bytes": (ctypes.c_size_t, [_c_i64, _c_i32]),
     "mdc_pca": (ctypes.c_int, [_c_i64, _c_i32] + [_vp] * 7 + [_vp]),
+    "mdc_render": (ctypes.c_int, [ctypes.POINTER(MdcRenderArgs), _vp]),
     "mdc_mean_field": (ctypes.c_int, [_c_i64, _vp, _vp, _c_i64, _vp, _vp, _vp, _vp, _c_d, _vp, _vp]),
     "mdc_affine_field": (ctypes.c_int, [_c_i64, _vp, _vp, _c_i64, _vp, _vp, _vp, _vp, _c_d, _c_d, _vp, _vp]),
     "mdc_rigid_field": (ctypes.c_int, [_c_i64, _vp, _vp, _c_i64, _vp, _vp, _vp, _vp, _c_d, _vp, _vp]),

@@ -2,20 +2,24 @@
 
 Mirror of the reference's ``render`` module (render.py:21-283) for the modes
 on the hot path: ``contour``, ``discrete``,
-``discrete+contour``.  Band indices for fields produced by
-``compute_fields(..., band_spacing=...)`` come fused out of the MLS kernel's
-epilogue; this module computes them (and the anti-aliased contour coverage)
-from a ``CoordinateField`` for drop-in callers.  The adaptive / gradient /
-texture modes and the legend are SURVEY.md §8f row 2 (next).
+``discrete+contour`` render on the GPU (``mdc_render``: np.gradient
+gradients, line coverage, band shading, fp64 compositing, RGBA8), both for
+drop-in ``CoordinateField`` callers and for whole ``compute_fields`` blocks
+(``render_fields``).  Band indices also come fused out of the MLS epilogue.
+The adaptive / gradient / texture modes and the legend are SURVEY.md §8f
+row 2 (next).
 """
 
 from __future__ import annotations
 
+import ctypes
 import io
 from dataclasses import dataclass, field
 
 import numpy as np
+import torch
 
+from . import _lib
 from .field import CoordinateField
 
 MODES = ("contour", "discrete", "discrete+contour", "adaptive", "gradient", "texture")
@@ -126,22 +130,75 @@ def _to_image(img: np.ndarray) -> RenderedImage:
     return RenderedImage(width=px.shape[1], height=px.shape[0], pixels=px)
 
 
+_MODE_CODE = {"contour": 0, "discrete": 1, "discrete+contour": 2}
+
+
+def _cmap_tensor(colormap, device) -> torch.Tensor:
+    return torch.as_tensor(np.array([_rgba(c) for c in colormap], dtype=np.float64)).to(device)
+
+
+def render_planes(values: torch.Tensor, strides, nimg: int, channels: int, width: int, height: int,
+                  spacing, spec: RenderSpec, want_coverage: bool = False):
+    """GPU render of ``nimg`` images (mdc_render): RGBA8 (nimg, H, W, 4) and
+    optionally the float coverage (nimg, H, W).  ``strides`` =
+    (img_stride, channel_stride, row_stride, pixel_stride) in elements."""
+    lib = _lib.require_cuda()
+    if spec.mode not in _MODE_CODE:
+        raise RenderError(f"mode {spec.mode!r} is not implemented on the GPU yet (SURVEY.md §8f); use {GPU_MODES}")
+    dev = values.device
+    sp = torch.as_tensor(np.broadcast_to(np.asarray(spacing, dtype=np.float64), (nimg,)).copy()).to(dev)
+    out = torch.empty((nimg, height, width, 4), dtype=torch.uint8, device=dev)
+    cov = torch.empty((nimg, height, width), dtype=torch.float32, device=dev) if want_coverage else None
+    cmap = _cmap_tensor(spec.colormap, dev)
+    a = _lib.MdcRenderArgs()
+    a.mode = _MODE_CODE[spec.mode]
+    a.dtype = _lib.MDC_F32 if values.dtype == torch.float32 else _lib.MDC_F64
+    a.width, a.height, a.nimg, a.channels = width, height, nimg, channels
+    a.values = _lib.ptr(values)
+    a.img_stride, a.cs, a.rs, a.ps = (int(v) for v in strides)
+    a.spacing = _lib.ptr(sp)
+    a.line_width_px = float(spec.line_width_px)
+    lc = list(spec.line_color) + [255] * (4 - len(spec.line_color))
+    bg = list(spec.background) + [255] * (4 - len(spec.background))
+    for k in range(4):
+        a.line_color[k] = int(lc[k])
+        a.background[k] = int(bg[k])
+    a.colormap, a.ncolors = _lib.ptr(cmap), len(spec.colormap)
+    a.out = _lib.ptr(out)
+    a.coverage = _lib.ptr(cov)
+    _lib.check(lib.mdc_render(ctypes.byref(a), _lib.stream_ptr()), "mdc_render")
+    return out, cov
+
+
+def _field_planes(fld: CoordinateField):
+    coords = torch.as_tensor(np.ascontiguousarray(fld.coords, dtype=np.float64)).cuda()
+    w, h = fld.width, fld.height
+    return coords, (0, 1, 2 * w, 2)
+
+
+def render_fields(block, spacing, spec: RenderSpec):
+    """Per-channel isocontour images of a ``compute_fields`` FieldBlock that
+    covers the full frame: (d, H, W, 4) uint8 CUDA tensor."""
+    vals = block.values
+    d, rows, w = vals.shape
+    if block.row0 != 0 or rows != block.transform.height:
+        raise RenderError("render_fields needs a full-frame FieldBlock (np.gradient spans rows)")
+    out, _ = render_planes(vals, (rows * w, 0, w, 1), d, 1, w, rows, spacing, spec)
+    return out
+
+
 def _gradient_magnitudes(fld: CoordinateField) -> np.ndarray:
     jac = fld.jacobian()
     return np.hypot(jac[..., 0], jac[..., 1])
 
 
 def line_coverage(fld: CoordinateField, spacing: float, line_width_px: float) -> np.ndarray:
-    """render.py:116-126."""
-    grads = _gradient_magnitudes(fld)
-    cov = np.zeros(fld.coords.shape[:2])
-    for ch in range(fld.active_channels):
-        vals = fld.coords[..., ch]
-        dist = np.abs(vals - spacing * np.round(vals / spacing))
-        g = grads[..., ch]
-        px = np.where(g > 1e-30, dist / np.where(g > 1e-30, g, 1.0), np.inf)
-        cov = np.maximum(cov, np.clip(0.5 * line_width_px + 0.5 - px, 0.0, 1.0))
-    return cov
+    """render.py:116-126, on the GPU (float32 coverage, fp64 arithmetic)."""
+    coords, strides = _field_planes(fld)
+    spec = RenderSpec(mode="contour", spacing=spacing, line_width_px=line_width_px)
+    _, cov = render_planes(coords, strides, 1, fld.active_channels, fld.width, fld.height, spacing, spec,
+                           want_coverage=True)
+    return cov[0].double().cpu().numpy()
 
 
 def band_indices(fld: CoordinateField, spacing: float) -> np.ndarray:
@@ -155,25 +212,28 @@ def band_indices(fld: CoordinateField, spacing: float) -> np.ndarray:
 _band_indices = band_indices
 
 
+def _render_gpu(fld: CoordinateField, spec: RenderSpec) -> RenderedImage:
+    coords, strides = _field_planes(fld)
+    out, _ = render_planes(coords, strides, 1, fld.active_channels, fld.width, fld.height, spec.spacing, spec)
+    px = out[0].cpu().numpy()
+    return RenderedImage(width=px.shape[1], height=px.shape[0], pixels=px)
+
+
 def render_contours(fld: CoordinateField, spec: RenderSpec) -> RenderedImage:
-    img = _flat(fld.coords.shape[:2], spec.background)
-    _over(img, spec.line_color, line_coverage(fld, spec.spacing, spec.line_width_px))
-    return _to_image(img)
+    """render.py:129-132 on the GPU."""
+    return _render_gpu(fld, RenderSpec(**{**spec.__dict__, "mode": "contour"}))
 
 
 def render_discrete(fld: CoordinateField, spec: RenderSpec) -> RenderedImage:
-    table = np.array([_rgba(c) for c in spec.colormap])
-    img = table[np.mod(band_indices(fld, spec.spacing), len(table))]
-    if spec.mode == "discrete+contour":
-        _over(img, spec.line_color, line_coverage(fld, spec.spacing, spec.line_width_px))
-    return _to_image(img)
+    """render.py:142-148 on the GPU."""
+    mode = spec.mode if spec.mode in ("discrete", "discrete+contour") else "discrete"
+    return _render_gpu(fld, RenderSpec(**{**spec.__dict__, "mode": mode}))
 
 
 def render(fld: CoordinateField, spec: RenderSpec) -> RenderedImage:
-    if spec.mode == "contour":
-        return render_contours(fld, spec)
-    if spec.mode in ("discrete", "discrete+contour"):
-        return render_discrete(fld, spec)
+    """render.py:272-283 for the GPU modes."""
+    if spec.mode in _MODE_CODE:
+        return _render_gpu(fld, spec)
     raise RenderError(f"mode {spec.mode!r} is not implemented yet (SURVEY.md §8f); use {GPU_MODES}")
 
 
