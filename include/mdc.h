@@ -197,6 +197,12 @@ typedef struct MdcLayoutArgs {
     double *dbg_bh;     /* n x 2 Barnes-Hut force            */
     double *dbg_force;  /* n x 2 BH + spring + node-edge      */
     double *dbg_scale;  /* n clamp factor s                   */
+    /* vertex partition for multi-GPU steps: this rank
+     * updates the vertices at kd-tree leaf-order positions
+     * [n*rank/world, n*(rank+1)/world) and writes 0.0 for every other vertex,
+     * so a SUM all-reduce of pos across ranks reassembles the step exactly.
+     * world <= 1: the whole mesh. */
+    int32_t part_rank, part_world;
 } MdcLayoutArgs;
 
 typedef struct MdcLayoutPlan MdcLayoutPlan;

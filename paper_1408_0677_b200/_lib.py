@@ -58,6 +58,7 @@ class MdcLayoutArgs(ctypes.Structure):
         ("workspace", _vp),
         ("workspace_bytes", ctypes.c_size_t),
         ("dbg_bh", _vp), ("dbg_force", _vp), ("dbg_scale", _vp),
+        ("part_rank", _c_i32), ("part_world", _c_i32),
     ]
 
 

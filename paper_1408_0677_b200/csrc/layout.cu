@@ -726,14 +726,14 @@ __device__ __forceinline__ void monopole(const double4 g1, double xi, double yi,
 // monopole is added by exactly one task), then walks its subtree.  The set of
 // interactions per point is exactly the reference's; partial sums per task
 // are combined in task order by the consumer.
-__global__ void __launch_bounds__(BH_WARPS * 32) bh_kernel(int64_t n, DevTree t, double c, double eta,
-                                                           double theta) {
+__global__ void __launch_bounds__(BH_WARPS * 32) bh_kernel(int64_t n, int64_t k0, int64_t k1, DevTree t,
+                                                           double c, double eta, double theta) {
     __shared__ int s_node[BH_WARPS][BH_STACK];
     __shared__ unsigned s_mask[BH_WARPS][BH_STACK];
     const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int task = blockIdx.y;
-    const int64_t k = ((int64_t)blockIdx.x * BH_WARPS + wib) * 32 + lane;
-    const bool valid = k < n;
+    const int64_t k = k0 + ((int64_t)blockIdx.x * BH_WARPS + wib) * 32 + lane;
+    const bool valid = k < k1;
     double xi = 0.0, yi = 0.0;
     if (valid) {
         double2 p = reinterpret_cast<const double2 *>(t.spts)[k];
@@ -822,9 +822,9 @@ __device__ __forceinline__ double2 bh_total(const DevTree &t, int64_t n, int64_t
     return make_double2(fx, fy);
 }
 
-__global__ void bh_combine_kernel(int64_t n, DevTree t, const int32_t *perm, double *out) {
-    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= n) return;
+__global__ void bh_combine_kernel(int64_t n, int64_t k0, int64_t k1, DevTree t, const int32_t *perm, double *out) {
+    int64_t k = k0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= k1) return;
     reinterpret_cast<double2 *>(out)[perm[k]] = bh_total(t, n, k);
 }
 
@@ -841,6 +841,8 @@ struct LocalArgs {
     const double *temps;
     const int32_t *ctr;
     double *dbg_bh, *dbg_force, *dbg_scale;
+    const int32_t *perm;  // partitioned step: vertex = perm[k0 + idx]
+    int64_t k0, k1;
 };
 
 __device__ __forceinline__ double2 ld2(const double *p, int i) {
@@ -849,7 +851,12 @@ __device__ __forceinline__ double2 ld2(const double *p, int i) {
 
 __global__ void local_kernel(LocalArgs a) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= a.n) return;
+    if (a.perm) {
+        if (a.k0 + i >= a.k1) return;
+        i = a.perm[a.k0 + i];
+    } else if (i >= a.n) {
+        return;
+    }
     const double T = a.temps[*a.ctr];
     const double2 pi = ld2(a.pos, (int)i);
     double2 f = ld2(a.bh, (int)i);
@@ -1017,24 +1024,38 @@ static int build_tree(MdcLayoutPlan *p, const double *pts, cudaStream_t s, const
     return MDC_OK;
 }
 
-static int run_bh(MdcLayoutPlan *p, const double *pts, double *out, cudaStream_t s) {
+static void part_range(const MdcLayoutPlan *p, int64_t &k0, int64_t &k1) {
+    int64_t n = p->shape.n;
+    int w = p->a.part_world > 1 ? p->a.part_world : 1;
+    int r = p->a.part_world > 1 ? p->a.part_rank : 0;
+    k0 = n * r / w;
+    k1 = n * (r + 1) / w;
+}
+
+static int run_bh(MdcLayoutPlan *p, const double *pts, double *out, cudaStream_t s,
+                  const int32_t **perm_out = nullptr) {
     const int32_t *perm = nullptr;
     int rc = build_tree(p, pts, s, &perm);
     if (rc) return rc;
-    int64_t n = p->shape.n;
-    int64_t warps = (n + 31) / 32;
-    dim3 grid((unsigned)((warps + BH_WARPS - 1) / BH_WARPS), (unsigned)p->shape.ntask);
-    bh_kernel<<<grid, BH_WARPS * 32, 0, s>>>(n, p->b.t, p->a.c, p->a.eta, p->a.theta);
-    bh_combine_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, p->b.t, perm, out);
+    int64_t n = p->shape.n, k0, k1;
+    part_range(p, k0, k1);
+    int64_t warps = (k1 - k0 + 31) / 32;
+    if (warps > 0) {
+        dim3 grid((unsigned)((warps + BH_WARPS - 1) / BH_WARPS), (unsigned)p->shape.ntask);
+        bh_kernel<<<grid, BH_WARPS * 32, 0, s>>>(n, k0, k1, p->b.t, p->a.c, p->a.eta, p->a.theta);
+        bh_combine_kernel<<<(unsigned)((k1 - k0 + 255) / 256), 256, 0, s>>>(n, k0, k1, p->b.t, perm, out);
+    }
     MDC_CHECK_LAUNCH();
+    if (perm_out) *perm_out = perm;
     return MDC_OK;
 }
 
 static int enqueue_step(MdcLayoutPlan *p, const double *pin, double *pout, const double *temps,
                         cudaStream_t s) {
     int64_t n = p->shape.n;
+    const int32_t *perm = nullptr;
     if (n >= 2) {
-        int rc = run_bh(p, pin, p->b.bh, s);
+        int rc = run_bh(p, pin, p->b.bh, s, &perm);
         if (rc) return rc;
     } else {
         MDC_CHECK_CUDA(cudaMemsetAsync(p->b.bh, 0, sizeof(double) * 2 * (size_t)n, s));
@@ -1058,7 +1079,15 @@ static int enqueue_step(MdcLayoutPlan *p, const double *pin, double *pout, const
     la.dbg_bh = p->a.dbg_bh;
     la.dbg_force = p->a.dbg_force;
     la.dbg_scale = p->a.dbg_scale;
-    local_kernel<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(la);
+    la.perm = nullptr;
+    la.k0 = 0;
+    la.k1 = n;
+    if (p->a.part_world > 1 && perm) {
+        part_range(p, la.k0, la.k1);
+        la.perm = perm;
+        MDC_CHECK_CUDA(cudaMemsetAsync(pout, 0, sizeof(double) * 2 * (size_t)n, s));
+    }
+    if (la.k1 > la.k0) local_kernel<<<(unsigned)((la.k1 - la.k0 + 127) / 128), 128, 0, s>>>(la);
     incr_kernel<<<1, 1, 0, s>>>(p->b.ctr);
     MDC_CHECK_LAUNCH();
     return MDC_OK;

@@ -102,7 +102,7 @@ LEAF_SIZE = 32  # bhtree.py:74 passes leaf_size=32 on the layout path
 class LayoutEngine:
     """Device-resident topology + libmdc plan for one mesh and parameter set."""
 
-    def __init__(self, mesh, params: LayoutParams, device=None, leaf: int = LEAF_SIZE):
+    def __init__(self, mesh, params: LayoutParams, device=None, leaf: int = LEAF_SIZE, part=(0, 1)):
         lib = _lib.require_cuda()
         self.lib = lib
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
@@ -115,6 +115,7 @@ class LayoutEngine:
         self.pos = torch.empty((self.n, 2), dtype=torch.float64, device=dev)
         self.ws = torch.empty(int(lib.mdc_layout_workspace_bytes(self.n, leaf)), dtype=torch.uint8, device=dev)
         self.leaf = leaf
+        self.part = (int(part[0]), int(part[1]))
         self._plans = {}
         self.temps = None
 
@@ -128,6 +129,7 @@ class LayoutEngine:
         a.tris, a.inc_off, a.inc = _lib.ptr(self.topo["tris"]), _lib.ptr(self.topo["inc_off"]), _lib.ptr(self.topo["inc"])
         a.pos = _lib.ptr(self.pos)
         a.workspace, a.workspace_bytes = _lib.ptr(self.ws), self.ws.numel()
+        a.part_rank, a.part_world = self.part
         if dbg is not None:
             a.dbg_bh, a.dbg_force, a.dbg_scale = (_lib.ptr(t) for t in dbg)
         return a
@@ -238,6 +240,30 @@ def layout_debug_step(mesh, pos: np.ndarray, params: LayoutParams, temperature: 
     eng.run(np.array([temperature]), use_graph=False, debug=True)
     bh, force, s = (t.cpu().numpy() for t in eng.dbg)
     return eng.pos.cpu().numpy(), bh, force, s
+
+
+def layout_run_partitioned(mesh, params: LayoutParams, group=None) -> LayoutState:
+    """layout_run with the vertices partitioned over the ranks of ``group``
+    (SURVEY.md §8e, config 4): every rank rebuilds the kd-tree from the full
+    snapshot, updates its leaf-order slice of the vertices, and one SUM
+    all-reduce per iteration (non-owned entries are exactly 0.0) reassembles
+    the step -- bit-identical to the single-GPU trajectory."""
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    state = initial_state(mesh, params)
+    k = params.iterations
+    temps = temperature_schedule(state.temperature, params.decay_lambda, k + 1)
+    eng = LayoutEngine(mesh, params, part=(rank, world))
+    eng.set_positions(mesh.current_pos)
+    for it in range(k):
+        eng.run(temps[it:it + 1], use_graph=True)
+        if world > 1:
+            dist.all_reduce(eng.pos, op=dist.ReduceOp.SUM, group=group)
+    mesh.current_pos = eng.pos.cpu().numpy()
+    return LayoutState(mesh=mesh, iteration=k, temperature=float(temps[k]) if k else params.initial_temp,
+                       relaxed_pos=mesh.current_pos.copy())
 
 
 def interpolate_layout(state: LayoutState, t: float) -> np.ndarray:
