@@ -15,6 +15,7 @@ build/%.o: $(PKG)/csrc/%.cu $(wildcard $(PKG)/csrc/*.cuh) include/mdc.h
 
 # the seam kernels mirror numba's operation order: no FMA contraction
 build/seam.o: NVFLAGS += -fmad=false
+build/linear.o: NVFLAGS += -fmad=false
 
 $(PKG)/libmdc.so: $(OBJ)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJ)

@@ -123,6 +123,32 @@ MDC_API size_t mdc_snap_workspace_bytes(int32_t width, int32_t rows);
 MDC_API int mdc_mls_snap(const MdcMlsArgs *a, const double *pos, const double *tvals, double eps,
                  void *workspace, void *stream);
 
+/* ------------------------------------------------------------------------ */
+/* Linear variant (field._linear_field, field.py:497-515): rows [row0,row1) of
+ * the raster get the barycentric blend of the lowest-index covering triangle
+ * (_kernels.rasterize_linear, _kernels.py:233-269), else the plane of the
+ * nearest hull triangle (_kernels.extend_hull, _kernels.py:272-313).
+ * pos (n x 2 fp64, un-centred), tvals (n x nch fp64), tris (ntri x 3 int32),
+ * hull (nhull x 3 int32: u, v, triangle in field._hull_edges order).  out in
+ * `dtype` with the MdcMlsArgs stride convention.  workspace:
+ * mdc_linear_workspace_bytes(width, rows) bytes of int32 INT32_MAX on first
+ * use; the call leaves it in that state. */
+typedef struct MdcLinearArgs {
+    int32_t width, height, row0, row1;
+    double x0, y1, sx, sy;
+    int64_t n, ntri;
+    int32_t nch, dtype;
+    const double *pos, *tvals;
+    const int32_t *tris, *hull;
+    int32_t nhull;
+    void *out;
+    int64_t out_cs, out_rs, out_ps;
+    void *workspace;
+} MdcLinearArgs;
+MDC_API size_t mdc_linear_workspace_bytes(int32_t width, int32_t rows);
+MDC_API int mdc_linear_field(const MdcLinearArgs *a, void *stream);
+
+/* ------------------------------------------------------------------------ */
 /* Isocontour rendering (render.py:91-148): per image, band shading and/or
  * anti-aliased contour lines with np.gradient gradients, fp64 compositing,
  * RGBA8 out (images x H x W x 4).  An image is `channels` planes (1: the

@@ -524,3 +524,81 @@ EXPORT void orc_jacobi_eigh(int64_t d, double *a, double *evals, double *evecs) 
     }
     for (int64_t i = 0; i < d; ++i) evals[i] = a[i * d + i];
 }
+
+/* ------------------------------------------------------------------------- */
+/* Linear variant: _kernels.py:233-313 `rasterize_linear` (serial, first
+ * triangle wins) + `extend_hull` (nearest hull segment, strict <, hull order),
+ * as driven by field._linear_field (field.py:497-515).  out (h, w, nch),
+ * tvals (n, nch); hull arrays from field._hull_edges order. */
+EXPORT void orc_linear_field(int64_t n, const double *pos, const double *tvals, int64_t nch, int64_t ntri,
+                             const int64_t *tris, int64_t nh, const int64_t *hull_u, const int64_t *hull_v,
+                             const int64_t *hull_t, double x0, double y1, double sx, double sy, int64_t w,
+                             int64_t h, double *out) {
+    unsigned char *assigned = (unsigned char *)calloc((size_t)(w * h), 1);
+    for (int64_t t = 0; t < ntri; ++t) {
+        int64_t ia = tris[3 * t], ib = tris[3 * t + 1], ic = tris[3 * t + 2];
+        double ax = pos[2 * ia], ay = pos[2 * ia + 1], bx = pos[2 * ib], by = pos[2 * ib + 1];
+        double cx = pos[2 * ic], cy = pos[2 * ic + 1];
+        double det = (bx - ax) * (cy - ay) - (by - ay) * (cx - ax);
+        if (det == 0.0) continue;
+        double xlo = fmin(ax, fmin(bx, cx)), xhi = fmax(ax, fmax(bx, cx));
+        double ylo = fmin(ay, fmin(by, cy)), yhi = fmax(ay, fmax(by, cy));
+        int64_t c0 = (int64_t)floor((xlo - x0) / sx - 0.5); if (c0 < 0) c0 = 0;
+        int64_t c1 = (int64_t)ceil((xhi - x0) / sx); if (c1 > w - 1) c1 = w - 1;
+        int64_t r0 = (int64_t)floor((y1 - yhi) / sy - 0.5); if (r0 < 0) r0 = 0;
+        int64_t r1 = (int64_t)ceil((y1 - ylo) / sy); if (r1 > h - 1) r1 = h - 1;
+        for (int64_t row = r0; row <= r1; ++row) {
+            double gy = y1 - ((double)row + 0.5) * sy;
+            for (int64_t col = c0; col <= c1; ++col) {
+                if (assigned[row * w + col]) continue;
+                double gx = x0 + ((double)col + 0.5) * sx;
+                double l1 = ((bx - gx) * (cy - gy) - (by - gy) * (cx - gx)) / det;
+                double l2 = ((cx - gx) * (ay - gy) - (cy - gy) * (ax - gx)) / det;
+                double l3 = 1.0 - l1 - l2;
+                if (l1 >= -1e-12 && l2 >= -1e-12 && l3 >= -1e-12) {
+                    assigned[row * w + col] = 1;
+                    for (int64_t k = 0; k < nch; ++k)
+                        out[(row * w + col) * nch + k] =
+                            l1 * tvals[ia * nch + k] + l2 * tvals[ib * nch + k] + l3 * tvals[ic * nch + k];
+                }
+            }
+        }
+    }
+#pragma omp parallel for schedule(dynamic, 4)
+    for (int64_t row = 0; row < h; ++row) {
+        double gy = y1 - ((double)row + 0.5) * sy;
+        for (int64_t col = 0; col < w; ++col) {
+            if (assigned[row * w + col]) continue;
+            double gx = x0 + ((double)col + 0.5) * sx;
+            double best = INFINITY;
+            int64_t best_t = 0;
+            for (int64_t k = 0; k < nh; ++k) {
+                double axp = pos[2 * hull_u[k]], ayp = pos[2 * hull_u[k] + 1];
+                double bxp = pos[2 * hull_v[k]], byp = pos[2 * hull_v[k] + 1];
+                double ex = bxp - axp, ey = byp - ayp, ee = ex * ex + ey * ey, s = 0.0;
+                if (ee > 0.0) {
+                    s = ((gx - axp) * ex + (gy - ayp) * ey) / ee;
+                    if (s < 0.0) s = 0.0;
+                    else if (s > 1.0) s = 1.0;
+                }
+                double ddx = gx - (axp + s * ex), ddy = gy - (ayp + s * ey);
+                double d2 = ddx * ddx + ddy * ddy;
+                if (d2 < best) {
+                    best = d2;
+                    best_t = hull_t[k];
+                }
+            }
+            int64_t ia = tris[3 * best_t], ib = tris[3 * best_t + 1], ic = tris[3 * best_t + 2];
+            double ax = pos[2 * ia], ay = pos[2 * ia + 1], bx = pos[2 * ib], by = pos[2 * ib + 1];
+            double cx = pos[2 * ic], cy = pos[2 * ic + 1];
+            double det = (bx - ax) * (cy - ay) - (by - ay) * (cx - ax);
+            double l1 = ((bx - gx) * (cy - gy) - (by - gy) * (cx - gx)) / det;
+            double l2 = ((cx - gx) * (ay - gy) - (cy - gy) * (ax - gx)) / det;
+            double l3 = 1.0 - l1 - l2;
+            for (int64_t k = 0; k < nch; ++k)
+                out[(row * w + col) * nch + k] =
+                    l1 * tvals[ia * nch + k] + l2 * tvals[ib * nch + k] + l3 * tvals[ic * nch + k];
+        }
+    }
+    free(assigned);
+}

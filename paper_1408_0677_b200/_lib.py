@@ -62,6 +62,21 @@ class MdcLayoutArgs(ctypes.Structure):
     ]
 
 
+class MdcLinearArgs(ctypes.Structure):
+    _fields_ = [
+        ("width", _c_i32), ("height", _c_i32), ("row0", _c_i32), ("row1", _c_i32),
+        ("x0", _c_d), ("y1", _c_d), ("sx", _c_d), ("sy", _c_d),
+        ("n", _c_i64), ("ntri", _c_i64),
+        ("nch", _c_i32), ("dtype", _c_i32),
+        ("pos", _vp), ("tvals", _vp),
+        ("tris", _vp), ("hull", _vp),
+        ("nhull", _c_i32),
+        ("out", _vp),
+        ("out_cs", _c_i64), ("out_rs", _c_i64), ("out_ps", _c_i64),
+        ("workspace", _vp),
+    ]
+
+
 class MdcRenderArgs(ctypes.Structure):
     _fields_ = [
         ("mode", _c_i32), ("dtype", _c_i32), ("width", _c_i32), ("height", _c_i32),
@@ -97,6 +112,8 @@ SIGNATURES = {
     "mdc_pca_workspace_bytes": (ctypes.c_size_t, [_c_i64, _c_i32]),
     "mdc_pca": (ctypes.c_int, [_c_i64, _c_i32] + [_vp] * 7 + [_vp]),
     "mdc_render": (ctypes.c_int, [ctypes.POINTER(MdcRenderArgs), _vp]),
+    "mdc_linear_workspace_bytes": (ctypes.c_size_t, [_c_i32, _c_i32]),
+    "mdc_linear_field": (ctypes.c_int, [ctypes.POINTER(MdcLinearArgs), _vp]),
     "mdc_mean_field": (ctypes.c_int, [_c_i64, _vp, _vp, _c_i64, _vp, _vp, _vp, _vp, _c_d, _vp, _vp]),
     "mdc_affine_field": (ctypes.c_int, [_c_i64, _vp, _vp, _c_i64, _vp, _vp, _vp, _vp, _c_d, _c_d, _vp, _vp]),
     "mdc_rigid_field": (ctypes.c_int, [_c_i64, _vp, _vp, _c_i64, _vp, _vp, _vp, _vp, _c_d, _vp, _vp]),

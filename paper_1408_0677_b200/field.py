@@ -171,6 +171,68 @@ def field_gradient(fld: CoordinateField, x: int, y: int) -> np.ndarray:
 
 
 _SNAP_WS: dict[int, torch.Tensor] = {}
+_LIN_WS: dict[int, torch.Tensor] = {}
+
+
+def hull_edges(tris: np.ndarray) -> np.ndarray:
+    """field.py:440-447 `_hull_edges`, vectorised: (u, v, triangle) per
+    boundary edge, u < v, in first-appearance order over triangles' edges
+    (a, b), (b, c), (c, a)."""
+    tris = np.asarray(tris, dtype=np.int64).reshape(-1, 3)
+    e = np.stack([tris[:, [0, 1]], tris[:, [1, 2]], tris[:, [2, 0]]], axis=1).reshape(-1, 2)
+    key = np.sort(e, axis=1)
+    uniq, first, counts = np.unique(key, axis=0, return_index=True, return_counts=True)
+    keep = counts == 1
+    order = np.argsort(first[keep], kind="stable")
+    sel = uniq[keep][order]
+    tri = first[keep][order] // 3
+    return np.column_stack([sel, tri]).astype(np.int64)
+
+
+def _linear_workspace(nbytes: int, device: torch.device) -> torch.Tensor:
+    key = device.index if device.index is not None else torch.cuda.current_device()
+    ws = _LIN_WS.get(key)
+    if ws is None or ws.numel() * 4 < nbytes:
+        ws = torch.full((max(nbytes // 4, 1),), 2**31 - 1, dtype=torch.int32, device=device)
+        _LIN_WS[key] = ws
+    return ws
+
+
+def linear_device(positions, tvals, triangles, width, height, row_range=None, dtype="f64", out=None,
+                  strides=None):
+    """The 'linear' variant (field.py:497-515) on the GPU (mdc_linear_field).
+    Returns the output tensor ((nch, rows, W) unless ``out``/``strides``)."""
+    lib = _lib.require_cuda()
+    pos = np.ascontiguousarray(positions, dtype=np.float64)
+    tv = np.ascontiguousarray(tvals, dtype=np.float64)
+    if tv.ndim == 1:
+        tv = tv[:, None]
+    tris = np.asarray(triangles, dtype=np.int64).reshape(-1, 3)
+    hull = hull_edges(tris)
+    tr = ViewportTransform.fit(pos, width, height)
+    sx, sy = tr.units_per_px
+    r0, r1 = (0, height) if row_range is None else (int(row_range[0]), int(row_range[1]))
+    dev = torch.device("cuda", torch.cuda.current_device())
+    dcode = _resolve_dtype(dtype)
+    nch = tv.shape[1]
+    if out is None:
+        out = torch.empty((nch, r1 - r0, width), dtype=torch.float32 if dcode == _lib.MDC_F32 else torch.float64,
+                          device=dev)
+        strides = ((r1 - r0) * width, width, 1)
+    t_pos, t_tv = _h2d(pos, dev), _h2d(tv, dev)
+    t_tris, t_hull = _h2d(tris.astype(np.int32), dev), _h2d(hull.astype(np.int32), dev)
+    ws = _linear_workspace(int(lib.mdc_linear_workspace_bytes(width, r1 - r0)), dev)
+    a = _lib.MdcLinearArgs()
+    a.width, a.height, a.row0, a.row1 = width, height, r0, r1
+    a.x0, a.y1, a.sx, a.sy = tr.x0, tr.y1, sx, sy
+    a.n, a.ntri, a.nch, a.dtype = len(pos), len(tris), nch, dcode
+    a.pos, a.tvals, a.tris, a.hull = _lib.ptr(t_pos), _lib.ptr(t_tv), _lib.ptr(t_tris), _lib.ptr(t_hull)
+    a.nhull = len(hull)
+    a.out = _lib.ptr(out)
+    a.out_cs, a.out_rs, a.out_ps = (int(v) for v in strides)
+    a.workspace = _lib.ptr(ws)
+    _lib.check(lib.mdc_linear_field(ctypes.byref(a), _lib.stream_ptr()), "mdc_linear_field")
+    return out, tr
 
 
 def _snap_workspace(nbytes: int, device: torch.device) -> torch.Tensor:
@@ -338,7 +400,7 @@ def compute_fields(positions, targets, params: MlsParams, width: int, height: in
     Returns a FieldBlock of device tensors (rows [row0, row1) only).
     """
     if params.variant == "linear":
-        raise FieldError("the linear variant is not on the GPU path yet (SURVEY.md §8f)")
+        raise FieldError("compute_fields(variant='linear') needs the mesh: use linear_device")
     prob = problem or MlsProblem(positions, targets, params.variant, width, height,
                                  alpha=params.resolved_alpha, reg_eps=params.reg_eps,
                                  epsilon_dist=params.epsilon_dist, dtype=dtype, axis=axis,
@@ -367,10 +429,22 @@ def compute_field(mesh, positions: np.ndarray, targets: TargetAssignment, params
     the fp64 parity mode (default) or the fp32 throughput mode."""
     if params.variant == "rigid" and targets.active_channels == 1:
         raise FieldError("rigid MLS is degenerate for single-dimension targets; use mean or affine")
-    if params.variant == "linear":
-        raise FieldError("the linear variant is not on the GPU path yet (SURVEY.md §8f)")
     positions = np.asarray(positions, dtype=np.float64)
     tvals = targets.targets.astype(float)
+    if params.variant == "linear":
+        dev = torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else None
+        if dev is None:
+            _lib.require_cuda()
+        tdt = torch.float32 if _resolve_dtype(dtype) == _lib.MDC_F32 else torch.float64
+        out = torch.empty((height, width, 2), dtype=tdt, device=dev)
+        _, tr = linear_device(positions, tvals, mesh.triangles, width, height, dtype=dtype, out=out,
+                              strides=(1, 2 * width, 2))
+        coords = out.double().cpu().numpy()
+        if not np.all(np.isfinite(coords)):
+            raise FieldError("field evaluation produced non-finite coordinates")
+        return CoordinateField(width=width, height=height, coords=coords,
+                               source_positions=positions, transform=tr,
+                               active_channels=targets.active_channels)
     prob = MlsProblem(positions, tvals, params.variant, width, height, alpha=params.resolved_alpha,
                       reg_eps=params.reg_eps, epsilon_dist=params.epsilon_dist, dtype=dtype,
                       axis=[0, 1])

@@ -139,6 +139,9 @@ def main():
         ("mean_proj", "mean", None, ("projection", ())),
         ("rigid_proj", "rigid", 1.0, ("projection", ())),
         ("rigid_proj_a15", "rigid", 1.5, ("projection", ())),
+        ("linear_dim0", "linear", None, ("dims", (0,))),
+        ("linear_proj", "linear", None, ("projection", ())),
+        ("linear_dims13", "linear", None, ("dims", (1, 3))),
     ]
     for name, variant, alpha, (mode, dims) in cases:
         if mode == "projection":
@@ -178,6 +181,8 @@ def main():
     g["field_affine_dim0"] = fld.coords
     g["targets_affine_dim0"] = tg.targets
     g["field_positions"] = states[5]
+    fld = F.compute_field(mesh, states[5], tg, F.MlsParams(variant="linear"), 120, 90)
+    g["field_linear_dim0"] = fld.coords
     out["g2k"] = g
 
     # ---- scene g10k: config-2 data (10000 x 16, seed 2) ------------------

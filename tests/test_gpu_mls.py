@@ -166,3 +166,24 @@ def test_tensor_core_row_bands_bit_identical(c1):
     parts = [F.compute_fields(pos, raw, F.MlsParams("affine"), W, H, dtype="f32", row_range=rr).values.cpu()
              for rr in ((0, 5), (5, 33), (33, H))]
     assert torch.equal(torch.cat(parts, dim=1), full)
+
+
+def test_linear_variant_bit_exact(c1, g2k):
+    """rasterize_linear + extend_hull on the GPU: same IEEE sequence as numba
+    (no FMA), first-wins via atomicMin -> bit-exact fields."""
+    W, H = (int(v) for v in c1["field_wh"])
+    m = golden_mesh(c1)
+    for name in ("linear_dim0", "linear_proj", "linear_dims13"):
+        fld = F.compute_field(m, c1["field_positions"], _targets(c1, name), F.MlsParams("linear"), W, H)
+        assert np.array_equal(fld.coords, c1[f"field_{name}"]), name
+    fld = F.compute_field(golden_mesh(g2k), g2k["field_positions"],
+                          F.TargetAssignment(g2k["targets_affine_dim0"], "dims", ("a",)),
+                          F.MlsParams("linear"), 120, 90)
+    assert np.array_equal(fld.coords, g2k["field_linear_dim0"])
+
+
+def test_linear_row_bands(g2k):
+    pos, tv = g2k["field_positions"], g2k["targets_affine_dim0"]
+    full, _ = F.linear_device(pos, tv, g2k["triangles"], 120, 90)
+    parts = [F.linear_device(pos, tv, g2k["triangles"], 120, 90, row_range=rr)[0] for rr in ((0, 31), (31, 90))]
+    assert torch.equal(torch.cat(parts, dim=1), full)

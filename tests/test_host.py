@@ -29,7 +29,8 @@ def test_library_exports_every_header_symbol():
 
 def test_ctypes_structs_match_header_field_order():
     txt = open(os.path.join(ROOT, "include", "mdc.h")).read()
-    for cname, py in (("MdcMlsArgs", _lib.MdcMlsArgs), ("MdcLayoutArgs", _lib.MdcLayoutArgs)):
+    for cname, py in (("MdcMlsArgs", _lib.MdcMlsArgs), ("MdcLayoutArgs", _lib.MdcLayoutArgs),
+                      ("MdcRenderArgs", _lib.MdcRenderArgs), ("MdcLinearArgs", _lib.MdcLinearArgs)):
         body = re.search(r"typedef struct %s \{(.*?)\} %s;" % (cname, cname), txt, re.S).group(1)
         body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
         names = []
@@ -38,7 +39,7 @@ def test_ctypes_structs_match_header_field_order():
             if not decl:
                 continue
             decl = re.sub(r"^(const\s+)?\w+\s*", "", decl)
-            names += [n.strip().lstrip("*").strip() for n in decl.split(",")]
+            names += [re.sub(r"\[.*\]", "", n).strip().lstrip("*").strip() for n in decl.split(",")]
         assert names == [f[0] for f in py._fields_], cname
 
 

@@ -12,9 +12,15 @@ def test_oracle_mls_fields_bit_exact(c1):
     W, H = (int(v) for v in c1["field_wh"])
     for name, var, a in zip(c1["field_cases"], c1["field_variants"], c1["field_alphas"]):
         got = O.compute_field(pos, c1[f"targets_{name}"], str(var), W, H,
-                              alpha=None if np.isnan(a) else float(a))
+                              alpha=None if np.isnan(a) else float(a), tris=c1["triangles"])
         # numba kernels and the C restatement perform the same IEEE sequence
         assert np.array_equal(got, c1[f"field_{name}"]), name
+
+
+def test_oracle_linear_larger(g2k):
+    got = O.compute_field(g2k["field_positions"], g2k["targets_affine_dim0"], "linear", 120, 90,
+                          tris=g2k["triangles"])
+    assert np.array_equal(got, g2k["field_linear_dim0"])
 
 
 def test_oracle_bands_and_coverage(c1):
