@@ -158,6 +158,20 @@ def test_tensor_core_path_vs_oracle_and_simt(n, d, W, H, alpha):
         assert normwise(vt[k], vs[k]) <= FP32_TOL
 
 
+def test_fp32_accuracy_margin(c1):
+    """The fp32 kernels (tcgen05 and SIMT) must sit well inside the 1e-4
+    contract on the reference's own fields."""
+    pos = c1["field_positions"]
+    W, H = (int(v) for v in c1["field_wh"])
+    raw = np.tile(c1["raw"], (1, 4))
+    errs = {}
+    for tag, kw in (("tc", {}), ("simt", {"tensor_cores": False})):
+        v = F.compute_fields(pos, raw, F.MlsParams("affine"), W, H, dtype="f32", **kw).values.double().cpu().numpy()
+        errs[tag] = max(normwise(v[k], c1[f"field_affine_dim{k}"][..., 0]) for k in range(4))
+    print("fp32 normwise errors:", errs)
+    assert max(errs.values()) <= 1e-5
+
+
 def test_tensor_core_row_bands_bit_identical(c1):
     pos = c1["field_positions"]
     W, H = (int(v) for v in c1["field_wh"])
