@@ -161,6 +161,9 @@ MDC_API int mdc_linear_field(const MdcLinearArgs *a, void *stream);
 #define MDC_RENDER_CONTOUR 0
 #define MDC_RENDER_DISCRETE 1
 #define MDC_RENDER_DISCRETE_CONTOUR 2
+#define MDC_RENDER_ADAPTIVE 3  /* render.py:151-178, octaves -3..3 */
+#define MDC_RENDER_GRADIENT 4  /* render.py:181-201, needs channels == 2 */
+#define MDC_RENDER_TEXTURE 5   /* render.py:204-234, RGBA8 texture tex_h x tex_w */
 typedef struct MdcRenderArgs {
     int32_t mode, dtype, width, height, nimg, channels;
     const void *values;
@@ -172,8 +175,22 @@ typedef struct MdcRenderArgs {
     int32_t ncolors;
     uint8_t *out;
     float *coverage;
+    int32_t gradient_corners[16];   /* c00, c10, c01, c11 RGBA */
+    double adaptive_target_px;
+    const uint8_t *texture;
+    int32_t tex_w, tex_h;
 } MdcRenderArgs;
 MDC_API int mdc_render(const MdcRenderArgs *a, void *stream);
+
+/* Point overlay (render.py:237-257): anti-aliased discs of radius r at the
+ * n projected points (pix: device n x 2 fp64 pixel coordinates =
+ * ViewportTransform.to_pixels), composited onto img (device H x W x 4 RGBA8,
+ * in place) in point order.  color: HOST pointer to 4 ints (RGBA).
+ * workspace: mdc_overlay_workspace_bytes(n, r) device bytes. */
+MDC_API size_t mdc_overlay_workspace_bytes(int64_t n, double radius);
+MDC_API int mdc_overlay_points(uint8_t *img, int32_t width, int32_t height, int64_t n, const double *pix,
+                               double radius, const int32_t *color, void *workspace, size_t workspace_bytes,
+                               void *stream);
 
 /* ------------------------------------------------------------------------ */
 /* One-to-one seam replacements of the reference's numba kernels (same

@@ -90,6 +90,10 @@ class MdcRenderArgs(ctypes.Structure):
         ("ncolors", _c_i32),
         ("out", _vp),
         ("coverage", _vp),
+        ("gradient_corners", _c_i32 * 16),
+        ("adaptive_target_px", _c_d),
+        ("texture", _vp),
+        ("tex_w", _c_i32), ("tex_h", _c_i32),
     ]
 
 
@@ -113,6 +117,8 @@ SIGNATURES = {
     "mdc_pca": (ctypes.c_int, [_c_i64, _c_i32] + [_vp] * 7 + [_vp]),
     "mdc_render": (ctypes.c_int, [ctypes.POINTER(MdcRenderArgs), _vp]),
     "mdc_linear_workspace_bytes": (ctypes.c_size_t, [_c_i32, _c_i32]),
+    "mdc_overlay_workspace_bytes": (ctypes.c_size_t, [_c_i64, _c_d]),
+    "mdc_overlay_points": (ctypes.c_int, [_vp, _c_i32, _c_i32, _c_i64, _vp, _c_d, _vp, _vp, ctypes.c_size_t, _vp]),
     "mdc_linear_field": (ctypes.c_int, [ctypes.POINTER(MdcLinearArgs), _vp]),
     "mdc_mean_field": (ctypes.c_int, [_c_i64, _vp, _vp, _c_i64, _vp, _vp, _vp, _vp, _c_d, _vp, _vp]),
     "mdc_affine_field": (ctypes.c_int, [_c_i64, _vp, _vp, _c_i64, _vp, _vp, _vp, _vp, _c_d, _c_d, _vp, _vp]),

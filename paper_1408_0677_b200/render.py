@@ -1,13 +1,13 @@
 """Field-to-pixels mappings (contour lines, discrete bands, point overlay).
 
-Mirror of the reference's ``render`` module (render.py:21-283) for the modes
-on the hot path: ``contour``, ``discrete``,
-``discrete+contour`` render on the GPU (``mdc_render``: np.gradient
-gradients, line coverage, band shading, fp64 compositing, RGBA8), both for
-drop-in ``CoordinateField`` callers and for whole ``compute_fields`` blocks
-(``render_fields``).  Band indices also come fused out of the MLS epilogue.
-The adaptive / gradient / texture modes and the legend are SURVEY.md §8f
-row 2 (next).
+Mirror of the reference's ``render`` module (render.py:21-318).  Every
+render mode -- contour, discrete, discrete+contour,
+adaptive, gradient, texture (§8f row 2) -- runs on the GPU (``mdc_render``:
+np.gradient gradients, line coverage, band shading, fp64 compositing,
+RGBA8), for drop-in ``CoordinateField`` callers and whole ``compute_fields``
+blocks (``render_fields``); the point overlay too (``mdc_overlay_points``).
+Band indices also come fused out of the MLS epilogue.  The legend strip
+(text via PIL) stays on the host.
 """
 
 from __future__ import annotations
@@ -23,7 +23,7 @@ from . import _lib
 from .field import CoordinateField
 
 MODES = ("contour", "discrete", "discrete+contour", "adaptive", "gradient", "texture")
-GPU_MODES = ("contour", "discrete", "discrete+contour")
+GPU_MODES = MODES
 
 DEFAULT_COLORMAP = [
     (255, 255, 217), (237, 248, 177), (199, 233, 180), (127, 205, 187),
@@ -130,7 +130,17 @@ def _to_image(img: np.ndarray) -> RenderedImage:
     return RenderedImage(width=px.shape[1], height=px.shape[0], pixels=px)
 
 
-_MODE_CODE = {"contour": 0, "discrete": 1, "discrete+contour": 2}
+_MODE_CODE = {"contour": 0, "discrete": 1, "discrete+contour": 2, "adaptive": 3, "gradient": 4, "texture": 5}
+
+
+def _texture_rgba(tex) -> np.ndarray:
+    """render.py:224-229 texture normalisation to RGBA8."""
+    tex = np.asarray(tex)
+    if tex.ndim == 2:
+        tex = np.stack([tex] * 3, axis=-1)
+    if tex.shape[2] == 3:
+        tex = np.concatenate([tex, np.full(tex.shape[:2] + (1,), 255, tex.dtype)], axis=2)
+    return np.ascontiguousarray(tex.astype(np.uint8))
 
 
 def _cmap_tensor(colormap, device) -> torch.Tensor:
@@ -144,7 +154,9 @@ def render_planes(values: torch.Tensor, strides, nimg: int, channels: int, width
     (img_stride, channel_stride, row_stride, pixel_stride) in elements."""
     lib = _lib.require_cuda()
     if spec.mode not in _MODE_CODE:
-        raise RenderError(f"mode {spec.mode!r} is not implemented on the GPU yet (SURVEY.md §8f); use {GPU_MODES}")
+        raise RenderError(f"unknown mode {spec.mode!r}")
+    if spec.mode in ("gradient", "texture") and channels != 2:
+        raise RenderError(f"{spec.mode} mode requires a two-dimensional target")
     dev = values.device
     sp = torch.as_tensor(np.broadcast_to(np.asarray(spacing, dtype=np.float64), (nimg,)).copy()).to(dev)
     out = torch.empty((nimg, height, width, 4), dtype=torch.uint8, device=dev)
@@ -166,7 +178,19 @@ def render_planes(values: torch.Tensor, strides, nimg: int, channels: int, width
     a.colormap, a.ncolors = _lib.ptr(cmap), len(spec.colormap)
     a.out = _lib.ptr(out)
     a.coverage = _lib.ptr(cov)
+    for i, c in enumerate(spec.gradient_corners):
+        cc = list(c) + [255] * (4 - len(c))
+        for k in range(4):
+            a.gradient_corners[4 * i + k] = int(cc[k])
+    a.adaptive_target_px = float(spec.adaptive_target_px)
+    tex_t = None
+    if spec.mode == "texture":
+        tex = _texture_rgba(spec.texture)
+        tex_t = torch.as_tensor(tex).to(dev)
+        a.texture, a.tex_h, a.tex_w = _lib.ptr(tex_t), tex.shape[0], tex.shape[1]
     _lib.check(lib.mdc_render(ctypes.byref(a), _lib.stream_ptr()), "mdc_render")
+    if tex_t is not None:
+        torch.cuda.current_stream().synchronize()
     return out, cov
 
 
@@ -230,29 +254,96 @@ def render_discrete(fld: CoordinateField, spec: RenderSpec) -> RenderedImage:
     return _render_gpu(fld, RenderSpec(**{**spec.__dict__, "mode": mode}))
 
 
+def render_adaptive(fld: CoordinateField, spec: RenderSpec) -> RenderedImage:
+    """render.py:169-178 on the GPU."""
+    return _render_gpu(fld, RenderSpec(**{**spec.__dict__, "mode": "adaptive"}))
+
+
+def render_gradient(fld: CoordinateField, spec: RenderSpec) -> RenderedImage:
+    """render.py:194-201 on the GPU."""
+    if fld.active_channels != 2:
+        raise RenderError("gradient mode requires a two-dimensional target")
+    return _render_gpu(fld, RenderSpec(**{**spec.__dict__, "mode": "gradient"}))
+
+
+def render_texture(fld: CoordinateField, spec: RenderSpec) -> RenderedImage:
+    """render.py:224-234 on the GPU."""
+    return _render_gpu(fld, RenderSpec(**{**spec.__dict__, "mode": "texture"}))
+
+
 def render(fld: CoordinateField, spec: RenderSpec) -> RenderedImage:
-    """render.py:272-283 for the GPU modes."""
+    """render.py:272-283: every mode renders on the GPU (mdc_render)."""
     if spec.mode in _MODE_CODE:
+        if spec.mode == "gradient" and fld.active_channels != 2:
+            raise RenderError("gradient mode requires a two-dimensional target")
         return _render_gpu(fld, spec)
-    raise RenderError(f"mode {spec.mode!r} is not implemented yet (SURVEY.md §8f); use {GPU_MODES}")
+    raise RenderError(f"unknown mode {spec.mode!r}")
+
+
+def overlay_points_device(pixels: torch.Tensor, positions, transform, spec: RenderSpec) -> torch.Tensor:
+    """render.py:237-257 on the GPU (mdc_overlay_points): discs composited in
+    point order onto an (H, W, 4) uint8 CUDA tensor, in place."""
+    lib = _lib.require_cuda()
+    h, w = pixels.shape[:2]
+    pix = np.ascontiguousarray(transform.to_pixels(np.asarray(positions, dtype=float).reshape(-1, 2)))
+    n = len(pix)
+    if n == 0:
+        return pixels
+    dev = pixels.device
+    pix_t = torch.as_tensor(pix).to(dev)
+    col = list(spec.point_color) + [255] * (4 - len(spec.point_color))
+    r = float(spec.point_radius)
+    nbytes = int(lib.mdc_overlay_workspace_bytes(n, r))
+    ws = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    col_arr = (ctypes.c_int32 * 4)(*[int(c) for c in col])
+    _lib.check(lib.mdc_overlay_points(_lib.ptr(pixels), w, h, n, _lib.ptr(pix_t), r,
+                                      ctypes.cast(col_arr, ctypes.c_void_p), _lib.ptr(ws), nbytes,
+                                      _lib.stream_ptr()), "mdc_overlay_points")
+    return pixels
 
 
 def overlay_points(img: RenderedImage, positions, transform, spec: RenderSpec) -> RenderedImage:
-    """render.py:237-257 anti-aliased discs at the projected points."""
-    base = img.pixels.astype(float) / 255.0
-    h, w = base.shape[:2]
-    r = spec.point_radius
-    pix = transform.to_pixels(np.asarray(positions, dtype=float).reshape(-1, 2))
-    for px, py in pix:
-        if not (-r - 1 <= px <= w + r and -r - 1 <= py <= h + r):
-            continue
-        c0 = max(0, int(np.floor(px - r - 1)))
-        c1 = min(w - 1, int(np.ceil(px + r + 1)))
-        r0 = max(0, int(np.floor(py - r - 1)))
-        r1 = min(h - 1, int(np.ceil(py + r + 1)))
-        if c0 > c1 or r0 > r1:
-            continue
-        yy, xx = np.mgrid[r0: r1 + 1, c0: c1 + 1]
-        cov = np.clip(r + 0.5 - np.hypot(xx - px, yy - py), 0.0, 1.0)
-        _over(base[r0: r1 + 1, c0: c1 + 1], spec.point_color, cov)
-    return _to_image(base)
+    """render.py:237-257 anti-aliased discs at the projected points (GPU)."""
+    dev = torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else None
+    if dev is None:
+        _lib.require_cuda()
+    px = torch.as_tensor(np.ascontiguousarray(img.pixels)).to(dev)
+    overlay_points_device(px, positions, transform, spec)
+    out = px.cpu().numpy()
+    return RenderedImage(width=out.shape[1], height=out.shape[0], pixels=out)
+
+
+def render_legend(fld: CoordinateField, spec: RenderSpec, width: int = 72) -> RenderedImage:
+    """render.py:286-308: value-to-colour strip for channel 0 with PIL text
+    labels (a UI helper; host-side, SURVEY.md §2 'legend' is out of the GPU
+    hot path)."""
+    from PIL import Image, ImageDraw
+
+    h = fld.height
+    vals = np.linspace(fld.coords[..., 0].max(), fld.coords[..., 0].min(), h)[:, None].repeat(width, axis=1)
+    if spec.mode in ("discrete", "discrete+contour"):
+        table = np.array([_rgba(c) for c in spec.colormap])
+        img = table[np.mod(np.floor(vals / spec.spacing).astype(np.int64), len(table))]
+    elif spec.mode == "gradient":
+        c00, c10, c01, c11 = (_rgba(c) for c in spec.gradient_corners)
+        fu = np.mod(vals / spec.spacing, 1.0)[..., None]
+        img = (1 - fu) * c00 + fu * c10
+    else:
+        img = _flat(vals.shape, spec.background)
+    on_line = np.abs(vals - spec.spacing * np.round(vals / spec.spacing))
+    step = abs(vals[0, 0] - vals[-1, 0]) / max(h - 1, 1)
+    _over(img, spec.line_color, np.clip(1.0 - on_line / max(step, 1e-30), 0.0, 1.0))
+    pil = Image.fromarray(np.clip(np.rint(img * 255), 0, 255).astype(np.uint8), "RGBA")
+    draw = ImageDraw.Draw(pil)
+    draw.text((3, 2), f"{vals[0, 0]:.3g}", fill=(0, 0, 0, 255))
+    draw.text((3, h - 12), f"{vals[-1, 0]:.3g}", fill=(0, 0, 0, 255))
+    draw.text((3, h // 2), f"step {spec.spacing:.3g}", fill=(0, 0, 0, 255))
+    return RenderedImage(width=width, height=h, pixels=np.array(pil))
+
+
+def attach_legend(img: RenderedImage, legend: RenderedImage) -> RenderedImage:
+    """render.py:311-318."""
+    if legend.height != img.height:
+        raise RenderError("legend height must match the image")
+    return RenderedImage(width=img.width + legend.width, height=img.height,
+                         pixels=np.concatenate([img.pixels, legend.pixels], axis=1))

@@ -52,3 +52,35 @@ def test_render_fields_per_channel(c1):
                             "discrete+contour")
         diff = np.abs(imgs[k].astype(int) - ref.astype(int))
         assert (diff > 1).mean() <= 2e-3, k   # fp64 field vs reference field: ~1e-12 apart
+
+
+@pytest.mark.parametrize("mode", ["adaptive", "gradient", "texture"])
+def test_render_remaining_modes(c1, mode):
+    rng = np.random.default_rng(4)
+    tex = rng.integers(0, 256, (13, 17, 3)).astype(np.uint8)
+    names = ("affine_dims23", "rigid_dims01", "affine_proj") if mode != "adaptive" else ("affine_dim1", "affine_proj")
+    for name in names:
+        fld = _fld(c1, name)
+        sp = float(c1[f"spacing_{name}"]) if f"spacing_{name}" in c1.files else 0.5
+        spec = R.RenderSpec(mode=mode, spacing=sp, texture=tex if mode == "texture" else None)
+        img = R.render(fld, spec)
+        ref = O.render_rgba(fld.coords, fld.active_channels, sp, mode, texture=tex)
+        diff = np.abs(img.pixels.astype(int) - ref.astype(int))
+        assert diff.max() <= 1, (name, mode)
+        assert (diff > 0).mean() <= 1e-3, (name, mode)
+
+
+def test_gradient_mode_needs_two_channels(c1):
+    with pytest.raises(R.RenderError):
+        R.render(_fld(c1, "affine_dim0"), R.RenderSpec(mode="gradient", spacing=1.0))
+
+
+def test_overlay_points_matches_reference_order(c1):
+    fld = _fld(c1, "affine_dim0")
+    base = R.render(fld, R.RenderSpec(mode="discrete", spacing=float(c1["spacing_affine_dim0"])))
+    pos = np.concatenate([c1["field_positions"], c1["field_positions"][:20] + 1e-3])  # overlapping discs
+    spec = R.RenderSpec(point_radius=2.5)
+    got = R.overlay_points(base, pos, fld.transform, spec).pixels
+    ref = O.overlay_points(base.pixels, fld.transform.to_pixels(pos), 2.5)
+    diff = np.abs(got.astype(int) - ref.astype(int))
+    assert diff.max() <= 1 and (diff > 0).mean() <= 1e-3
