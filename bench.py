@@ -240,6 +240,9 @@ def main():
     ap.add_argument("--frame", default=None, help="override the raster, WxH (profiling only)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-tc", action="store_true", help="force the SIMT MLS kernel (A/B)")
+    ap.add_argument("--dist-backend", default="nccl",
+                    help="torch.distributed backend (gloo: host-mediated collectives, lets several ranks "
+                         "share one GPU for a functional check of the N>1 path; never a bench number)")
     ap.add_argument("--layout-partition", action="store_true",
                     help="vertex-partition the layout over the ranks (default for config 4)")
     args = ap.parse_args()
@@ -260,9 +263,13 @@ def main():
     import torch
     import torch.distributed as dist
 
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(args.dist_backend)
     from paper_1408_0677_b200 import _lib
     from paper_1408_0677_b200 import field as F
     from paper_1408_0677_b200 import layout as L
