@@ -28,6 +28,19 @@
 
 namespace mdc {
 
+// fp32 runs: partial sums cover one control tile (NT controls) and are then
+// added into fp64 totals, bounding the rounding error by the tile length
+// instead of N (a single fp32 accumulator over 100k controls misses the 1e-4
+// fp32 contract; the affine pass-2 sum has heavy cancellation).  fp64
+// kernels keep one accumulator (flush is a no-op).
+template <typename T>
+__device__ __forceinline__ void run_flush(T &part, double &tot) {
+    if constexpr (sizeof(T) == 4) {
+        tot += (double)part;
+        part = T(0);
+    }
+}
+
 // ------------------------------------------------------------------------------
 // The fused kernel.  VAR: MDC_MEAN / MDC_AFFINE / MDC_RIGID; DC: channels per
 // pass-2 chunk; R: pixels per thread.
@@ -96,8 +109,12 @@ __global__ void __launch_bounds__(NT, MDC_MLS_MINB) mls_kernel(KArgs a) {
     if constexpr (VAR == MDC_AFFINE) {
         // ---------------- pass 1: moments ----------------
         T sw[R], mx[R], my[R], sxx[R], sxy_[R], syy[R];
+        double tsw[R], tmx[R], tmy[R], tsxx[R], tsxy[R], tsyy[R];
 #pragma unroll
-        for (int r = 0; r < R; ++r) sw[r] = mx[r] = my[r] = sxx[r] = sxy_[r] = syy[r] = T(0);
+        for (int r = 0; r < R; ++r) {
+            sw[r] = mx[r] = my[r] = sxx[r] = sxy_[r] = syy[r] = T(0);
+            tsw[r] = tmx[r] = tmy[r] = tsxx[r] = tsxy[r] = tsyy[r] = 0.0;
+        }
         stream_controls(0, false, [&](const T *, int cnt) {
 #pragma unroll 4
             for (int j = 0; j < cnt; ++j) {
@@ -115,15 +132,24 @@ __global__ void __launch_bounds__(NT, MDC_MLS_MINB) mls_kernel(KArgs a) {
                     syy[r] += wdy * dy;
                 }
             }
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                run_flush(sw[r], tsw[r]);
+                run_flush(mx[r], tmx[r]);
+                run_flush(my[r], tmy[r]);
+                run_flush(sxx[r], tsxx[r]);
+                run_flush(sxy_[r], tsxy[r]);
+                run_flush(syy[r], tsyy[r]);
+            }
         });
         // per-pixel solve in fp64: c = (A + diag(0, reg, reg))^{-1} e0
         T c0[R], c1[R], c2[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            double s = sw[r], m0 = mx[r], m1 = my[r];
-            double a00 = (double)sxx[r] - m0 * m0 / s;
-            double a01 = (double)sxy_[r] - m0 * m1 / s;
-            double a11 = (double)syy[r] - m1 * m1 / s;
+            double s = tsw[r] + (double)sw[r], m0 = tmx[r] + (double)mx[r], m1 = tmy[r] + (double)my[r];
+            double a00 = (tsxx[r] + (double)sxx[r]) - m0 * m0 / s;
+            double a01 = (tsxy[r] + (double)sxy_[r]) - m0 * m1 / s;
+            double a11 = (tsyy[r] + (double)syy[r]) - m1 * m1 / s;
             double reg = a.reg_eps * (a00 + a11);
             a00 += reg;
             a11 += reg;
@@ -140,10 +166,14 @@ __global__ void __launch_bounds__(NT, MDC_MLS_MINB) mls_kernel(KArgs a) {
         for (int r = 0; r < R; ++r) bad[r] = false;
         for (int c0ch = 0; c0ch < a.d; c0ch += DC) {
             T acc[R][DC];
+            double tacc[R][DC];
 #pragma unroll
             for (int r = 0; r < R; ++r)
 #pragma unroll
-                for (int k = 0; k < DC; ++k) acc[r][k] = T(0);
+                for (int k = 0; k < DC; ++k) {
+                    acc[r][k] = T(0);
+                    tacc[r][k] = 0.0;
+                }
             stream_controls(c0ch, true, [&](const T *sq, int cnt) {
 #pragma unroll 2
                 for (int j = 0; j < cnt; ++j) {
@@ -160,6 +190,10 @@ __global__ void __launch_bounds__(NT, MDC_MLS_MINB) mls_kernel(KArgs a) {
                         for (int k = 0; k < DC; ++k) acc[r][k] += g * qv[k];
                     }
                 }
+#pragma unroll
+                for (int r = 0; r < R; ++r)
+#pragma unroll
+                    for (int k = 0; k < DC; ++k) run_flush(acc[r][k], tacc[r][k]);
             });
             // epilogue: add back qm, write, bands
 #pragma unroll
@@ -173,7 +207,7 @@ __global__ void __launch_bounds__(NT, MDC_MLS_MINB) mls_kernel(KArgs a) {
                 for (int k = 0; k < DC; ++k) {
                     int ch = c0ch + k;
                     if (ch >= a.d) break;
-                    T f = to_t<T>((double)acc[r][k] + a.qm[ch]);
+                    T f = to_t<T>((tacc[r][k] + (double)acc[r][k]) + a.qm[ch]);
                     reinterpret_cast<T *>(a.out)[ch * a.out_cs + lr * a.out_rs + col * a.out_ps] = f;
                     if (!isfinite((double)f)) bad[r] = true;
                     if (a.bands)
@@ -195,11 +229,16 @@ __global__ void __launch_bounds__(NT, MDC_MLS_MINB) mls_kernel(KArgs a) {
         for (int r = 0; r < R; ++r) bad[r] = false;
         for (int c0ch = 0; c0ch < a.d; c0ch += DC) {
             T acc[R][DC], sw[R];
+            double tacc[R][DC], tsw[R];
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 sw[r] = T(0);
+                tsw[r] = 0.0;
 #pragma unroll
-                for (int k = 0; k < DC; ++k) acc[r][k] = T(0);
+                for (int k = 0; k < DC; ++k) {
+                    acc[r][k] = T(0);
+                    tacc[r][k] = 0.0;
+                }
             }
             stream_controls(c0ch, true, [&](const T *sq, int cnt) {
 #pragma unroll 2
@@ -217,6 +256,12 @@ __global__ void __launch_bounds__(NT, MDC_MLS_MINB) mls_kernel(KArgs a) {
                         for (int k = 0; k < DC; ++k) acc[r][k] += w * qv[k];
                     }
                 }
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    run_flush(sw[r], tsw[r]);
+#pragma unroll
+                    for (int k = 0; k < DC; ++k) run_flush(acc[r][k], tacc[r][k]);
+                }
             });
 #pragma unroll
             for (int r = 0; r < R; ++r) {
@@ -230,7 +275,7 @@ __global__ void __launch_bounds__(NT, MDC_MLS_MINB) mls_kernel(KArgs a) {
                     int ch = c0ch + k;
                     if (ch >= a.d) break;
                     double v = a.axis[ch] == 0 ? vxg[r] : vyg[r];
-                    T f = to_t<T>((v + (double)acc[r][k] / (double)sw[r]) + a.qm[ch]);
+                    T f = to_t<T>((v + (tacc[r][k] + (double)acc[r][k]) / (tsw[r] + (double)sw[r])) + a.qm[ch]);
                     reinterpret_cast<T *>(a.out)[ch * a.out_cs + lr * a.out_rs + col * a.out_ps] = f;
                     if (!isfinite((double)f)) bad[r] = true;
                     if (a.bands)
@@ -248,9 +293,13 @@ __global__ void __launch_bounds__(NT, MDC_MLS_MINB) mls_kernel(KArgs a) {
     } else {
         // Rigid (_kernels.py:127-175), 2 channels, one pass, pixel-local frame.
         T sw[R], mx[R], my[R], bqx[R], bqy[R], b00[R], b01[R], b10[R], b11[R];
+        double t_[9][R];
 #pragma unroll
-        for (int r = 0; r < R; ++r)
+        for (int r = 0; r < R; ++r) {
             sw[r] = mx[r] = my[r] = bqx[r] = bqy[r] = b00[r] = b01[r] = b10[r] = b11[r] = T(0);
+#pragma unroll
+            for (int i = 0; i < 9; ++i) t_[i][r] = 0.0;
+        }
         stream_controls(0, true, [&](const T *sq, int cnt) {
 #pragma unroll 2
             for (int j = 0; j < cnt; ++j) {
@@ -272,18 +321,31 @@ __global__ void __launch_bounds__(NT, MDC_MLS_MINB) mls_kernel(KArgs a) {
                     b11[r] += wdy * qy;
                 }
             }
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                run_flush(sw[r], t_[0][r]);
+                run_flush(mx[r], t_[1][r]);
+                run_flush(my[r], t_[2][r]);
+                run_flush(bqx[r], t_[3][r]);
+                run_flush(bqy[r], t_[4][r]);
+                run_flush(b00[r], t_[5][r]);
+                run_flush(b01[r], t_[6][r]);
+                run_flush(b10[r], t_[7][r]);
+                run_flush(b11[r], t_[8][r]);
+            }
         });
         int cnt_bad = 0;
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             if (!active[r]) continue;
-            double s = sw[r];
-            double psx = (double)mx[r] / s, psy = (double)my[r] / s;  // delta*
-            double qsx = (double)bqx[r] / s, qsy = (double)bqy[r] / s;
-            double c00 = (double)b00[r] - qsx * (double)mx[r];
-            double c01 = (double)b01[r] - qsy * (double)mx[r];
-            double c10 = (double)b10[r] - qsx * (double)my[r];
-            double c11 = (double)b11[r] - qsy * (double)my[r];
+            double s = t_[0][r] + (double)sw[r];
+            const double Mx = t_[1][r] + (double)mx[r], My = t_[2][r] + (double)my[r];
+            double psx = Mx / s, psy = My / s;  // delta*
+            double qsx = (t_[3][r] + (double)bqx[r]) / s, qsy = (t_[4][r] + (double)bqy[r]) / s;
+            double c00 = (t_[5][r] + (double)b00[r]) - qsx * Mx;
+            double c01 = (t_[6][r] + (double)b01[r]) - qsy * Mx;
+            double c10 = (t_[7][r] + (double)b10[r]) - qsx * My;
+            double c11 = (t_[8][r] + (double)b11[r]) - qsy * My;
             double ss = c00 + c11, dd = c10 - c01;
             double dx = -psx, dy = -psy;  // v - p*
             double fx = dx * ss + dy * dd;
@@ -344,7 +406,7 @@ static int launch_t(const KArgs &k, cudaStream_t s) {
 
 template <typename T, int VAR, int AM>
 static int dispatch_dc(const KArgs &k, cudaStream_t s) {
-    // channel chunk: smallest instantiated DC >= d (cap 32 for f32, 16 for f64)
+    // channel chunk: smallest instantiated DC >= d (cap 8 for f32, 16 for f64)
     constexpr bool F32 = sizeof(T) == 4;
     constexpr int R = 2;
     int d = k.d;
@@ -354,8 +416,8 @@ static int dispatch_dc(const KArgs &k, cudaStream_t s) {
     if (d <= 4) return launch_t<T, VAR, AM, 4, R>(k, s);
     if (d <= 8) return launch_t<T, VAR, AM, 8, R>(k, s);
     if constexpr (F32) {
-        if (d <= 16) return launch_t<T, VAR, AM, 16, R>(k, s);
-        return launch_t<T, VAR, AM, 32, R>(k, s);
+        // fp32 keeps fp64 run totals per channel in registers: chunks of 8
+        return launch_t<T, VAR, AM, 8, R>(k, s);
     } else {
         return launch_t<T, VAR, AM, 16, R>(k, s);
     }

@@ -58,6 +58,26 @@ __device__ __forceinline__ float weight(float d2, float neg_alpha) {
     }
 }
 
+// Packed form for two controls at once: the arithmetic runs as FFMA2/FMUL2
+// (one issue slot for two lanes of fp32 work), the MUFU ops stay scalar.
+// Lane-wise identical to weight<AM>(float).
+template <int AM>
+__device__ __forceinline__ float2 weight2(float2 d2, float neg_alpha) {
+    if (AM == A_THREE_HALVES) {
+        float2 r = make_float2(rsqrt_approx(d2.x), rsqrt_approx(d2.y));
+        return __fmul2_rn(__fmul2_rn(r, r), r);
+    } else if (AM == A_ONE) {
+        return make_float2(rcp_approx(d2.x), rcp_approx(d2.y));
+    } else if (AM == A_HALF) {
+        return make_float2(rsqrt_approx(d2.x), rsqrt_approx(d2.y));
+    } else if (AM == A_TWO) {
+        float2 r = make_float2(rcp_approx(d2.x), rcp_approx(d2.y));
+        return __fmul2_rn(r, r);
+    } else {
+        float2 l = __fmul2_rn(make_float2(lg2_approx(d2.x), lg2_approx(d2.y)), make_float2(neg_alpha, neg_alpha));
+        return make_float2(ex2_approx(l.x), ex2_approx(l.y));
+    }
+}
 template <int AM>
 __device__ __forceinline__ double weight(double d2, double neg_alpha) {
     // fp64 mirrors _kernels.py:37-49 including the 1e-300 floor.

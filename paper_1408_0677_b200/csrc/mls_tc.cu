@@ -1,34 +1,40 @@
 // mls_tc.cu -- affine MLS with the pass-2 contraction on the 5th-gen tensor
-// cores (tcgen05, kind::tf32, 3xTF32 split, accumulators in TMEM).
+// cores (tcgen05, kind::tf32, 3xTF32 split, A operand and accumulators in TMEM).
 //
 // Same mathematics as mls.cu (SURVEY.md §8a M6'; reference _kernels.py:70-124):
-//   pass 1 (SIMT, fp32 FMA pipe): 6 pixel-local moments -> c = A_reg^{-1} e0
+//   pass 1 (SIMT, packed f32x2 on the FP32 pipe): 6 pixel-local moments
+//           -> c = A_reg^{-1} e0 (fp64 solve)
 //   pass 2: F[p, k] = sum_j G[p, j] Q[j, k],  G[p, j] = w_pj (c0 + c1 dx + c2 dy)
 // Pass 2 is a dense (pixels x N) . (N x d) contraction (north_star: "tensor
-// cores ... only for the global-support weight case").  The SIMT threads only
-// evaluate G (one weight per pair) and store it, split hi + lo, straight into
-// shared memory in the UMMA K-major core-matrix layout; one elected thread
-// issues tcgen05.mma (M = 128 pixels, N = channels, K = 8 controls) x 3
-// (hi*hi + hi*lo + lo*hi, ~fp32-accurate) per K step, accumulating in TMEM.
-// A two-stage ring (mbarrier armed by tcgen05.commit) overlaps the tensor
-// core with the SIMT evaluation of the next tile.  The target block Q is
-// pre-arranged once per call into the same core-matrix layout (hi/lo), so its
-// tiles are plain contiguous cp.async copies.
+// cores ... only for the global-support weight case").  The SIMT threads
+// evaluate G (one weight per pair), split it hi + lo and write it straight
+// into TMEM with tcgen05.st (thread = pixel = TMEM lane), so the A operand
+// never touches shared memory; one elected thread issues tcgen05.mma
+// (M = 128 pixels, N = channels, K = 8 controls) x 3 (hi*hi + hi*lo + lo*hi,
+// ~fp32-accurate) per K step with B = the target tile.  A two-stage ring
+// (mbarrier armed by tcgen05.commit) overlaps the tensor core with the SIMT
+// evaluation of the next tile.  The target block Q is pre-arranged once per
+// call into the UMMA core-matrix layout (hi/lo), one bulk copy per K tile.
+//
+// Accuracy at scale: G has both signs (affine weights), so F is a sum with
+// heavy cancellation; a single fp32 accumulator over 100k controls misses
+// the 1e-4 fp32 contract by ~5x.  Both passes therefore accumulate in fp32
+// only over bounded runs (pass 1: one staging round; pass 2: FLUSH K tiles
+// in TMEM) and add the runs into fp64 totals (registers / shared memory).
 //
 // Tile geometry (A/B-tuned): CTA = 128 pixels (one M = 128 MMA tile) + an
-// issuer warp, K tile = 16 controls, 2-stage ring, 5 CTAs per SM.
+// issuer warp, K tile = 16 controls, 2-stage ring, 4 CTAs per SM (TMEM).
 #include "mls_common.cuh"
 #include "tcgen05.cuh"
 
 namespace mdc {
 namespace tc {
 
-#ifndef MDC_TC_TPB
-#define MDC_TC_TPB 128
+constexpr int TPB = 128;          // compute threads == pixels per CTA == MMA M
+#ifndef MDC_TC_XYR
+#define MDC_TC_XYR 256
 #endif
-constexpr int TPB = MDC_TC_TPB;   // compute threads == pixels per CTA (multiple of 128)
-constexpr int MT = TPB / 128;     // M = 128 MMA tiles per CTA
-constexpr int XYR = 256;          // controls per position staging round
+constexpr int XYR = MDC_TC_XYR;   // controls per position staging round
 #ifndef MDC_TC_KT
 #define MDC_TC_KT 16
 #endif
@@ -36,18 +42,16 @@ constexpr int XYR = 256;          // controls per position staging round
 #define MDC_TC_STAGES 2
 #endif
 #ifndef MDC_TC_MINB
-#define MDC_TC_MINB 5
+#define MDC_TC_MINB 4
+#endif
+#ifndef MDC_TC_FLUSH
+#define MDC_TC_FLUSH 32  // K tiles accumulated in TMEM before the fp64 flush (512 controls)
 #endif
 constexpr int KT = MDC_TC_KT;          // controls per K tile (multiple of 8 = tcgen05 tf32 K)
 constexpr int STAGES = MDC_TC_STAGES;  // ring depth
-constexpr int A_SBO = (KT / 4) * 128;                  // bytes between 8-row core-matrix groups
-constexpr int A_HALF = (TPB / 8) * A_SBO;              // one of hi/lo: TPB rows x KT
-constexpr int A_STAGE = 2 * A_HALF;
-
-// byte offset of (row m, k) in a K-major core-matrix tile with SBO = A_SBO
-__device__ __forceinline__ uint32_t cm_off(int m, int k) {
-    return (uint32_t)((m >> 3) * A_SBO + (k >> 2) * 128 + (m & 7) * 16 + (k & 3) * 4);
-}
+constexpr int FLUSH = MDC_TC_FLUSH;
+constexpr int A_SBO = (KT / 4) * 128;  // bytes between 8-row core-matrix groups of a Q tile
+constexpr int NC_MAX = 32;             // channels per pass-2 chunk (fp64 totals in shared memory)
 
 // ---------------------------------------------------------------------------
 // Q -> tiled core-matrix image, hi/lo split.  img[(chunk * ntiles + t)][hi|lo]
@@ -75,16 +79,16 @@ __global__ void q_image_kernel(const float *q, int64_t n, int ldq, int d, int nc
     *reinterpret_cast<float *>(base + tile_bytes + off) = lo;
 }
 
-// Warp roles: warps 0..7 (256 threads, one pixel each) evaluate moments and
-// G tiles; warp 8 is the producer/issuer: lane 0 waits for a full stage
-// (8 warp arrivals + the bulk-copied Q tile's bytes), issues the MMAs and
-// commits them to the stage's "empty" barrier.  No block-wide barrier per
-// K tile; compute warps only wait when the ring wraps onto a stage whose
-// MMAs are still in flight.
+// Warp roles: warps 0..3 (128 threads, one pixel each) evaluate moments and
+// G tiles; warp 4 is the issuer: lane 0 waits for a full stage (4 warp
+// arrivals + the bulk-copied Q tile's bytes), issues the MMAs and commits
+// them to the stage's "empty" barrier.  No block-wide barrier per K tile;
+// compute warps only wait when the ring wraps onto a stage whose MMAs are
+// still in flight, and at each fp64 flush.
 constexpr int CWARPS = TPB / 32;        // compute warps
 constexpr int THREADS = TPB + 32;       // + one issuer warp
 
-__device__ __forceinline__ void compute_bar_sync() {  // named barrier over the 256 compute threads
+__device__ __forceinline__ void compute_bar_sync() {  // named barrier over the compute threads
     asm volatile("bar.sync 1, %0;" ::"n"(TPB) : "memory");
 }
 
@@ -92,13 +96,15 @@ template <int AM, int NC>
 __global__ void __launch_bounds__(THREADS, MDC_TC_MINB) mls_tc_kernel(KArgs a, const float *qimg, int64_t ntiles, int nchunk) {
     constexpr int B_HALF = NC * KT * 4;
     constexpr int B_STAGE = 2 * B_HALF;
-    constexpr int COLS = MT * NC;
-    constexpr int TMEM_COLS = COLS <= 32 ? 32 : (COLS <= 64 ? 64 : (COLS <= 128 ? 128 : 256));
+    // TMEM columns: accumulators (NC) then the G ring ({hi, lo} x KT per stage)
+    constexpr int ACOL = NC;
+    constexpr int COLS = ACOL + STAGES * 2 * KT;
+    constexpr int TMEM_COLS = COLS <= 32 ? 32 : (COLS <= 64 ? 64 : (COLS <= 128 ? 128 : (COLS <= 256 ? 256 : 512)));
     constexpr int PER = XYR / TPB;  // staged controls per thread per round
     extern __shared__ __align__(128) unsigned char smem[];
-    unsigned char *sA = smem;                                          // STAGES x A_STAGE
-    unsigned char *sB = sA + STAGES * A_STAGE;                         // STAGES x B_STAGE
-    float2 *sxy = reinterpret_cast<float2 *>(sB + STAGES * B_STAGE);  // 2 x XYR controls
+    unsigned char *sB = smem;                                          // STAGES x B_STAGE
+    double *tot = reinterpret_cast<double *>(sB + STAGES * B_STAGE);   // NC x TPB fp64 totals
+    float2 *sxy = reinterpret_cast<float2 *>(tot + NC * TPB);         // 2 x XYR controls
     uint64_t *full = reinterpret_cast<uint64_t *>(sxy + 2 * XYR);     // STAGES: G + Q ready
     uint64_t *empty = full + STAGES;                                   // STAGES: MMAs retired
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(empty + STAGES);
@@ -130,34 +136,23 @@ __global__ void __launch_bounds__(THREADS, MDC_TC_MINB) mls_tc_kernel(KArgs a, c
         // ------------------------------ MMA issuer --------------------------
         if (lane == 0) {
             uint32_t ring = 0;
-#ifdef MDC_TC_PASS1_ONLY
-            nchunk = 0;
-#endif
             for (int chunk = 0; chunk < nchunk; ++chunk) {
                 for (int64_t t = 0; t < ntiles; ++t, ++ring) {
                     const int s = ring % STAGES;
                     mbar_wait(&full[s], (ring / STAGES) & 1);
                     asm volatile("tcgen05.fence::after_thread_sync;");
-                    unsigned char *as = sA + s * A_STAGE;
-                    unsigned char *bs = sB + s * B_STAGE;
-                    const uint32_t a_hi = smem_u32(as), a_lo = smem_u32(as + A_HALF);
-                    const uint32_t b_hi = smem_u32(bs), b_lo = smem_u32(bs + B_HALF);
+                    const uint32_t b_hi = smem_u32(sB + s * B_STAGE), b_lo = b_hi + B_HALF;
 #pragma unroll
-                    for (int mt = 0; mt < MT; ++mt) {
-                        const uint32_t dcol = tmem + mt * NC;
-                        const uint32_t moff = mt * (128 / 8) * A_SBO;
-#pragma unroll
-                        for (int kk = 0; kk < KT / 8; ++kk) {
-                            const uint32_t koff = kk * 256;
-                            const uint32_t acc = (t > 0 || kk > 0) ? 1u : 0u;
-                            const uint64_t dah = umma_desc(a_hi + moff + koff, 128, A_SBO);
-                            const uint64_t dal = umma_desc(a_lo + moff + koff, 128, A_SBO);
-                            const uint64_t dbh = umma_desc(b_hi + koff, 128, A_SBO);
-                            const uint64_t dbl = umma_desc(b_lo + koff, 128, A_SBO);
-                            mma_tf32(dcol, dah, dbh, idesc, acc);
-                            mma_tf32(dcol, dah, dbl, idesc, 1u);
-                            mma_tf32(dcol, dal, dbh, idesc, 1u);
-                        }
+                    for (int kk = 0; kk < KT / 8; ++kk) {
+                        const uint32_t koff = kk * 256;
+                        // a fresh fp32 run after every fp64 flush
+                        const uint32_t acc = (t % FLUSH != 0 || kk > 0) ? 1u : 0u;
+                        const uint64_t dbh = umma_desc(b_hi + koff, 128, A_SBO);
+                        const uint64_t dbl = umma_desc(b_lo + koff, 128, A_SBO);
+                        const uint32_t ta = tmem + ACOL + s * 2 * KT + kk * 8;
+                        mma_tf32_ts(tmem, ta, dbh, idesc, acc);
+                        mma_tf32_ts(tmem, ta, dbl, idesc, 1u);
+                        mma_tf32_ts(tmem, ta + KT, dbh, idesc, 1u);
                     }
                     asm volatile(
                         "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -183,25 +178,41 @@ __global__ void __launch_bounds__(THREADS, MDC_TC_MINB) mls_tc_kernel(KArgs a, c
         const float vx = (float)(vxg - ox), vy = (float)(vyg - oy);
         const int64_t n = a.n;
         const int64_t nxy = (n + XYR - 1) / XYR;
+        const uint32_t lane_addr = (uint32_t)(warp * 32) << 16;  // this warp's TMEM lanes
 
         // Control positions stream through a double-buffered staging area,
         // one named barrier per round.  Controls past n are parked far away
         // (weight underflows to 0, G stays finite) and their Q rows are zero:
         // full tiles, no masking.
+        // Staging layout: one float4 per control PAIR, {x0, x1, y0, y1}, so
+        // a 128-bit load yields packed (x0, x1) / (y0, y1) operands for the
+        // f32x2 arithmetic below.  Each thread stages whole pairs.
+        static_assert(PER % 2 == 0, "controls are staged in pairs");
         double2 pre[PER];
         auto fetch = [&](int64_t r) {
 #pragma unroll
-            for (int e = 0; e < PER; ++e) {
-                int64_t j = r * XYR + e * TPB + tid;
-                pre[e] = (r < nxy && j < n) ? reinterpret_cast<const double2 *>(a.pc)[j] : make_double2(1e300, 1e300);
+            for (int e = 0; e < PER / 2; ++e) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    int64_t j = r * XYR + 2 * (e * TPB + tid) + h;
+                    pre[2 * e + h] = (r < nxy && j < n) ? reinterpret_cast<const double2 *>(a.pc)[j]
+                                                        : make_double2(1e300, 1e300);
+                }
             }
         };
         auto store = [&](int64_t r) {
-            float2 *buf = sxy + (r & 1) * XYR;
+            float4 *buf = reinterpret_cast<float4 *>(sxy + (r & 1) * XYR);
 #pragma unroll
-            for (int e = 0; e < PER; ++e)
-                buf[e * TPB + tid] = pre[e].x == 1e300 ? make_float2(1e18f, 1e18f)
-                                                       : make_float2((float)(pre[e].x - ox), (float)(pre[e].y - oy));
+            for (int e = 0; e < PER / 2; ++e) {
+                float x[2], y[2];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const double2 v = pre[2 * e + h];
+                    x[h] = v.x == 1e300 ? 1e18f : (float)(v.x - ox);
+                    y[h] = v.x == 1e300 ? 1e18f : (float)(v.y - oy);
+                }
+                buf[e * TPB + tid] = make_float4(x[0], x[1], y[0], y[1]);
+            }
         };
         auto xy_init = [&]() {
             compute_bar_sync();
@@ -215,48 +226,49 @@ __global__ void __launch_bounds__(THREADS, MDC_TC_MINB) mls_tc_kernel(KArgs a, c
             fetch(r + 2);
         };
 
-        // ---------------- pass 1: moments (SIMT) ----------------
-        float sw = 0.f, mx = 0.f, my = 0.f, sxx = 0.f, sxy_ = 0.f, syy = 0.f;
+        // ---------------- pass 1: moments (SIMT, packed f32x2) ----------------
+        // Lane 0 of each float2 accumulates the even controls, lane 1 the odd
+        // ones.  The fp32 partials cover one staging round (XYR controls) and
+        // are then added into fp64 totals, so the rounding error is bounded by
+        // the round length instead of growing with N (100k-control frames
+        // otherwise exceed the 1e-4 fp32 contract).
+        const float2 nvx = make_float2(-vx, -vx), nvy = make_float2(-vy, -vy);
+        double tw = 0.0, tmx = 0.0, tmy = 0.0, txx = 0.0, txy = 0.0, tyy = 0.0;
         xy_init();
         for (int64_t r = 0; r < nxy; ++r) {
             xy_step(r);
-            const float2 *buf = sxy + (r & 1) * XYR;
+            const float4 *s4 = reinterpret_cast<const float4 *>(sxy + (r & 1) * XYR);
             const int cnt = (int)min((int64_t)XYR, n - r * XYR);
-            const float4 *s4 = reinterpret_cast<const float4 *>(buf);
-            int j = 0;
+            float2 sw2 = make_float2(0.f, 0.f), mx2 = sw2, my2 = sw2, sxx2 = sw2, sxy2 = sw2, syy2 = sw2;
+            auto acc = [&](const float4 pp, bool odd_tail) {
+                const float2 dx = __fadd2_rn(make_float2(pp.x, pp.y), nvx);
+                const float2 dy = __fadd2_rn(make_float2(pp.z, pp.w), nvy);
+                float2 w = weight2<AM>(__ffma2_rn(dy, dy, __fmul2_rn(dx, dx)), neg_alpha);
+                if (odd_tail) w.y = 0.f;  // parked control (alpha < 1 does not underflow)
+                const float2 wdx = __fmul2_rn(w, dx), wdy = __fmul2_rn(w, dy);
+                sw2 = __fadd2_rn(sw2, w);
+                mx2 = __fadd2_rn(mx2, wdx);
+                my2 = __fadd2_rn(my2, wdy);
+                sxx2 = __ffma2_rn(wdx, dx, sxx2);
+                sxy2 = __ffma2_rn(wdx, dy, sxy2);
+                syy2 = __ffma2_rn(wdy, dy, syy2);
+            };
 #pragma unroll 4
-            for (; j + 1 < cnt; j += 2) {
-                float4 pp = s4[j >> 1];
-                {
-                    float dx = pp.x - vx, dy = pp.y - vy;
-                    float w = weight<AM>(dx * dx + dy * dy, neg_alpha);
-                    float wdx = w * dx, wdy = w * dy;
-                    sw += w; mx += wdx; my += wdy;
-                    sxx += wdx * dx; sxy_ += wdx * dy; syy += wdy * dy;
-                }
-                {
-                    float dx = pp.z - vx, dy = pp.w - vy;
-                    float w = weight<AM>(dx * dx + dy * dy, neg_alpha);
-                    float wdx = w * dx, wdy = w * dy;
-                    sw += w; mx += wdx; my += wdy;
-                    sxx += wdx * dx; sxy_ += wdx * dy; syy += wdy * dy;
-                }
-            }
-            if (j < cnt) {
-                float2 pp = buf[j];
-                float dx = pp.x - vx, dy = pp.y - vy;
-                float w = weight<AM>(dx * dx + dy * dy, neg_alpha);
-                float wdx = w * dx, wdy = w * dy;
-                sw += w; mx += wdx; my += wdy;
-                sxx += wdx * dx; sxy_ += wdx * dy; syy += wdy * dy;
-            }
+            for (int j2 = 0; j2 < (cnt >> 1); ++j2) acc(s4[j2], false);
+            if (cnt & 1) acc(s4[cnt >> 1], true);
+            tw += (double)sw2.x + (double)sw2.y;
+            tmx += (double)mx2.x + (double)mx2.y;
+            tmy += (double)my2.x + (double)my2.y;
+            txx += (double)sxx2.x + (double)sxx2.y;
+            txy += (double)sxy2.x + (double)sxy2.y;
+            tyy += (double)syy2.x + (double)syy2.y;
         }
         float c0, c1, c2;
         {
-            double s = sw, m0 = mx, m1 = my;
-            double a00 = (double)sxx - m0 * m0 / s;
-            double a01 = (double)sxy_ - m0 * m1 / s;
-            double a11 = (double)syy - m1 * m1 / s;
+            double s = tw, m0 = tmx, m1 = tmy;
+            double a00 = txx - m0 * m0 / s;
+            double a01 = txy - m0 * m1 / s;
+            double a11 = tyy - m1 * m1 / s;
             double reg = a.reg_eps * (a00 + a11);
             a00 += reg;
             a11 += reg;
@@ -268,17 +280,36 @@ __global__ void __launch_bounds__(THREADS, MDC_TC_MINB) mls_tc_kernel(KArgs a, c
             c2 = (float)(-u1 / s);
         }
 
-        // ---------------- pass 2: G tiles -> ring -> tcgen05 ----------------
-#ifdef MDC_TC_PASS1_ONLY
-        if (c0 == 12345.f) a.nonfinite[0] = 1;  // keep pass 1 alive
-        nchunk = 0;
-#endif
+        // ---------------- pass 2: G tiles -> TMEM ring -> tcgen05 ----------------
         bool bad = false;
         uint32_t ring = 0;
+        const float2 c0v = make_float2(c0, c0), c1v = make_float2(c1, c1), c2v = make_float2(c2, c2);
         const int64_t row = p / a.width;
         const int64_t col = p - row * a.width;
         const int64_t lr = row - a.row0;
         constexpr int TPR = XYR / KT;  // K tiles per staging round
+        // Read the TMEM accumulator run (after its last MMA retired) into the
+        // fp64 totals; `init` starts a chunk's totals.
+        auto flush = [&](bool init) {
+            asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+            for (int c8 = 0; c8 < NC / 8; ++c8) {
+                uint32_t v[8];
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                    : "r"(tmem + lane_addr + c8 * 8));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    double &t = tot[(c8 * 8 + e) * TPB + tid];
+                    t = (init ? 0.0 : t) + (double)__uint_as_float(v[e]);
+                }
+            }
+            // the next run's first MMA (accumulate = 0) overwrites these
+            // columns only after this warp's next arrival
+            asm volatile("tcgen05.fence::before_thread_sync;");
+        };
         for (int chunk = 0; chunk < nchunk; ++chunk) {
             const char *qchunk = reinterpret_cast<const char *>(qimg) + (size_t)chunk * ntiles * B_STAGE;
             xy_init();
@@ -288,79 +319,54 @@ __global__ void __launch_bounds__(THREADS, MDC_TC_MINB) mls_tc_kernel(KArgs a, c
                 if (tin == 0) xy_step(round);
                 const int s = ring % STAGES;
                 if (ring >= STAGES) mbar_wait(&empty[s], ((ring - STAGES) / STAGES) & 1);
-                unsigned char *as = sA + s * A_STAGE;
+                asm volatile("tcgen05.fence::after_thread_sync;");  // the stage's MMAs retired
                 if (tid == 0) {  // Q tile: one bulk copy, completion counted on full[s]
                     mbar_arrive_tx(&full[s], B_STAGE);
                     bulk_g2s(sB + s * B_STAGE, qchunk + (size_t)t * B_STAGE, B_STAGE, &full[s]);
                 }
-                const float2 *buf = sxy + (round & 1) * XYR + tin * KT;
+                const float4 *buf = reinterpret_cast<const float4 *>(sxy + (round & 1) * XYR + tin * KT);
+                uint32_t ghi[KT], glo[KT];
 #pragma unroll
-                for (int q4 = 0; q4 < KT / 4; ++q4) {
-                    const float4 *s4 = reinterpret_cast<const float4 *>(buf + q4 * 4);
-                    float g[4];
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        float4 pp = s4[h];
-                        float dx = pp.x - vx, dy = pp.y - vy;
-                        float w = weight<AM>(dx * dx + dy * dy, neg_alpha);
-                        g[2 * h] = w * (c0 + c1 * dx + c2 * dy);
-                        dx = pp.z - vx;
-                        dy = pp.w - vy;
-                        w = weight<AM>(dx * dx + dy * dy, neg_alpha);
-                        g[2 * h + 1] = w * (c0 + c1 * dx + c2 * dy);
-                    }
-                    uint4 hi, lo;
-                    uint32_t *hp = &hi.x, *lp = &lo.x;
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        uint32_t hb = tf32_hi_bits(g[e]);
-                        hp[e] = hb;
-                        lp[e] = __float_as_uint(g[e] - __uint_as_float(hb));
-                    }
-                    const uint32_t off = cm_off(tid, q4 * 4);
-                    *reinterpret_cast<uint4 *>(as + off) = hi;
-                    *reinterpret_cast<uint4 *>(as + A_HALF + off) = lo;
+                for (int h = 0; h < KT / 2; ++h) {
+                    const float4 pp = buf[h];
+                    const float2 dx = __fadd2_rn(make_float2(pp.x, pp.y), nvx);
+                    const float2 dy = __fadd2_rn(make_float2(pp.z, pp.w), nvy);
+                    const float2 w = weight2<AM>(__ffma2_rn(dy, dy, __fmul2_rn(dx, dx)), neg_alpha);
+                    const float2 g = __fmul2_rn(w, __ffma2_rn(c2v, dy, __ffma2_rn(c1v, dx, c0v)));
+                    const float2 gh = make_float2(__uint_as_float(tf32_hi_bits(g.x)), __uint_as_float(tf32_hi_bits(g.y)));
+                    const float2 gl = __ffma2_rn(gh, make_float2(-1.f, -1.f), g);  // g - hi, exact
+                    ghi[2 * h] = __float_as_uint(gh.x);
+                    ghi[2 * h + 1] = __float_as_uint(gh.y);
+                    glo[2 * h] = __float_as_uint(gl.x);
+                    glo[2 * h + 1] = __float_as_uint(gl.y);
                 }
-                // make this warp's generic-proxy stores visible to the tensor core
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                // this warp's 32 rows (TMEM lanes) of the stage's G tile
+                const uint32_t ta = tmem + lane_addr + ACOL + s * 2 * KT;
+                tmem_st<KT>(ta, ghi);
+                tmem_st<KT>(ta + KT, glo);
+                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                asm volatile("tcgen05.fence::before_thread_sync;");
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&full[s]);
+                if (t % FLUSH == FLUSH - 1 || t == ntiles - 1) {
+                    // the run ends with this tile: MMAs retire in order
+                    mbar_wait(&empty[s], (ring / STAGES) & 1);
+                    flush(t < FLUSH);
+                }
             }
-            // drain: the chunk's last MMAs retire in order
-            {
-                const uint32_t last = ring - 1;
-                mbar_wait(&empty[last % STAGES], (last / STAGES) & 1);
-            }
-            asm volatile("tcgen05.fence::after_thread_sync;");
-            const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
-            const uint32_t col0 = tmem + (warp >> 2) * NC;
-#pragma unroll
-            for (int c8 = 0; c8 < NC / 8; ++c8) {
-                uint32_t v[8];
-                asm volatile(
-                    "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
-                    : "r"(lane_base + col0 + c8 * 8));
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                if (active) {
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) {
-                        const int ch = chunk * NC + c8 * 8 + e;
-                        if (ch < a.d) {
-                            float f = (float)((double)__uint_as_float(v[e]) + a.qm[ch]);
-                            reinterpret_cast<float *>(a.out)[ch * a.out_cs + lr * a.out_rs + col * a.out_ps] = f;
-                            if (!isfinite(f)) bad = true;
-                            if (a.bands)
-                                a.bands[ch * a.band_cs + lr * a.band_rs + col] =
-                                    (int32_t)floor((double)f / a.spacing[ch]);
-                        }
+            if (active) {
+#pragma unroll 4
+                for (int c = 0; c < NC; ++c) {
+                    const int ch = chunk * NC + c;
+                    if (ch < a.d) {
+                        float f = (float)(tot[c * TPB + tid] + a.qm[ch]);
+                        reinterpret_cast<float *>(a.out)[ch * a.out_cs + lr * a.out_rs + col * a.out_ps] = f;
+                        if (!isfinite(f)) bad = true;
+                        if (a.bands)
+                            a.bands[ch * a.band_cs + lr * a.band_rs + col] = (int32_t)floor((double)f / a.spacing[ch]);
                     }
                 }
             }
-            // TMEM is re-used by the next chunk's first MMA, which the issuer
-            // only starts after every compute warp has arrived on that tile
-            // (i.e. after these tcgen05.ld completed).
-            asm volatile("tcgen05.fence::before_thread_sync;");
         }
         if (a.nonfinite && active && bad) atomicAdd(a.nonfinite, 1);
     }
@@ -373,11 +379,11 @@ __global__ void __launch_bounds__(THREADS, MDC_TC_MINB) mls_tc_kernel(KArgs a, c
 
 template <int NC>
 static size_t tc_smem_bytes() {
-    return STAGES * (size_t)A_STAGE + STAGES * (size_t)(2 * NC * KT * 4) + 2 * XYR * sizeof(float2) +
+    return STAGES * (size_t)(2 * NC * KT * 4) + (size_t)NC * TPB * sizeof(double) + 2 * XYR * sizeof(float2) +
            2 * STAGES * sizeof(uint64_t) + 16;
 }
 
-static int pick_nc(int d) { return d <= 16 ? 16 : (d <= 32 ? 32 : 64); }
+static int pick_nc(int d) { return d <= 16 ? 16 : NC_MAX; }
 
 }  // namespace tc
 
@@ -416,8 +422,7 @@ template <int AM>
 static int launch_tc_am(const KArgs &k, void *ws, cudaStream_t s) {
     switch (tc::pick_nc(k.d)) {
         case 16: return launch_tc_nc<AM, 16>(k, ws, s);
-        case 32: return launch_tc_nc<AM, 32>(k, ws, s);
-        default: return launch_tc_nc<AM, 64>(k, ws, s);
+        default: return launch_tc_nc<AM, tc::NC_MAX>(k, ws, s);
     }
 }
 

@@ -201,3 +201,32 @@ def test_linear_row_bands(g2k):
     full, _ = F.linear_device(pos, tv, g2k["triangles"], 120, 90)
     parts = [F.linear_device(pos, tv, g2k["triangles"], 120, 90, row_range=rr)[0] for rr in ((0, 31), (31, 90))]
     assert torch.equal(torch.cat(parts, dim=1), full)
+
+
+@pytest.mark.parametrize("tensor_cores", [True, False])
+def test_fp32_contract_at_bench_scale(tensor_cores):
+    """The bench workload itself (config 3: N=100k Gaussian-mixture points,
+    d=32, 3840x2160): fp32 fields on three row bands (top, middle, bottom)
+    against the fp64 oracle on the same rows, 1e-4 normwise contract.  A
+    single fp32 accumulator over 100k controls fails this by ~5x; the
+    kernels accumulate bounded fp32 runs into fp64 totals."""
+    import bench
+    from paper_1408_0677_b200 import dataset as D
+    from paper_1408_0677_b200 import projection as P
+
+    cfg = bench.CONFIGS[3]
+    X = bench.gmm(cfg["n"], cfg["d"], cfg["seed"])
+    ds = D.normalize(D.Dataset(names=[f"d{i}" for i in range(cfg["d"])], data=X))
+    _, cloud = P.pca_project(ds)
+    pos = cloud.positions
+    raw = np.column_stack([ds.raw_column(nm) for nm in ds.names])
+    W, H = cfg["W"], cfg["H"]
+    worst = 0.0
+    for r0, r1 in ((0, 4), (H // 2 - 2, H // 2 + 2), (H - 4, H)):
+        v = F.compute_fields(pos, raw, F.MlsParams("affine"), W, H, dtype="f32", row_range=(r0, r1),
+                             tensor_cores=tensor_cores).values.double().cpu().numpy()
+        ref = O.compute_field(pos, raw[:, [0, 31]], "affine", W, H, rows=(r0, r1))
+        for j, c in enumerate((0, 31)):
+            worst = max(worst, normwise(v[c], ref[..., j]))
+    print("bench-scale fp32 normwise:", worst)
+    assert worst <= FP32_TOL / 5
