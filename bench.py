@@ -398,17 +398,19 @@ def main():
     alg_flops = pairs * (19 + 6 * d)  # SURVEY.md §8d per-pair figure (one-pass formulation)
     use_tc = (not args.no_tc) and d >= 8
     if use_tc:
-        nc = 16 if d <= 16 else (32 if d <= 32 else 64)
+        nc = 16 if d <= 16 else 32
         chunks = -(-d // nc)
-        fma_instr = pairs * (13 + 10 * chunks)     # SIMT FMA-pipe ops: moments + G evaluation
+        # SIMT FP32 lane-ops per pair (FFMA2/FADD2/FMUL2 count 2): pass-1 moments 14,
+        # pass-2 G evaluation + tf32 split 10 per channel chunk
+        fma_instr = pairs * (14 + 10 * chunks)
         tc_flops = pairs * chunks * 3 * 2 * nc      # 3xTF32 MMAs
         kname = f"mls_tc_kernel<alpha=1.5, N={nc}> (tcgen05 kind::tf32 3xTF32 pass 2)"
     else:
         dc = 1
-        while dc < d and dc < 32:
+        while dc < d and dc < 8:
             dc *= 2
         chunks = -(-d // dc)
-        fma_instr = pairs * (13 + 9 * chunks + d)
+        fma_instr = pairs * (14 + 9 * chunks + d)
         tc_flops = 0
         kname = f"mls_kernel<float, AFFINE, alpha=1.5, DC={dc}, R=2> (SIMT)"
     sec = kernel_ms * 1e-3
@@ -418,7 +420,7 @@ def main():
     roofline = {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak, "traffic": None,
                 "kernel": kname, "kernel_ms": kernel_ms,
-                "achieved_def": "FP32-pipe ops executed (FMA-pipe instruction = 2 FLOP) / kernel time",
+                "achieved_def": "FP32-pipe lane-ops executed x 2 (one FMA-pipe lane-op = one FFMA = 2 FLOP) / kernel time",
                 "peak_source": "measured FFMA microbenchmark (mdc_peak_ffma), this run",
                 "algorithmic_tflops": alg_flops / sec / 1e12,
                 "algorithmic_def": "SURVEY.md §8d 19+6d FLOP per (pixel, control) pair",

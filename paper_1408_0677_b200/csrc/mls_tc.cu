@@ -44,6 +44,9 @@ constexpr int XYR = MDC_TC_XYR;   // controls per position staging round
 #ifndef MDC_TC_MINB
 #define MDC_TC_MINB 4
 #endif
+#ifndef MDC_TC_SLEEPC
+#define MDC_TC_SLEEPC 0  // compute warps park (1) or spin (0) on the ring's empty barriers
+#endif
 #ifndef MDC_TC_FLUSH
 #define MDC_TC_FLUSH 32  // K tiles accumulated in TMEM before the fp64 flush (512 controls)
 #endif
@@ -139,7 +142,7 @@ __global__ void __launch_bounds__(THREADS, MDC_TC_MINB) mls_tc_kernel(KArgs a, c
             for (int chunk = 0; chunk < nchunk; ++chunk) {
                 for (int64_t t = 0; t < ntiles; ++t, ++ring) {
                     const int s = ring % STAGES;
-                    mbar_wait(&full[s], (ring / STAGES) & 1);
+                    mbar_wait_sleep(&full[s], (ring / STAGES) & 1);
                     asm volatile("tcgen05.fence::after_thread_sync;");
                     const uint32_t b_hi = smem_u32(sB + s * B_STAGE), b_lo = b_hi + B_HALF;
 #pragma unroll
@@ -318,7 +321,13 @@ __global__ void __launch_bounds__(THREADS, MDC_TC_MINB) mls_tc_kernel(KArgs a, c
                 const int64_t round = t / TPR;
                 if (tin == 0) xy_step(round);
                 const int s = ring % STAGES;
-                if (ring >= STAGES) mbar_wait(&empty[s], ((ring - STAGES) / STAGES) & 1);
+                if (ring >= STAGES) {
+#if MDC_TC_SLEEPC
+                    mbar_wait_sleep(&empty[s], ((ring - STAGES) / STAGES) & 1);
+#else
+                    mbar_wait(&empty[s], ((ring - STAGES) / STAGES) & 1);
+#endif
+                }
                 asm volatile("tcgen05.fence::after_thread_sync;");  // the stage's MMAs retired
                 if (tid == 0) {  // Q tile: one bulk copy, completion counted on full[s]
                     mbar_arrive_tx(&full[s], B_STAGE);

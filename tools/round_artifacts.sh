@@ -1,0 +1,16 @@
+#!/bin/bash
+# Round-end measurement bundle (run under gpurun from the repo root):
+# bench line, reference arm, launch list, ncu --set full of the two top kernels.
+set -x
+mkdir -p gpurun_out
+python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
+tail -1 gpurun_out/bench.json
+python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
+tail -1 gpurun_out/bench_ref.json
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
+    python bench.py --steps 2 --warmup 1 --no-cpu > gpurun_out/ncu_launch.log 2>&1
+ncu --set full --import-source on --clock-control none -k regex:mls_tc_kernel -s 1 -c 1 -o gpurun_out/mls_tc_full -f \
+    python bench.py --steps 1 --warmup 1 --no-cpu --no-e2e --no-layout > gpurun_out/ncu_mls.log 2>&1
+ncu --set full --import-source on --clock-control none -k regex:bh_kernel -s 20 -c 1 -o gpurun_out/bh_full -f \
+    python bench.py --steps 1 --warmup 0 --no-cpu --no-e2e --layout-iters 30 > gpurun_out/ncu_bh.log 2>&1
+ls -la gpurun_out
