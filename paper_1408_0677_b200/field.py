@@ -18,7 +18,7 @@ from __future__ import annotations
 
 import ctypes
 import struct
-from dataclasses import dataclass
+from dataclasses import dataclass, field as dc_field
 
 import numpy as np
 import torch
@@ -138,6 +138,10 @@ class CoordinateField:
     source_positions: np.ndarray
     transform: ViewportTransform
     active_channels: int = 2
+    # GPU-resident copy of ``coords`` ((H, W, 2) fp64 CUDA tensor, same
+    # values) kept by compute_field so render / service caches skip the
+    # re-upload; not part of the reference's dataclass identity.
+    device_coords: object = dc_field(default=None, repr=False, compare=False)
 
     def jacobian(self) -> np.ndarray:
         dy, dx = np.gradient(self.coords, axis=(0, 1))
@@ -439,12 +443,13 @@ def compute_field(mesh, positions: np.ndarray, targets: TargetAssignment, params
         out = torch.empty((height, width, 2), dtype=tdt, device=dev)
         _, tr = linear_device(positions, tvals, mesh.triangles, width, height, dtype=dtype, out=out,
                               strides=(1, 2 * width, 2))
-        coords = out.double().cpu().numpy()
+        dev64 = out if out.dtype == torch.float64 else out.double()
+        coords = dev64.cpu().numpy()
         if not np.all(np.isfinite(coords)):
             raise FieldError("field evaluation produced non-finite coordinates")
         return CoordinateField(width=width, height=height, coords=coords,
                                source_positions=positions, transform=tr,
-                               active_channels=targets.active_channels)
+                               active_channels=targets.active_channels, device_coords=dev64)
     prob = MlsProblem(positions, tvals, params.variant, width, height, alpha=params.resolved_alpha,
                       reg_eps=params.reg_eps, epsilon_dist=params.epsilon_dist, dtype=dtype,
                       axis=[0, 1])
@@ -452,12 +457,14 @@ def compute_field(mesh, positions: np.ndarray, targets: TargetAssignment, params
     nonfinite = torch.zeros((), dtype=torch.int32, device=prob.device)
     a = prob.args(out, (1, 2 * width, 2), 0, height, nonfinite=nonfinite)
     prob.run(a)
-    coords = out.double().cpu().numpy()
+    dev64 = out if out.dtype == torch.float64 else out.double()
+    coords = dev64.cpu().numpy()
     if int(nonfinite.item()) != 0 or not np.all(np.isfinite(coords)):
         raise FieldError("field evaluation produced non-finite coordinates")
     return CoordinateField(width=width, height=height, coords=coords,
                            source_positions=np.asarray(positions, dtype=float),
-                           transform=prob.transform, active_channels=targets.active_channels)
+                           transform=prob.transform, active_channels=targets.active_channels,
+                           device_coords=dev64)
 
 
 MAGIC = b"MLSF"

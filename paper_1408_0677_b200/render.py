@@ -195,7 +195,11 @@ def render_planes(values: torch.Tensor, strides, nimg: int, channels: int, width
 
 
 def _field_planes(fld: CoordinateField):
-    coords = torch.as_tensor(np.ascontiguousarray(fld.coords, dtype=np.float64)).cuda()
+    dev = getattr(fld, "device_coords", None)
+    if isinstance(dev, torch.Tensor) and dev.is_cuda and dev.dtype == torch.float64 and dev.is_contiguous():
+        coords = dev  # compute_field kept the GPU copy (same values as fld.coords)
+    else:
+        coords = torch.as_tensor(np.ascontiguousarray(fld.coords, dtype=np.float64)).cuda()
     w, h = fld.width, fld.height
     return coords, (0, 1, 2 * w, 2)
 
@@ -241,6 +245,30 @@ def _render_gpu(fld: CoordinateField, spec: RenderSpec) -> RenderedImage:
     out, _ = render_planes(coords, strides, 1, fld.active_channels, fld.width, fld.height, spec.spacing, spec)
     px = out[0].cpu().numpy()
     return RenderedImage(width=px.shape[1], height=px.shape[0], pixels=px)
+
+
+def render_device(fld: CoordinateField, spec: RenderSpec) -> torch.Tensor:
+    """``render`` without the host round trip: (H, W, 4) uint8 CUDA tensor
+    (the service composes the overlay on it and downloads once)."""
+    mode = spec.mode
+    if mode not in MODES:
+        raise RenderError(f"unknown mode {mode!r}")
+    coords, strides = _field_planes(fld)
+    out, _ = render_planes(coords, strides, 1, fld.active_channels, fld.width, fld.height, spec.spacing, spec)
+    return out[0]
+
+
+def point_mask(img_shape, positions, transform, spec: RenderSpec) -> np.ndarray:
+    """render.py:260-269: boolean mask of pixels the point overlay covers
+    (a host helper for comparisons, not a render path)."""
+    h, w = img_shape
+    mask = np.zeros((h, w), dtype=bool)
+    r = spec.point_radius
+    pix = transform.to_pixels(np.asarray(positions, dtype=float).reshape(-1, 2))
+    yy, xx = np.mgrid[0:h, 0:w]
+    for px, py in pix:
+        mask |= np.hypot(xx - px, yy - py) <= r + 0.5
+    return mask
 
 
 def render_contours(fld: CoordinateField, spec: RenderSpec) -> RenderedImage:
