@@ -226,6 +226,50 @@ def measure_peaks(lib, torch):
     return out
 
 
+# fp64 pipe ops per BH unit (bh_kernel source): leaf pair = 2 sub + 2 fma (r2)
+# + 5 (rsqrt.approx + 3rd-order correction) + 3 (r^3 + eta) + 3 (rcp.approx +
+# correction) + 2 fma (force); monopole = 19; opening test = 12 (box distance,
+# IEEE sqrt fix-up, theta compare).
+BH_OPS = {"leaf_pairs": 17, "monopoles": 19, "node_tests": 12}
+LOCAL_BYTES_PER_VERTEX = 204  # SURVEY.md §8d algorithmic bytes per vertex-iteration
+
+
+def layout_roofline(eng, params, lib, torch):
+    """Per-phase device times of one eager step after the timed run
+    (mdc_layout_profile) and the two layout roofs of SURVEY.md §8d: BH on the
+    FP64 pipe (executed lane-ops x 2 vs the live DFMA peak) and the local
+    sweep against HBM (algorithmic bytes; the working set is L2-resident, so
+    frac may exceed 1)."""
+    prof = eng.profile_step(params.initial_temp * params.decay_lambda ** params.iterations)
+    ms = prof["ms"]
+    n = eng.n
+    peaks = measure_peaks(lib, torch)
+    ops = sum(BH_OPS[k] * prof[k] for k in BH_OPS)
+    bh_tflops = 2 * ops / (ms["bh_traversal"] * 1e-3) / 1e12
+    hbm = _measured_hbm_gbs()
+    local_gbs = LOCAL_BYTES_PER_VERTEX * n / (ms["local"] * 1e-3) / 1e9
+    return {
+        "phases_ms_one_eager_step": ms,
+        "bh": {"bound": "fp64", "achieved": bh_tflops, "peak": peaks["fp64"] / 1e12, "unit": "TFLOP/s",
+               "frac": bh_tflops * 1e12 / peaks["fp64"],
+               "interactions_per_vertex": (prof["leaf_pairs"] - n + prof["monopoles"]) / n,
+               "node_tests_per_vertex": prof["node_tests"] / n,
+               "ops_def": "fp64 lane-ops x 2 / bh_kernel time; 17/leaf pair, 19/monopole, 12/opening test",
+               "peak_source": "measured DFMA microbenchmark (mdc_peak_dfma), this run"},
+        "local": {"bound": "hbm", "achieved": local_gbs, "peak": hbm, "unit": "GB/s", "frac": local_gbs / hbm,
+                  "bytes_per_vertex": LOCAL_BYTES_PER_VERTEX,
+                  "note": "algorithmic bytes (SURVEY.md §8d); working set L2-resident at this N",
+                  "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
+    }
+
+
+def _measured_hbm_gbs():
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:
+        return 6650.0  # B200_PROFILING.md fallback (6.65 TB/s)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -320,6 +364,8 @@ def main():
                       "orientation_flips": flips,
                       "scaling": "strong (vertex-partitioned, SUM all-reduce per iteration)" if partition
                       else "replicas only"}
+        if rank == 0:
+            layout_res["roofline"] = layout_roofline(eng, params, lib, torch)
 
     # ---- MLS frame: d dims, row band per rank ---------------------------
     from paper_1408_0677_b200.field import MlsProblem

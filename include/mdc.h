@@ -260,6 +260,15 @@ MDC_API int mdc_layout_plan_destroy(MdcLayoutPlan *plan);
  * captured CUDA graph per step. */
 MDC_API int mdc_layout_steps(MdcLayoutPlan *plan, int32_t k, const double *temps, int32_t use_graph,
                      void *stream);
+/* Profiling: ONE eager step of the plan (same result as mdc_layout_steps
+ * k=1) with CUDA events between its phases.  ms_out[5] = {axis sorts, tree
+ * levels + centroids, BH traversal, BH task combine, local forces + clamp +
+ * update}.  counts_out[3] (nullable) = {leaf-pair interactions incl. the
+ * zero self terms, monopole interactions, node opening tests} over this
+ * rank's points, from a separate instrumented traversal before the timed
+ * step.  Synchronizes the stream. */
+MDC_API int mdc_layout_profile(MdcLayoutPlan *plan, const double *temps, float *ms_out, int64_t *counts_out,
+                               void *stream);
 /* Barnes-Hut repulsion alone for positions pts (bhtree.py:69-95). */
 MDC_API int mdc_layout_repulsion(MdcLayoutPlan *plan, const double *pts, double *out, void *stream);
 /* kd-tree of pts: node arrays (count = mdc_layout_node_count) copied out. */

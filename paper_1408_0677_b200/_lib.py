@@ -110,6 +110,7 @@ SIGNATURES = {
     "mdc_layout_plan_create": (ctypes.c_int, [ctypes.POINTER(MdcLayoutArgs), ctypes.POINTER(_vp), _vp]),
     "mdc_layout_plan_destroy": (ctypes.c_int, [_vp]),
     "mdc_layout_steps": (ctypes.c_int, [_vp, _c_i32, _vp, _c_i32, _vp]),
+    "mdc_layout_profile": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp]),
     "mdc_layout_repulsion": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
     "mdc_layout_node_count": (_c_i64, [_vp]),
     "mdc_layout_kdtree": (ctypes.c_int, [_vp, _vp] + [_vp] * 10 + [_vp]),

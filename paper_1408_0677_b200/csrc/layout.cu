@@ -170,8 +170,9 @@ struct DevTree {
 
 struct Buffers {
     DevTree t;
-    unsigned long long *kx, *ky, *kx_out, *ky_out;
-    int32_t *ids, *xs[2], *ys[2];
+    unsigned long long *kx, *ky, *kx_out, *ky_out;  // kx|ky and kx_out|ky_out are contiguous (2n keys)
+    int32_t *ids, *xs[2], *ys[2];                    // ids: 2n sort values; xs[0]|ys[0] contiguous
+    int32_t *runflag;                                // 2n, all-zero between steps
     int32_t *flag, *blocksum;
     double *pos_b, *bh;
     int32_t *ctr;
@@ -185,7 +186,7 @@ static size_t cub_sort_bytes(int64_t n) {
     size_t bytes = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, bytes, (unsigned long long *)nullptr,
                                     (unsigned long long *)nullptr, (int32_t *)nullptr,
-                                    (int32_t *)nullptr, (int)n);
+                                    (int32_t *)nullptr, (int)(2 * n), 0, 33);
     return bytes;
 }
 
@@ -230,11 +231,12 @@ static size_t carve(Buffers &b, char *base, const TreeShape &s) {
     b.ky = c.take<unsigned long long>(n);
     b.kx_out = c.take<unsigned long long>(n);
     b.ky_out = c.take<unsigned long long>(n);
-    b.ids = c.take<int32_t>(n);
-    b.xs[0] = c.take<int32_t>(n);
+    b.ids = c.take<int32_t>(2 * n);
+    b.xs[0] = c.take<int32_t>(2 * n);
+    b.ys[0] = b.xs[0] + n;
     b.xs[1] = c.take<int32_t>(n);
-    b.ys[0] = c.take<int32_t>(n);
     b.ys[1] = c.take<int32_t>(n);
+    b.runflag = c.take<int32_t>(2 * n);
     b.flag = c.take<int32_t>(n);
     b.blocksum = c.take<int32_t>(std::max<int64_t>((n + SCAN_BLOCK - 1) / SCAN_BLOCK + 1, 1024));
     b.pos_b = c.take<double>(2 * n);
@@ -254,14 +256,92 @@ __device__ __forceinline__ unsigned long long order_key(double x) {
     return (b & 0x8000000000000000ULL) ? ~b : (b | 0x8000000000000000ULL);
 }
 
-__global__ void keys_kernel(const double *pts, int64_t n, unsigned long long *kx,
-                            unsigned long long *ky, int32_t *ids) {
+// Both axes in ONE radix sort of 2n 33-bit keys {axis bit, order-preserving
+// bits of (float)coord}: 5 digit passes instead of 2 x 8 for fp64 keys.  The
+// float rounding is monotone, so the result is already ordered by the exact
+// (coord, id) key except inside runs of equal float keys (distinct doubles
+// within one float ulp); those runs are detected and re-sorted by the exact
+// key below.  Stable sort + ids in input order = ties by id.
+__device__ __forceinline__ uint32_t order_key32(double x) {
+    float f = (float)x;
+    if (f == 0.0f) f = 0.0f;
+    uint32_t b = __float_as_uint(f);
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+
+__global__ void keys_kernel(const double *pts, int64_t n, unsigned long long *keys, int32_t *ids) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    double2 p = reinterpret_cast<const double2 *>(pts)[i];
-    kx[i] = order_key(p.x);
-    ky[i] = order_key(p.y);
-    ids[i] = (int32_t)i;
+    if (i >= 2 * n) return;
+    const int axis = i >= n;
+    const int64_t j = i - axis * n;
+    keys[i] = ((unsigned long long)axis << 32) | order_key32(pts[2 * j + axis]);
+    ids[i] = (int32_t)j;
+}
+
+// exact order (coord, id) of two ids on one axis
+__device__ __forceinline__ bool exact_less(const double *pts, int axis, int32_t a, int32_t b) {
+    unsigned long long ka = order_key(pts[2 * a + axis]), kb = order_key(pts[2 * b + axis]);
+    return ka < kb || (ka == kb && a < b);
+}
+
+// Flag the start of every run of equal float keys that is NOT already in
+// exact order (exact-tie runs stay untouched: they are sorted by id).
+__global__ void run_mark_kernel(int64_t n, const unsigned long long *keys, const int32_t *ids, const double *pts,
+                                int32_t *runflag) {
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x + 1;
+    if (k >= 2 * n || keys[k] != keys[k - 1]) return;
+    const int axis = (int)(keys[k] >> 32);
+    if (!exact_less(pts, axis, ids[k], ids[k - 1])) return;
+    int64_t s0 = k - 1;
+    while (s0 > 0 && keys[s0 - 1] == keys[k]) --s0;
+    runflag[s0] = 1;
+}
+
+// Insertion-sort each flagged run by the exact key (runs are a few elements:
+// distinct doubles sharing one float), then clear its flag.
+__global__ void run_sort_kernel(int64_t n, const unsigned long long *keys, int32_t *ids, const double *pts,
+                                int32_t *runflag) {
+    int64_t s0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s0 >= 2 * n || !runflag[s0]) return;
+    runflag[s0] = 0;
+    const unsigned long long key = keys[s0];
+    const int axis = (int)(key >> 32);
+    int64_t e = s0 + 1;
+    while (e < 2 * n && keys[e] == key) ++e;
+    int32_t *r = ids + s0;
+    const int64_t len = e - s0;
+    if (len <= 64) {
+        for (int64_t i = 1; i < len; ++i) {
+            const int32_t v = r[i];
+            int64_t j = i - 1;
+            while (j >= 0 && exact_less(pts, axis, v, r[j])) {
+                r[j + 1] = r[j];
+                --j;
+            }
+            r[j + 1] = v;
+        }
+        return;
+    }
+    // pathological long run (many distinct doubles inside one float ulp):
+    // heap sort keeps it O(L log L)
+    auto sift = [&](int64_t root, int64_t end) {
+        while (2 * root + 1 < end) {
+            int64_t child = 2 * root + 1;
+            if (child + 1 < end && exact_less(pts, axis, r[child], r[child + 1])) ++child;
+            if (!exact_less(pts, axis, r[root], r[child])) return;
+            const int32_t t = r[root];
+            r[root] = r[child];
+            r[child] = t;
+            root = child;
+        }
+    };
+    for (int64_t i = len / 2 - 1; i >= 0; --i) sift(i, len);
+    for (int64_t end = len - 1; end > 0; --end) {
+        const int32_t t = r[0];
+        r[0] = r[end];
+        r[end] = t;
+        sift(0, end);
+    }
 }
 
 // Node stats for nodes at one depth: bbox from the ends of the sorted runs
@@ -726,8 +806,13 @@ __device__ __forceinline__ void monopole(const double4 g1, double xi, double yi,
 // monopole is added by exactly one task), then walks its subtree.  The set of
 // interactions per point is exactly the reference's; partial sums per task
 // are combined in task order by the consumer.
+// COUNT (profiling only, mdc_layout_profile): also tally leaf-pair and
+// monopole interactions and node opening tests into cnt[0..2].
+template <bool COUNT>
 __global__ void __launch_bounds__(BH_WARPS * 32) bh_kernel(int64_t n, int64_t k0, int64_t k1, DevTree t,
-                                                           double c, double eta, double theta) {
+                                                           double c, double eta, double theta,
+                                                           unsigned long long *cnt) {
+    unsigned long long n_leaf = 0, n_mono = 0, n_test = 0;
     __shared__ int s_node[BH_WARPS][BH_STACK];
     __shared__ unsigned s_mask[BH_WARPS][BH_STACK];
     const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -745,9 +830,13 @@ __global__ void __launch_bounds__(BH_WARPS * 32) bh_kernel(int64_t n, int64_t k0
     for (int dd = 0; dd < t.cut; ++dd) {
         int a = t.task_path[task * t.cut + dd];
         double4 g0 = t.geo[2 * a], g1 = t.geo[2 * a + 1];
+        if (COUNT && act) ++n_test;
         if (act && far_node(g0, g1.z, xi, yi, theta)) {
             act = false;
-            if (t.task_first[task * t.cut + dd]) monopole(g1, xi, yi, eta, fx, fy);
+            if (t.task_first[task * t.cut + dd]) {
+                monopole(g1, xi, yi, eta, fx, fy);
+                if (COUNT) ++n_mono;
+            }
         }
     }
     unsigned m0 = __ballot_sync(0xffffffffu, act);
@@ -772,6 +861,7 @@ __global__ void __launch_bounds__(BH_WARPS * 32) bh_kernel(int64_t n, int64_t k0
                 // weight stays finite), so no j != i test is needed --
                 // coincident distinct points also contribute 0 in the reference.
                 if (on) {
+                    if (COUNT) n_leaf += (unsigned long long)(tp.y - tp.x);
 #pragma unroll 4
                     for (int q = tp.x; q < tp.y; ++q) {
                         double2 pj = __ldg(sp2 + q);
@@ -790,10 +880,13 @@ __global__ void __launch_bounds__(BH_WARPS * 32) bh_kernel(int64_t n, int64_t k0
             bool open = false;
             if (on) {
                 double4 g0 = t.geo[2 * node], g1 = t.geo[2 * node + 1];
-                if (far_node(g0, g1.z, xi, yi, theta))
+                if (COUNT) ++n_test;
+                if (far_node(g0, g1.z, xi, yi, theta)) {
                     monopole(g1, xi, yi, eta, fx, fy);
-                else
+                    if (COUNT) ++n_mono;
+                } else {
                     open = true;
+                }
             }
             unsigned om = __ballot_sync(0xffffffffu, open);
             if (om) {
@@ -809,6 +902,11 @@ __global__ void __launch_bounds__(BH_WARPS * 32) bh_kernel(int64_t n, int64_t k0
         }
     }
     if (valid) reinterpret_cast<double2 *>(t.part)[(size_t)task * n + k] = make_double2(c * fx, c * fy);
+    if (COUNT && valid) {
+        atomicAdd(cnt + 0, n_leaf);
+        atomicAdd(cnt + 1, n_mono);
+        atomicAdd(cnt + 2, n_test);
+    }
 }
 
 // Combine the task partials (task order) into out[i] by point id.
@@ -966,6 +1064,14 @@ struct MdcLayoutPlan {
     cudaStream_t cap_stream = nullptr;
     const double *graph_temps = nullptr;
     int build_blocks = 0;
+    // profiling (mdc_layout_profile): events recorded between step phases
+    cudaEvent_t ev[8] = {};
+    int nev = 0;
+    bool timing = false;
+    unsigned long long *count = nullptr;  // non-null: instrumented BH launch
+    void mark(cudaStream_t s) {
+        if (timing && nev < 8) cudaEventRecord(ev[nev++], s);
+    }
 };
 
 namespace mdc {
@@ -975,7 +1081,6 @@ static int build_tree(MdcLayoutPlan *p, const double *pts, cudaStream_t s, const
     const TreeShape &sh = p->shape;
     Buffers &b = p->b;
     int64_t n = sh.n;
-    int nb = (int)((n + 255) / 256);
     if (n <= BSORT_MAX) {
         size_t smem = sizeof(typename cub::BlockRadixSort<unsigned long long, BSORT_THREADS, BSORT_ITEMS,
                                                            int32_t>::TempStorage);
@@ -988,15 +1093,17 @@ static int build_tree(MdcLayoutPlan *p, const double *pts, cudaStream_t s, const
         block_sort_kernel<<<2, BSORT_THREADS, smem, s>>>(pts, (int)n, b.xs[0], b.ys[0]);
         MDC_CHECK_LAUNCH();
     } else {
-        keys_kernel<<<nb, 256, 0, s>>>(pts, n, b.kx, b.ky, b.ids);
+        const int nb2 = (int)((2 * n + 255) / 256);
+        keys_kernel<<<nb2, 256, 0, s>>>(pts, n, b.kx, b.ids);
         MDC_CHECK_LAUNCH();
         size_t bytes = b.cub_bytes;
         MDC_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(b.cub_tmp, bytes, b.kx, b.kx_out, b.ids, b.xs[0],
-                                                       (int)n, 0, 64, s));
-        bytes = b.cub_bytes;
-        MDC_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(b.cub_tmp, bytes, b.ky, b.ky_out, b.ids, b.ys[0],
-                                                       (int)n, 0, 64, s));
+                                                       (int)(2 * n), 0, 33, s));
+        run_mark_kernel<<<nb2, 256, 0, s>>>(n, b.kx_out, b.xs[0], pts, b.runflag);
+        run_sort_kernel<<<nb2, 256, 0, s>>>(n, b.kx_out, b.xs[0], pts, b.runflag);
+        MDC_CHECK_LAUNCH();
     }
+    p->mark(s);  // sorts done
     BuildArgs ba;
     ba.pts = pts;
     ba.n = n;
@@ -1019,6 +1126,7 @@ static int build_tree(MdcLayoutPlan *p, const double *pts, cudaStream_t s, const
         MDC_CHECK_CUDA(cudaLaunchCooperativeKernel((const void *)build_levels_kernel<BUILD_THREADS, false>,
                                                    dim3(p->build_blocks), dim3(BUILD_THREADS), kargs, 0, s));
     }
+    p->mark(s);  // tree levels + centroids done
     int cur = sh.max_depth & 1;
     *perm_out = b.xs[cur];
     return MDC_OK;
@@ -1042,8 +1150,13 @@ static int run_bh(MdcLayoutPlan *p, const double *pts, double *out, cudaStream_t
     int64_t warps = (k1 - k0 + 31) / 32;
     if (warps > 0) {
         dim3 grid((unsigned)((warps + BH_WARPS - 1) / BH_WARPS), (unsigned)p->shape.ntask);
-        bh_kernel<<<grid, BH_WARPS * 32, 0, s>>>(n, k0, k1, p->b.t, p->a.c, p->a.eta, p->a.theta);
+        if (p->count)
+            bh_kernel<true><<<grid, BH_WARPS * 32, 0, s>>>(n, k0, k1, p->b.t, p->a.c, p->a.eta, p->a.theta, p->count);
+        else
+            bh_kernel<false><<<grid, BH_WARPS * 32, 0, s>>>(n, k0, k1, p->b.t, p->a.c, p->a.eta, p->a.theta, nullptr);
+        p->mark(s);  // traversal done
         bh_combine_kernel<<<(unsigned)((k1 - k0 + 255) / 256), 256, 0, s>>>(n, k0, k1, p->b.t, perm, out);
+        p->mark(s);  // combine done
     }
     MDC_CHECK_LAUNCH();
     if (perm_out) *perm_out = perm;
@@ -1054,6 +1167,7 @@ static int enqueue_step(MdcLayoutPlan *p, const double *pin, double *pout, const
                         cudaStream_t s) {
     int64_t n = p->shape.n;
     const int32_t *perm = nullptr;
+    p->mark(s);  // step start
     if (n >= 2) {
         int rc = run_bh(p, pin, p->b.bh, s, &perm);
         if (rc) return rc;
@@ -1088,6 +1202,7 @@ static int enqueue_step(MdcLayoutPlan *p, const double *pin, double *pout, const
         MDC_CHECK_CUDA(cudaMemsetAsync(pout, 0, sizeof(double) * 2 * (size_t)n, s));
     }
     if (la.k1 > la.k0) local_kernel<<<(unsigned)((la.k1 - la.k0 + 127) / 128), 128, 0, s>>>(la);
+    p->mark(s);  // local forces + update done
     incr_kernel<<<1, 1, 0, s>>>(p->b.ctr);
     MDC_CHECK_LAUNCH();
     return MDC_OK;
@@ -1158,6 +1273,7 @@ extern "C" int mdc_layout_plan_create(const MdcLayoutArgs *a, MdcLayoutPlan **pl
         p->build_blocks = std::max(1, std::min(std::max(1, per_sm) * sms, want));
         if (p->build_blocks > 1024) p->build_blocks = 1024;  // blocksum capacity below
     }
+    cudaMemsetAsync(p->b.runflag, 0, sizeof(int32_t) * 2 * (size_t)p->shape.n, s);
     // host vectors must outlive the async copies
     cudaError_t e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) {
@@ -1170,6 +1286,9 @@ extern "C" int mdc_layout_plan_create(const MdcLayoutArgs *a, MdcLayoutPlan **pl
 }
 
 extern "C" int mdc_layout_plan_destroy(MdcLayoutPlan *p) {
+    if (p)
+        for (int i = 0; i < 8; ++i)
+            if (p->ev[i]) cudaEventDestroy(p->ev[i]);
     if (!p) return MDC_OK;
     for (auto &g : p->graph)
         if (g) cudaGraphExecDestroy(g);
@@ -1213,6 +1332,42 @@ extern "C" int mdc_layout_steps(MdcLayoutPlan *p, int32_t k, const double *temps
     if (k & 1)
         MDC_CHECK_CUDA(cudaMemcpyAsync(p->a.pos, p->b.pos_b, sizeof(double) * 2 * (size_t)p->shape.n,
                                        cudaMemcpyDeviceToDevice, s));
+    return MDC_OK;
+}
+
+extern "C" int mdc_layout_profile(MdcLayoutPlan *p, const double *temps, float *ms_out, int64_t *counts_out,
+                                  void *stream) {
+    MDC_REQUIRE(p && temps && ms_out, "null pointer");
+    MDC_REQUIRE(p->shape.n >= 2, "profiling needs n >= 2");
+    cudaStream_t s = (cudaStream_t)stream;
+    int64_t n = p->shape.n;
+    // instrumented traversal first (its own launch, outside the timing)
+    if (counts_out) {
+        unsigned long long *cnt = nullptr;
+        MDC_CHECK_CUDA(cudaMallocAsync((void **)&cnt, 3 * sizeof(unsigned long long), s));
+        MDC_CHECK_CUDA(cudaMemsetAsync(cnt, 0, 3 * sizeof(unsigned long long), s));
+        p->count = cnt;
+        int rc = run_bh(p, p->a.pos, p->b.bh, s);
+        p->count = nullptr;
+        if (rc) return rc;
+        unsigned long long h[3];
+        MDC_CHECK_CUDA(cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, s));
+        MDC_CHECK_CUDA(cudaStreamSynchronize(s));
+        MDC_CHECK_CUDA(cudaFreeAsync(cnt, s));
+        for (int i = 0; i < 3; ++i) counts_out[i] = (int64_t)h[i];
+    }
+    for (int i = 0; i < 8; ++i)
+        if (!p->ev[i]) MDC_CHECK_CUDA(cudaEventCreate(&p->ev[i]));
+    MDC_CHECK_CUDA(cudaMemsetAsync(p->b.ctr, 0, sizeof(int32_t), s));
+    p->nev = 0;
+    p->timing = true;
+    int rc = enqueue_step(p, p->a.pos, p->b.pos_b, temps, s);
+    p->timing = false;
+    if (rc) return rc;
+    MDC_CHECK_CUDA(cudaMemcpyAsync(p->a.pos, p->b.pos_b, sizeof(double) * 2 * (size_t)n, cudaMemcpyDeviceToDevice, s));
+    MDC_CHECK_CUDA(cudaStreamSynchronize(s));
+    MDC_REQUIRE(p->nev == 6, "unexpected phase count");
+    for (int i = 0; i < 5; ++i) MDC_CHECK_CUDA(cudaEventElapsedTime(&ms_out[i], p->ev[i], p->ev[i + 1]));
     return MDC_OK;
 }
 

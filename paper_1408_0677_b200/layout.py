@@ -168,6 +168,22 @@ class LayoutEngine:
         _lib.check(self.lib.mdc_layout_steps(h, k, _lib.ptr(self.temps), int(use_graph and not debug),
                                              _lib.stream_ptr()), "mdc_layout_steps")
 
+    PHASES = ("sorts", "tree", "bh_traversal", "bh_combine", "local")
+
+    def profile_step(self, temperature: float, count: bool = True) -> dict:
+        """One eager step on ``self.pos`` with per-phase device times
+        (mdc_layout_profile) and, optionally, the BH interaction counts."""
+        t = torch.tensor([float(temperature)], dtype=torch.float64, device=self.device)
+        ms = (ctypes.c_float * 5)()
+        cnt = (ctypes.c_int64 * 3)()
+        _lib.check(self.lib.mdc_layout_profile(self.plan(), _lib.ptr(t), ctypes.cast(ms, ctypes.c_void_p),
+                                               ctypes.cast(cnt, ctypes.c_void_p) if count else None,
+                                               _lib.stream_ptr()), "mdc_layout_profile")
+        out = {"ms": dict(zip(self.PHASES, (float(v) for v in ms)))}
+        if count:
+            out["leaf_pairs"], out["monopoles"], out["node_tests"] = (int(v) for v in cnt)
+        return out
+
     def repulsion(self, pts: torch.Tensor) -> torch.Tensor:
         out = torch.empty_like(pts)
         _lib.check(self.lib.mdc_layout_repulsion(self.plan(), _lib.ptr(pts), _lib.ptr(out), _lib.stream_ptr()),

@@ -192,3 +192,30 @@ def test_vertex_partition_reassembles_bit_identically(g2k):
         pos = acc
         assert torch.equal(pos, full.pos), it
     assert normwise(pos.cpu().numpy(), g2k["states"][5]) <= FREE_TOL
+
+
+@pytest.mark.parametrize("kind", ["float_collisions", "long_run"])
+def test_kdtree_device_sort_exact_order(kind):
+    """n > 12288 takes the device radix sort on 33-bit float keys: runs of
+    distinct doubles that share a float key (and exact ties) must still end
+    up in exact (coord, id) order -- checked through the kd-tree membership
+    against the oracle."""
+    rng = np.random.default_rng(7)
+    n = 20000
+    if kind == "float_collisions":
+        base = rng.normal(0, 3, n // 8)
+        x = np.repeat(base, 8) * (1 + rng.integers(-3, 4, n) * 2.0 ** -45)  # same float, distinct doubles
+        y = rng.normal(0, 3, n)
+        x[::97] = x[0]  # exact ties as well
+    else:
+        x = 1.0 + rng.integers(0, 4000, n) * 2.0 ** -40  # one float key, a 20000-long run
+        y = rng.normal(0, 1, n)
+    pts = np.column_stack([x, y])
+    gt = bhtree.KdTree(pts, leaf_size=32)
+    ot = O.KdTree(pts, leaf_size=32)
+    nn = ot.count
+    for arr in ("lo", "hi", "left", "right"):
+        assert np.array_equal(getattr(gt, arr)[:nn], getattr(ot, arr)[:nn]), arr
+    for i in range(nn):
+        assert set(gt.perm[gt.lo[i]:gt.hi[i]].tolist()) == set(ot.perm[ot.lo[i]:ot.hi[i]].tolist()), i
+    assert np.array_equal(gt.bmin, ot.bmin[:nn]) and np.array_equal(gt.bmax, ot.bmax[:nn])
