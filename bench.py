@@ -254,6 +254,7 @@ def layout_roofline(eng, params, lib, torch):
                "frac": bh_tflops * 1e12 / peaks["fp64"],
                "interactions_per_vertex": (prof["leaf_pairs"] - n + prof["monopoles"]) / n,
                "node_tests_per_vertex": prof["node_tests"] / n,
+               "lane_efficiency": (prof["leaf_pairs"] + prof["node_tests"]) / max(1, prof["lane_slots"]),
                "ops_def": "fp64 lane-ops x 2 / bh_kernel time; 17/leaf pair, 19/monopole, 12/opening test",
                "peak_source": "measured DFMA microbenchmark (mdc_peak_dfma), this run"},
         "local": {"bound": "hbm", "achieved": local_gbs, "peak": hbm, "unit": "GB/s", "frac": local_gbs / hbm,

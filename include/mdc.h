@@ -263,8 +263,9 @@ MDC_API int mdc_layout_steps(MdcLayoutPlan *plan, int32_t k, const double *temps
 /* Profiling: ONE eager step of the plan (same result as mdc_layout_steps
  * k=1) with CUDA events between its phases.  ms_out[5] = {axis sorts, tree
  * levels + centroids, BH traversal, BH task combine, local forces + clamp +
- * update}.  counts_out[3] (nullable) = {leaf-pair interactions incl. the
- * zero self terms, monopole interactions, node opening tests} over this
+ * update}.  counts_out[4] (nullable) = {leaf-pair interactions incl. the
+ * zero self terms, monopole interactions, node opening tests, warp lane
+ * slots spent (32 per visited node + 32 per leaf-loop iteration)} over this
  * rank's points, from a separate instrumented traversal before the timed
  * step.  Synchronizes the stream. */
 MDC_API int mdc_layout_profile(MdcLayoutPlan *plan, const double *temps, float *ms_out, int64_t *counts_out,

@@ -39,6 +39,10 @@ struct TreeShape {
     // per level L (0..max_depth-1): frontier segments sorted by lo
     std::vector<int32_t> seg_off;                      // size levels+1
     std::vector<int32_t> seg_lo, seg_hi, seg_node, seg_split;
+    // seg_of[L * n + k]: global frontier segment of sorted position k at level
+    // L (data-independent: the tree shape depends only on n) -- one coalesced
+    // load instead of a binary search per element per phase
+    std::vector<int32_t> seg_of;
     // per depth L (0..max_depth): nodes created at that depth
     std::vector<int32_t> nd_off, nd_list;
     // leaves in left-to-right order and each node's contiguous leaf range
@@ -136,6 +140,10 @@ static void make_shape(TreeShape &t, int64_t n, int leaf) {
         }
         t.seg_off.push_back((int32_t)t.seg_lo.size());
     }
+    t.seg_of.resize((size_t)t.max_depth * (size_t)n);
+    for (int L = 0; L < t.max_depth; ++L)
+        for (int g = t.seg_off[L]; g < t.seg_off[L + 1]; ++g)
+            for (int32_t k = t.seg_lo[g]; k < t.seg_hi[g]; ++k) t.seg_of[(size_t)L * n + k] = g;
 }
 
 // ---------------------------------------------------------------------------
@@ -154,7 +162,7 @@ struct Carver {
 
 struct DevTree {
     int32_t *lo, *hi, *left, *right, *axis;
-    int32_t *seg_lo, *seg_hi, *seg_node, *seg_split, *nd_list;
+    int32_t *seg_lo, *seg_hi, *seg_node, *seg_split, *nd_list, *seg_of;
     int32_t *leaves, *leaf_lo, *leaf_hi;
     int32_t *seg_off, *nd_off;
     int32_t *task_node, *task_path, *task_first;
@@ -205,6 +213,7 @@ static size_t carve(Buffers &b, char *base, const TreeShape &s) {
     b.t.seg_hi = c.take<int32_t>(ns);
     b.t.seg_node = c.take<int32_t>(ns);
     b.t.seg_split = c.take<int32_t>(ns);
+    b.t.seg_of = c.take<int32_t>(std::max<size_t>(1, (size_t)s.max_depth * (size_t)(n > 0 ? n : 1)));
     size_t nl = s.leaves.size() ? s.leaves.size() : 1;
     b.t.seg_off = c.take<int32_t>(s.seg_off.size() + 1);
     b.t.task_node = c.take<int32_t>(s.task_node.size() + 1);
@@ -577,9 +586,25 @@ __global__ void __launch_bounds__(BSORT_THREADS) block_sort_kernel(const double 
 //   phase 4  stable partition of the other run, copy the rest (grid sync)
 // then leaf sums + leaf-order gather, and centroids.
 namespace cg = cooperative_groups;
-constexpr int BUILD_THREADS = 256;   // cooperative (multi-CTA) walk
+#ifndef MDC_BUILD_THREADS
+#define MDC_BUILD_THREADS 256
+#endif
+constexpr int BUILD_THREADS = MDC_BUILD_THREADS;  // cooperative (multi-CTA) walk
 constexpr int BUILD_SINGLE_THREADS = 1024;
 constexpr int64_t BUILD_SINGLE_MAX = 2048;  // one CTA walks the tree up to this n (A/B: slower at 10k)
+// Mid-size n: ONE thread-block cluster walks the tree; its per-phase barrier
+// is barrier.cluster (hardware, ~sub-microsecond) instead of a grid-wide
+// cooperative sync across hundreds of CTAs (~4 us per phase measured).
+#ifndef MDC_BUILD_CLUSTER
+#define MDC_BUILD_CLUSTER 16
+#endif
+constexpr int BUILD_CLUSTER = MDC_BUILD_CLUSTER;
+constexpr int BUILD_CLUSTER_THREADS = 1024;
+#ifndef MDC_BUILD_CLUSTER_MAX
+#define MDC_BUILD_CLUSTER_MAX 16384
+#endif
+constexpr int64_t BUILD_CLUSTER_MAX = MDC_BUILD_CLUSTER_MAX;
+enum BuildMode { BUILD_ONE_CTA = 0, BUILD_ONE_CLUSTER = 1, BUILD_GRID = 2 };
 
 struct BuildArgs {
     const double *pts;
@@ -607,17 +632,22 @@ __device__ __forceinline__ void stats_for(const BuildArgs &a, int node, const in
 
 // SINGLE = one CTA does the whole walk (small n): block barriers instead of
 // grid-wide ones, same code otherwise.
-template <int NTH, bool SINGLE>
+template <int NTH, int MODE>
 __global__ void __launch_bounds__(NTH) build_levels_kernel(BuildArgs a) {
     constexpr int BUILD_THREADS = NTH;
     typedef cub::BlockReduce<int, BUILD_THREADS> BR;
     typedef cub::BlockScan<int, BUILD_THREADS> BS;
     struct Sync {
         __device__ void sync() const {
-            if constexpr (SINGLE)
+            if constexpr (MODE == BUILD_ONE_CTA) {
                 __syncthreads();
-            else
+            } else if constexpr (MODE == BUILD_ONE_CLUSTER) {
+                // release/acquire at cluster scope: global-memory writes of
+                // every CTA in the cluster are visible after the barrier
+                asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+            } else {
                 cg::this_grid().sync();
+            }
         }
     } grid;
     __shared__ union {
@@ -637,9 +667,9 @@ __global__ void __launch_bounds__(NTH) build_levels_kernel(BuildArgs a) {
         const int d0 = t.nd_off[L], dn = t.nd_off[L + 1] - d0;
         for (int64_t e = gtid; e < dn; e += gsz) stats_for(a, t.nd_list[d0 + e], X, Y);
         if (L == a.max_depth) break;
-        const int seg0 = t.seg_off[L], nseg = t.seg_off[L + 1] - seg0;
+        // frontier segments of level L: t.seg_of[L * n + k] (global indices)
         for (int64_t k = gtid; k < n; k += gsz) {
-            int s = seg0 + find_seg(t.seg_lo + seg0, nseg, (int)k);
+            int s = t.seg_of[(int64_t)L * n + k];
             if (!t.seg_split[s]) continue;
             int lo = t.seg_lo[s], hi = t.seg_hi[s];
             double ex = a.pts[2 * X[hi - 1]] - a.pts[2 * X[lo]];
@@ -651,7 +681,7 @@ __global__ void __launch_bounds__(NTH) build_levels_kernel(BuildArgs a) {
         // ---- phase 2: other-run flags, per-block counts over this block's chunk
         int cnt = 0;
         for (int64_t k = c_lo + tid; k < c_hi; k += BUILD_THREADS) {
-            int s = seg0 + find_seg(t.seg_lo + seg0, nseg, (int)k);
+            int s = t.seg_of[(int64_t)L * n + k];
             int v = 0;
             if (t.seg_split[s]) {
                 const int32_t *O = t.axis[t.seg_node[s]] ? X : Y;
@@ -682,7 +712,7 @@ __global__ void __launch_bounds__(NTH) build_levels_kernel(BuildArgs a) {
         grid.sync();
         // ---- phase 4: stable partition
         for (int64_t k = gtid; k < n; k += gsz) {
-            int s = seg0 + find_seg(t.seg_lo + seg0, nseg, (int)k);
+            int s = t.seg_of[(int64_t)L * n + k];
             if (!t.seg_split[s]) {
                 Xn[k] = X[k];
                 Yn[k] = Y[k];
@@ -758,7 +788,14 @@ __global__ void __launch_bounds__(NTH) build_levels_kernel(BuildArgs a) {
 
 // ---------------------------------------------------------------------------
 // Barnes-Hut traversal (warp-cooperative union DFS).
-constexpr int BH_WARPS = 4;
+#ifndef MDC_BH_WARPS
+#define MDC_BH_WARPS 4
+#endif
+#ifndef MDC_BH_UNROLL
+#define MDC_BH_UNROLL 8
+#endif
+constexpr int BH_WARPS = MDC_BH_WARPS;
+constexpr int BH_UNROLL = MDC_BH_UNROLL;
 constexpr int BH_STACK = 64;
 
 // fp64 reciprocal / reciprocal square root: MUFU seed + one third-order
@@ -812,7 +849,7 @@ template <bool COUNT>
 __global__ void __launch_bounds__(BH_WARPS * 32) bh_kernel(int64_t n, int64_t k0, int64_t k1, DevTree t,
                                                            double c, double eta, double theta,
                                                            unsigned long long *cnt) {
-    unsigned long long n_leaf = 0, n_mono = 0, n_test = 0;
+    unsigned long long n_leaf = 0, n_mono = 0, n_test = 0, n_slot = 0;
     __shared__ int s_node[BH_WARPS][BH_STACK];
     __shared__ unsigned s_mask[BH_WARPS][BH_STACK];
     const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -855,6 +892,7 @@ __global__ void __launch_bounds__(BH_WARPS * 32) bh_kernel(int64_t n, int64_t k0
             __syncwarp();
             bool on = (mask >> lane) & 1u;
             int4 tp = t.topo[node];
+            if (COUNT && lane == 0) n_slot += tp.z < 0 ? 32ull * (unsigned long long)(tp.y - tp.x) : 32ull;
             if (tp.z < 0) {
                 // Leaf: pairwise sum over its points (_kernels.py:194-205).  The
                 // self term is exactly +0 (dx = dy = 0; r2 is floored so the
@@ -862,7 +900,7 @@ __global__ void __launch_bounds__(BH_WARPS * 32) bh_kernel(int64_t n, int64_t k0
                 // coincident distinct points also contribute 0 in the reference.
                 if (on) {
                     if (COUNT) n_leaf += (unsigned long long)(tp.y - tp.x);
-#pragma unroll 4
+#pragma unroll BH_UNROLL
                     for (int q = tp.x; q < tp.y; ++q) {
                         double2 pj = __ldg(sp2 + q);
                         double dx = xi - pj.x, dy = yi - pj.y;
@@ -906,6 +944,7 @@ __global__ void __launch_bounds__(BH_WARPS * 32) bh_kernel(int64_t n, int64_t k0
         atomicAdd(cnt + 0, n_leaf);
         atomicAdd(cnt + 1, n_mono);
         atomicAdd(cnt + 2, n_test);
+        if (lane == 0) atomicAdd(cnt + 3, n_slot);
     }
 }
 
@@ -1065,6 +1104,7 @@ struct MdcLayoutPlan {
     const double *graph_temps = nullptr;
     int build_blocks = 0;
     // profiling (mdc_layout_profile): events recorded between step phases
+    bool cluster_ok = false;  // the device can co-schedule one BUILD_CLUSTER cluster
     cudaEvent_t ev[8] = {};
     int nev = 0;
     bool timing = false;
@@ -1119,11 +1159,24 @@ static int build_tree(MdcLayoutPlan *p, const double *pts, cudaStream_t s, const
     ba.prefix = reinterpret_cast<int32_t *>(b.kx);
     ba.blocksum = b.blocksum;
     if (n <= BUILD_SINGLE_MAX) {
-        build_levels_kernel<BUILD_SINGLE_THREADS, true><<<1, BUILD_SINGLE_THREADS, 0, s>>>(ba);
+        build_levels_kernel<BUILD_SINGLE_THREADS, BUILD_ONE_CTA><<<1, BUILD_SINGLE_THREADS, 0, s>>>(ba);
         MDC_CHECK_LAUNCH();
+    } else if (n <= BUILD_CLUSTER_MAX && p->cluster_ok) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(BUILD_CLUSTER);
+        cfg.blockDim = dim3(BUILD_CLUSTER_THREADS);
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = BUILD_CLUSTER;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        MDC_CHECK_CUDA(cudaLaunchKernelEx(&cfg, build_levels_kernel<BUILD_CLUSTER_THREADS, BUILD_ONE_CLUSTER>, ba));
     } else {
         void *kargs[] = {&ba};
-        MDC_CHECK_CUDA(cudaLaunchCooperativeKernel((const void *)build_levels_kernel<BUILD_THREADS, false>,
+        MDC_CHECK_CUDA(cudaLaunchCooperativeKernel((const void *)build_levels_kernel<BUILD_THREADS, BUILD_GRID>,
                                                    dim3(p->build_blocks), dim3(BUILD_THREADS), kargs, 0, s));
     }
     p->mark(s);  // tree levels + centroids done
@@ -1250,6 +1303,7 @@ extern "C" int mdc_layout_plan_create(const MdcLayoutArgs *a, MdcLayoutPlan **pl
     rc |= up(p->b.t.seg_hi, sh.seg_hi);
     rc |= up(p->b.t.seg_node, sh.seg_node);
     rc |= up(p->b.t.seg_split, sh.seg_split);
+    rc |= up(p->b.t.seg_of, sh.seg_of);
     rc |= up(p->b.t.leaves, sh.leaves);
     rc |= up(p->b.t.seg_off, sh.seg_off);
     rc |= up(p->b.t.task_node, sh.task_node);
@@ -1267,11 +1321,27 @@ extern "C" int mdc_layout_plan_create(const MdcLayoutArgs *a, MdcLayoutPlan **pl
         int dev = 0, sms = 0, per_sm = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, build_levels_kernel<BUILD_THREADS, false>,
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, build_levels_kernel<BUILD_THREADS, BUILD_GRID>,
                                                       BUILD_THREADS, 0);
         int want = (int)((p->shape.n + BUILD_THREADS - 1) / BUILD_THREADS);
         p->build_blocks = std::max(1, std::min(std::max(1, per_sm) * sms, want));
         if (p->build_blocks > 1024) p->build_blocks = 1024;  // blocksum capacity below
+        auto ck = build_levels_kernel<BUILD_CLUSTER_THREADS, BUILD_ONE_CLUSTER>;
+        if (BUILD_CLUSTER > 8)
+            cudaFuncSetAttribute(ck, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(BUILD_CLUSTER);
+        cfg.blockDim = dim3(BUILD_CLUSTER_THREADS);
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = BUILD_CLUSTER;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int nclusters = 0;
+        p->cluster_ok = cudaOccupancyMaxActiveClusters(&nclusters, ck, &cfg) == cudaSuccess && nclusters >= 1;
+        cudaGetLastError();  // a refused query leaves the cooperative path in charge
     }
     cudaMemsetAsync(p->b.runflag, 0, sizeof(int32_t) * 2 * (size_t)p->shape.n, s);
     // host vectors must outlive the async copies
@@ -1344,17 +1414,17 @@ extern "C" int mdc_layout_profile(MdcLayoutPlan *p, const double *temps, float *
     // instrumented traversal first (its own launch, outside the timing)
     if (counts_out) {
         unsigned long long *cnt = nullptr;
-        MDC_CHECK_CUDA(cudaMallocAsync((void **)&cnt, 3 * sizeof(unsigned long long), s));
-        MDC_CHECK_CUDA(cudaMemsetAsync(cnt, 0, 3 * sizeof(unsigned long long), s));
+        MDC_CHECK_CUDA(cudaMallocAsync((void **)&cnt, 4 * sizeof(unsigned long long), s));
+        MDC_CHECK_CUDA(cudaMemsetAsync(cnt, 0, 4 * sizeof(unsigned long long), s));
         p->count = cnt;
         int rc = run_bh(p, p->a.pos, p->b.bh, s);
         p->count = nullptr;
         if (rc) return rc;
-        unsigned long long h[3];
+        unsigned long long h[4];
         MDC_CHECK_CUDA(cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, s));
         MDC_CHECK_CUDA(cudaStreamSynchronize(s));
         MDC_CHECK_CUDA(cudaFreeAsync(cnt, s));
-        for (int i = 0; i < 3; ++i) counts_out[i] = (int64_t)h[i];
+        for (int i = 0; i < 4; ++i) counts_out[i] = (int64_t)h[i];
     }
     for (int i = 0; i < 8; ++i)
         if (!p->ev[i]) MDC_CHECK_CUDA(cudaEventCreate(&p->ev[i]));

@@ -175,13 +175,13 @@ class LayoutEngine:
         (mdc_layout_profile) and, optionally, the BH interaction counts."""
         t = torch.tensor([float(temperature)], dtype=torch.float64, device=self.device)
         ms = (ctypes.c_float * 5)()
-        cnt = (ctypes.c_int64 * 3)()
+        cnt = (ctypes.c_int64 * 4)()
         _lib.check(self.lib.mdc_layout_profile(self.plan(), _lib.ptr(t), ctypes.cast(ms, ctypes.c_void_p),
                                                ctypes.cast(cnt, ctypes.c_void_p) if count else None,
                                                _lib.stream_ptr()), "mdc_layout_profile")
         out = {"ms": dict(zip(self.PHASES, (float(v) for v in ms)))}
         if count:
-            out["leaf_pairs"], out["monopoles"], out["node_tests"] = (int(v) for v in cnt)
+            out["leaf_pairs"], out["monopoles"], out["node_tests"], out["lane_slots"] = (int(v) for v in cnt)
         return out
 
     def repulsion(self, pts: torch.Tensor) -> torch.Tensor:
