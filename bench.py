@@ -504,7 +504,8 @@ def main():
 
 def run_e2e(args, positions, raw, spacing, W, H, d, r0, r1, dev, world):
     """The same frame through the public API: pinned host inputs -> H2D ->
-    kernels -> D2H of the fp32 field, every step."""
+    kernels -> D2H of the fp32 field, every step (field.compute_fields_to_host:
+    per-band D2H overlapped with the next band's kernels)."""
     import torch
     import torch.distributed as dist
 
@@ -519,11 +520,10 @@ def run_e2e(args, positions, raw, spacing, W, H, d, r0, r1, dev, world):
     h2d = [0]
 
     def e2e_step():
-        blk = F.compute_fields(pin_pos.numpy(), pin_raw.numpy(), mp, W, H, row_range=(r0, r1),
-                               dtype="f32", band_spacing=spacing)
-        host_out.copy_(blk.values, non_blocking=True)
-        torch.cuda.current_stream().synchronize()
-        h2d[0] = blk.h2d_bytes
+        # public API with host buffers in and out: the frame's row bands are
+        # copied back while the next band computes (compute_fields_to_host)
+        h2d[0] = F.compute_fields_to_host(pin_pos, pin_raw, mp, W, H, host_out,
+                                          row_range=(r0, r1), dtype="f32", band_spacing=spacing)
 
     e2e_step()
     torch.cuda.synchronize()

@@ -111,6 +111,17 @@ typedef struct MdcMlsArgs {
 MDC_API int mdc_mls_field(const MdcMlsArgs *a, void *stream);
 MDC_API size_t mdc_mls_workspace_bytes(const MdcMlsArgs *a);
 
+/* Input staging (field.py:607-613): from raw positions (n x 2) and targets
+ * (n x d, fp64, device), compute pm (2) and qm (d) -- deterministic chunked
+ * column means, identical on every device -- the centred controls pc
+ * (n x 2 fp64) and the padded target block q (n x ldq, MDC_F32/MDC_F64):
+ * qc = tvals - qm, or for MDC_MEAN dq = qc - pc[:, axis[k]] (_kernels.py:
+ * 52-67); columns d..ldq-1 are zero.  workspace: mdc_mls_prepare_workspace_bytes. */
+MDC_API size_t mdc_mls_prepare_workspace_bytes(int32_t d);
+MDC_API int mdc_mls_prepare(int64_t n, int32_t d, const double *positions, const double *tvals, int32_t variant,
+                            int32_t dtype, const int32_t *axis, int32_t ldq, double *pc, void *q, double *pm,
+                            double *qm, void *workspace, size_t workspace_bytes, void *stream);
+
 /* Snap (field.py:388-412): pixels of rows [row0,row1) whose centre lies at
  * squared distance < eps from control i (un-centred positions, fp64 decisions
  * with the reference's exact rounding sequence) take tvals[i] (n x d fp64,
@@ -291,6 +302,11 @@ MDC_API int mdc_pca(int64_t n, int32_t d, const double *x, double *mean, double 
 MDC_API int mdc_peak_ffma(float *sink, int32_t blocks, int32_t iters, void *stream);
 MDC_API int mdc_peak_dfma(double *sink, int32_t blocks, int32_t iters, void *stream);
 MDC_API int mdc_num_sms(void);
+/* Stream-ordered strided copy (cudaMemcpy2DAsync, any direction): `height`
+ * rows of `width_bytes`; used to deliver a row band of every channel plane
+ * to pinned host memory in one call while the next band computes. */
+MDC_API int mdc_copy_2d_async(void *dst, size_t dpitch, const void *src, size_t spitch, size_t width_bytes,
+                              size_t height, void *stream);
 
 #ifdef __cplusplus
 }

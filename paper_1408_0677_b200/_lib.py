@@ -110,6 +110,11 @@ SIGNATURES = {
     "mdc_layout_plan_create": (ctypes.c_int, [ctypes.POINTER(MdcLayoutArgs), ctypes.POINTER(_vp), _vp]),
     "mdc_layout_plan_destroy": (ctypes.c_int, [_vp]),
     "mdc_layout_steps": (ctypes.c_int, [_vp, _c_i32, _vp, _c_i32, _vp]),
+    "mdc_mls_prepare_workspace_bytes": (ctypes.c_size_t, [ctypes.c_int32]),
+    "mdc_mls_prepare": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int32, _vp, _vp, ctypes.c_int32, ctypes.c_int32,
+                                       _vp, ctypes.c_int32, _vp, _vp, _vp, _vp, _vp, ctypes.c_size_t, _vp]),
+    "mdc_copy_2d_async": (ctypes.c_int, [_vp, ctypes.c_size_t, _vp, ctypes.c_size_t, ctypes.c_size_t,
+                                         ctypes.c_size_t, _vp]),
     "mdc_layout_profile": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp]),
     "mdc_layout_repulsion": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
     "mdc_layout_node_count": (_c_i64, [_vp]),

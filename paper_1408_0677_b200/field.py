@@ -281,6 +281,13 @@ class FieldBlock:
             raise FieldError("field evaluation produced non-finite coordinates")
 
 
+def _to_device(t: torch.Tensor, device: torch.device) -> torch.Tensor:
+    """CPU tensor -> device (async when the caller's tensor is pinned)."""
+    if t.is_cuda:
+        return t.to(device)
+    return t.to(device, non_blocking=t.is_pinned())
+
+
 def _h2d(arr: np.ndarray, device: torch.device) -> torch.Tensor:
     """Host -> device through a pinned staging buffer (async on the current stream)."""
     t = torch.from_numpy(np.ascontiguousarray(arr))
@@ -306,12 +313,17 @@ class MlsProblem:
         self.lib = lib
         if variant not in ("mean", "affine", "rigid"):
             raise ValueError(f"GPU MLS variant must be mean, affine or rigid, got {variant!r}")
-        positions = np.ascontiguousarray(positions, dtype=np.float64)
-        tvals = np.ascontiguousarray(targets, dtype=np.float64)
-        if tvals.ndim == 1:
-            tvals = tvals[:, None]
-        n, d = tvals.shape
-        if len(positions) != n:
+        # inputs may be numpy arrays or (ideally pinned) CPU torch tensors
+        pos_t0 = positions if torch.is_tensor(positions) else torch.from_numpy(
+            np.ascontiguousarray(positions, dtype=np.float64))
+        tv_t0 = targets if torch.is_tensor(targets) else torch.from_numpy(
+            np.ascontiguousarray(targets, dtype=np.float64))
+        pos_t0 = pos_t0.to(torch.float64).contiguous()
+        tv_t0 = tv_t0.to(torch.float64).contiguous()
+        if tv_t0.ndim == 1:
+            tv_t0 = tv_t0[:, None]
+        n, d = tv_t0.shape
+        if pos_t0.shape[0] != n:
             raise ValueError("positions and targets disagree on the control count")
         if variant == "rigid" and d != 2:
             raise FieldError("rigid MLS needs exactly two target channels")
@@ -323,33 +335,33 @@ class MlsProblem:
         self.width, self.height, self.n, self.d = int(width), int(height), n, d
         self.alpha = DEFAULT_ALPHA[variant] if alpha is None else float(alpha)
         self.reg_eps = float(reg_eps)
-        self.transform = ViewportTransform.fit(positions, width, height)
+        pos_np = pos_t0.numpy() if not pos_t0.is_cuda else pos_t0.cpu().numpy()
+        self.transform = ViewportTransform.fit(pos_np, width, height)
         sx, sy = self.transform.units_per_px
         self.eps = epsilon_dist if epsilon_dist is not None else (0.25 * max(sx, sy)) ** 2
-        # field.py:607-610 -- identical numpy expressions
-        pm = positions.mean(axis=0)
-        qm = tvals.mean(axis=0)
-        pc = positions - pm
-        qc = tvals - qm
-        self.pm = pm
+        dev = self.device
+        # raw inputs to the device once; centring + dtype/padding on the device
+        # (mdc_mls_prepare: field.py:607-613, deterministic means)
+        self.pos_t = _to_device(pos_t0, dev)
+        self.tvals_t = _to_device(tv_t0, dev)
         if variant == "mean":
             ax = np.zeros(d, dtype=np.int32) if axis is None else np.asarray(axis, dtype=np.int32)
-            qk = qc - pc[:, ax]              # _kernels.py:52-67 dq = qc - pc
         else:
             ax = np.zeros(d, dtype=np.int32)
-            qk = qc
+        self.axis_t = _to_device(torch.from_numpy(np.ascontiguousarray(ax)), dev)
         ldq = _ldq(d, self.dcode, self.vcode)
-        qpad = np.zeros((n, ldq), dtype=np.float32 if self.dcode == _lib.MDC_F32 else np.float64)
-        qpad[:, :d] = qk
-        dev = self.device
-        self.pc_t = _h2d(pc, dev)
-        self.q_t = _h2d(qpad, dev)
-        self.qm_t = _h2d(qm, dev)
-        self.axis_t = _h2d(ax, dev)
-        self.pos_t = _h2d(positions, dev)
-        self.tvals_t = _h2d(tvals, dev)
-        self.h2d_bytes = sum(t.numel() * t.element_size() for t in
-                             (self.pc_t, self.q_t, self.qm_t, self.axis_t, self.pos_t, self.tvals_t))
+        self.pc_t = torch.empty((n, 2), dtype=torch.float64, device=dev)
+        self.q_t = torch.empty((n, ldq), dtype=self.tdtype, device=dev)
+        pm_t = torch.empty(2, dtype=torch.float64, device=dev)
+        self.qm_t = torch.empty(d, dtype=torch.float64, device=dev)
+        wsb = int(lib.mdc_mls_prepare_workspace_bytes(d))
+        ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+        _lib.check(lib.mdc_mls_prepare(n, d, _lib.ptr(self.pos_t), _lib.ptr(self.tvals_t), self.vcode, self.dcode,
+                                       _lib.ptr(self.axis_t), ldq, _lib.ptr(self.pc_t), _lib.ptr(self.q_t),
+                                       _lib.ptr(pm_t), _lib.ptr(self.qm_t), _lib.ptr(ws), wsb, _lib.stream_ptr()),
+                   "mdc_mls_prepare")
+        self.pm = pm_t.cpu().numpy()  # the kernels take the frame centre by value
+        self.h2d_bytes = sum(t.numel() * t.element_size() for t in (self.pos_t, self.tvals_t, self.axis_t))
         self.ldq = ldq
         self.flags = 0 if tensor_cores else _lib.MDC_FLAG_NO_TC
         self._ws = None
@@ -424,6 +436,79 @@ def compute_fields(positions, targets, params: MlsParams, width: int, height: in
     h2d = 0 if problem is not None else prob.h2d_bytes + (spacing_t.numel() * 8 if spacing_t is not None else 0)
     return FieldBlock(values=out, bands=bands, transform=prob.transform, row0=r0, row1=r1,
                       nonfinite=nonfinite, h2d_bytes=h2d)
+
+
+def compute_fields_to_host(positions, targets, params: MlsParams, width: int, height: int,
+                           out: torch.Tensor, bands_out: torch.Tensor | None = None, row_range=None,
+                           dtype="f32", band_spacing=None, nbands: int = 4, tensor_cores: bool = True) -> int:
+    """``compute_fields`` with the result delivered into HOST memory: ``out``
+    (d, rows, W) pinned float tensor (and optional int32 ``bands_out``).
+
+    The frame is evaluated in ``nbands`` row bands; each band's device->host
+    copy runs on a side stream while the next band computes (two device band
+    buffers, event-ordered), so only the last band's copy is exposed.  Bands
+    are bit-identical to the whole-frame result (tile frames are global).
+    Returns the host->device bytes uploaded.  Raises FieldError on
+    non-finite output."""
+    if params.variant == "linear":
+        raise FieldError("compute_fields_to_host(variant='linear') is not supported; use linear_device")
+    prob = MlsProblem(positions, targets, params.variant, width, height, alpha=params.resolved_alpha,
+                      reg_eps=params.reg_eps, epsilon_dist=params.epsilon_dist, dtype=dtype,
+                      tensor_cores=tensor_cores)
+    r0, r1 = (0, height) if row_range is None else (int(row_range[0]), int(row_range[1]))
+    rows = r1 - r0
+    d = prob.d
+    if tuple(out.shape) != (d, rows, width) or out.is_cuda or out.dtype != prob.tdtype or not out.is_contiguous():
+        raise ValueError(f"out must be a contiguous host {prob.tdtype} tensor of shape {(d, rows, width)}")
+    if bands_out is not None and (tuple(bands_out.shape) != (d, rows, width) or bands_out.is_cuda
+                                  or bands_out.dtype != torch.int32 or not bands_out.is_contiguous()):
+        raise ValueError(f"bands_out must be a contiguous host int32 tensor of shape {(d, rows, width)}")
+    dev = prob.device
+    nb = max(1, min(int(nbands), rows))
+    step = -(-rows // nb)
+    spacing_t = None
+    if band_spacing is not None:
+        sp = np.broadcast_to(np.asarray(band_spacing, dtype=np.float64), (d,)).copy()
+        spacing_t = _h2d(sp, dev)
+    nonfinite = torch.zeros((), dtype=torch.int32, device=dev)
+    vbuf = [torch.empty((d, step, width), dtype=prob.tdtype, device=dev) for _ in range(2)]
+    bbuf = [torch.empty((d, step, width), dtype=torch.int32, device=dev) for _ in range(2)] \
+        if bands_out is not None else [None, None]
+    compute = torch.cuda.current_stream(dev)
+    copy = torch.cuda.Stream(device=dev)
+    done = [None, None]  # copy-finished events per buffer
+    for i, b0 in enumerate(range(r0, r1, step)):
+        b1 = min(b0 + step, r1)
+        n_rows = b1 - b0
+        k = i & 1
+        if done[k] is not None:
+            compute.wait_event(done[k])
+        v = vbuf[k][:, :n_rows]
+        bt = bbuf[k][:, :n_rows] if bbuf[k] is not None else None
+        a = prob.args(v, (step * width, width, 1), b0, b1, bt, (step * width, width), spacing_t, nonfinite)
+        prob.run(a)
+        ready = torch.cuda.Event()
+        ready.record(compute)
+        copy.wait_event(ready)
+        # one strided async copy per plane set: d rows of (n_rows x W) elements
+        for src, dst in ((v, out), (bt, bands_out)):
+            if src is None:
+                continue
+            es = src.element_size()
+            _lib.check(prob.lib.mdc_copy_2d_async(
+                ctypes.c_void_p(dst.data_ptr() + (b0 - r0) * width * es), rows * width * es,
+                _lib.ptr(src), step * width * es, n_rows * width * es, d, ctypes.c_void_p(copy.cuda_stream)),
+                "mdc_copy_2d_async")
+        ev = torch.cuda.Event()
+        ev.record(copy)
+        done[k] = ev
+        vbuf[k].record_stream(copy)
+        if bbuf[k] is not None:
+            bbuf[k].record_stream(copy)
+    copy.synchronize()
+    if int(nonfinite.item()) != 0:
+        raise FieldError("field evaluation produced non-finite coordinates")
+    return prob.h2d_bytes + (spacing_t.numel() * 8 if spacing_t is not None else 0)
 
 
 def compute_field(mesh, positions: np.ndarray, targets: TargetAssignment, params: MlsParams,
