@@ -219,3 +219,33 @@ def test_kdtree_device_sort_exact_order(kind):
     for i in range(nn):
         assert set(gt.perm[gt.lo[i]:gt.hi[i]].tolist()) == set(ot.perm[ot.lo[i]:ot.hi[i]].tolist()), i
     assert np.array_equal(gt.bmin, ot.bmin[:nn]) and np.array_equal(gt.bmax, ot.bmax[:nn])
+
+
+def test_teacher_forced_at_bench_scale():
+    """The bench workload itself (config 3: 100k GMM points, PCA projection,
+    Delaunay mesh): GPU steps against the fp64 oracle restatement at steps 0,
+    1 and 250 of a GPU trajectory (teacher-forced: both take the same input
+    state), <= 1e-12 normwise; plus zero orientation flips after 250 steps."""
+    import bench
+
+    cfg = bench.CONFIGS[3]
+    ds, mesh, raw = bench.build_scene(cfg)
+    params = L.LayoutParams.defaults_for(mesh, iterations=500)
+    p = {k: getattr(params, k) for k in ("repulsion_c", "spring_scale", "desired_edge_d", "softening_eta",
+                                         "bh_theta", "initial_temp", "decay_lambda")}
+    temps = L.temperature_schedule(params.initial_temp, params.decay_lambda, 251)
+    eng = L.LayoutEngine(mesh, params)
+    eng.set_positions(mesh.original_pos)
+    states = {0: mesh.original_pos.copy()}
+    eng.run(temps[:1])
+    states[1] = eng.pos.cpu().numpy()
+    eng.run(temps[1:250])
+    states[250] = eng.pos.cpu().numpy()
+    signs0 = np.sign(mesh.signed_areas(mesh.original_pos))
+    assert np.array_equal(np.sign(mesh.signed_areas(states[250])), signs0)
+    for k in (0, 1, 250):
+        eng.set_positions(states[k])
+        eng.run(temps[k:k + 1], use_graph=False)
+        got = eng.pos.cpu().numpy()
+        ref = O.layout_step(states[k], mesh.csr_offsets, mesh.csr_targets, mesh.triangles, p, float(temps[k]))
+        assert normwise(got, ref) <= TF_TOL, (k, normwise(got, ref))
