@@ -264,6 +264,18 @@ def layout_roofline(eng, params, lib, torch):
     }
 
 
+def _kernel_traffic(cfg, W, H, d, use_tc):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu
+    capture, when this run is the captured workload (else None)."""
+    try:
+        t = json.load(open(os.path.join(ROOT, "profiles", "r01_mls_tc_kernel_traffic.json")))
+    except (OSError, ValueError):
+        return None
+    if use_tc and t.get("frame") == [W, H] and t.get("n") == cfg["n"] and t.get("d") == d:
+        return t["traffic_bytes"]
+    return None
+
+
 def _measured_hbm_gbs():
     try:
         return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
@@ -464,8 +476,14 @@ def main():
     achieved = 2 * fma_instr / sec / 1e12          # FP32-pipe FLOP-equivalents (FMA-pipe op = 2)
     peak = peaks["fp32"] / 1e12
     tf32_peak = 0.5 * _measured_bf16_tflops()       # dense tf32 = 1/2 bf16 (measured bf16, MEASURED_PEAKS.json)
+    traffic, alg_bytes = _kernel_traffic(cfg, W, H, d, use_tc), pairs // cfg["n"] * d * 8 + cfg["n"] * (16 + 4 * d)
     roofline = {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": achieved / peak, "traffic": None,
+                "frac": achieved / peak, "traffic": traffic,
+                "traffic_def": "dram__bytes_read.sum + dram__bytes_write.sum of one launch from the committed "
+                               "ncu --set full capture of this workload (profiles/r01_mls_tc_kernel_traffic.json)",
+                "algorithmic_bytes": alg_bytes,
+                "algorithmic_bytes_def": "fp32 field + int32 bands per pixel-channel, + controls (16 B) and "
+                                         "fp32 targets per control",
                 "kernel": kname, "kernel_ms": kernel_ms,
                 "achieved_def": "FP32-pipe lane-ops executed x 2 (one FMA-pipe lane-op = one FFMA = 2 FLOP) / kernel time",
                 "peak_source": "measured FFMA microbenchmark (mdc_peak_ffma), this run",
