@@ -353,193 +353,6 @@ __global__ void run_sort_kernel(int64_t n, const unsigned long long *keys, int32
     }
 }
 
-// Node stats for nodes at one depth: bbox from the ends of the sorted runs
-// (exact min/max), size = hypot(extent) (bhtree.py:47-48), split axis
-// argmax(extent) with ties -> x (bhtree.py:56).
-__global__ void node_stats_kernel(const double *pts, DevTree t, const int32_t *nodes, int count,
-                                  const int32_t *X, const int32_t *Y) {
-    int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= count) return;
-    int node = nodes[k];
-    int lo = t.lo[node], hi = t.hi[node];
-    double xmin = pts[2 * X[lo]], xmax = pts[2 * X[hi - 1]];
-    double ymin = pts[2 * Y[lo] + 1], ymax = pts[2 * Y[hi - 1] + 1];
-    t.bmin[2 * node] = xmin;
-    t.bmin[2 * node + 1] = ymin;
-    t.bmax[2 * node] = xmax;
-    t.bmax[2 * node + 1] = ymax;
-    double ex = xmax - xmin, ey = ymax - ymin;
-    t.size[node] = hypot(ex, ey);
-    t.mass[node] = (double)(hi - lo);
-    t.axis[node] = ey > ex ? 1 : 0;
-}
-
-__device__ __forceinline__ int find_seg(const int32_t *seg_lo, int cnt, int k) {
-    int lo = 0, hi = cnt - 1;  // last segment with seg_lo <= k
-    while (lo < hi) {
-        int mid = (lo + hi + 1) >> 1;
-        if (seg_lo[mid] <= k)
-            lo = mid;
-        else
-            hi = mid - 1;
-    }
-    return lo;
-}
-
-// flag[id] = 1 if id goes left in its splitting segment (first mid of the
-// primary run), written through the primary run; 0 otherwise.
-__global__ void flag_kernel(int64_t n, DevTree t, int seg0, int nseg, const int32_t *X,
-                            const int32_t *Y, int32_t *flag) {
-    int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= n) return;
-    int s = seg0 + find_seg(t.seg_lo + seg0, nseg, k);
-    if (!t.seg_split[s]) return;
-    int node = t.seg_node[s];
-    int lo = t.seg_lo[s], hi = t.seg_hi[s];
-    int mid = (hi - lo) / 2;
-    const int32_t *P = t.axis[node] ? Y : X;
-    flag[P[k]] = (k - lo) < mid ? 1 : 0;
-}
-
-// Per-block sums of the "other run" left-flags (0 outside splitting segments).
-__device__ __forceinline__ int other_flag(int k, const DevTree &t, int seg0, int nseg,
-                                          const int32_t *X, const int32_t *Y, const int32_t *flag,
-                                          int &s_out) {
-    int s = seg0 + find_seg(t.seg_lo + seg0, nseg, k);
-    s_out = s;
-    if (!t.seg_split[s]) return 0;
-    const int32_t *O = t.axis[t.seg_node[s]] ? X : Y;
-    return flag[O[k]];
-}
-
-__global__ void __launch_bounds__(SCAN_BLOCK) blocksum_kernel(int64_t n, DevTree t, int seg0,
-                                                              int nseg, const int32_t *X,
-                                                              const int32_t *Y,
-                                                              const int32_t *flag,
-                                                              int32_t *blocksum) {
-    typedef cub::BlockReduce<int, SCAN_BLOCK> BR;
-    __shared__ typename BR::TempStorage tmp;
-    int k = blockIdx.x * SCAN_BLOCK + threadIdx.x;
-    int s;
-    int v = k < n ? other_flag(k, t, seg0, nseg, X, Y, flag, s) : 0;
-    int sum = BR(tmp).Sum(v);
-    if (threadIdx.x == 0) blocksum[blockIdx.x] = sum;
-}
-
-__global__ void __launch_bounds__(SCAN_BLOCK) blockscan_kernel(int nblocks, int32_t *blocksum) {
-    typedef cub::BlockScan<int, SCAN_BLOCK> BS;
-    __shared__ typename BS::TempStorage tmp;
-    __shared__ int carry;
-    if (threadIdx.x == 0) carry = 0;
-    __syncthreads();
-    for (int base = 0; base < nblocks; base += SCAN_BLOCK) {
-        int k = base + threadIdx.x;
-        int v = k < nblocks ? blocksum[k] : 0, ex, agg;
-        BS(tmp).ExclusiveSum(v, ex, agg);
-        if (k < nblocks) blocksum[k] = ex + carry;
-        __syncthreads();
-        if (threadIdx.x == 0) carry += agg;
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) blocksum[nblocks] = carry;
-}
-
-// Exclusive prefix of other-run flags at position k, for stable partition.
-__global__ void __launch_bounds__(SCAN_BLOCK) scatter_kernel(int64_t n, DevTree t, int seg0,
-                                                             int nseg, const int32_t *X,
-                                                             const int32_t *Y, const int32_t *flag,
-                                                             const int32_t *blocksum,
-                                                             int32_t *Xn, int32_t *Yn,
-                                                             int32_t *prefix_at) {
-    typedef cub::BlockScan<int, SCAN_BLOCK> BS;
-    __shared__ typename BS::TempStorage tmp;
-    int k = blockIdx.x * SCAN_BLOCK + threadIdx.x;
-    int s = 0;
-    int v = k < n ? other_flag(k, t, seg0, nseg, X, Y, flag, s) : 0;
-    int ex;
-    BS(tmp).ExclusiveSum(v, ex);
-    ex += blocksum[blockIdx.x];
-    if (k >= n) return;
-    prefix_at[k] = ex;  // global exclusive prefix, read back at segment starts below
-    (void)Xn;
-    (void)Yn;
-}
-
-__global__ void partition_kernel(int64_t n, DevTree t, int seg0, int nseg, const int32_t *X,
-                                 const int32_t *Y, const int32_t *flag, const int32_t *prefix,
-                                 int32_t *Xn, int32_t *Yn) {
-    int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= n) return;
-    int s = seg0 + find_seg(t.seg_lo + seg0, nseg, k);
-    if (!t.seg_split[s]) {
-        Xn[k] = X[k];
-        Yn[k] = Y[k];
-        return;
-    }
-    int node = t.seg_node[s];
-    int lo = t.seg_lo[s], hi = t.seg_hi[s];
-    int mid = (hi - lo) / 2;
-    int ax = t.axis[node];
-    const int32_t *P = ax ? Y : X;
-    const int32_t *O = ax ? X : Y;
-    int32_t *Pn = ax ? Yn : Xn;
-    int32_t *On = ax ? Xn : Yn;
-    Pn[k] = P[k];
-    int id = O[k];
-    int left_before = prefix[k] - prefix[lo];
-    int dest = flag[id] ? lo + left_before : lo + mid + (k - lo - left_before);
-    On[dest] = id;
-}
-
-// Centroids (mean, bhtree.py:46), deterministic two-level sum: one warp per
-// leaf sums its points (and gathers them into leaf order for the traversal),
-// then one warp per node sums its contiguous run of leaf sums.
-__global__ void leaf_sum_kernel(const double *pts, DevTree t, const int32_t *perm) {
-    int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    int lane = threadIdx.x & 31;
-    if (w >= t.nleaves) return;
-    int node = t.leaves[w];
-    int lo = t.lo[node], hi = t.hi[node];
-    double sx = 0.0, sy = 0.0;
-    for (int k = lo + lane; k < hi; k += 32) {
-        double2 p = reinterpret_cast<const double2 *>(pts)[perm[k]];
-        reinterpret_cast<double2 *>(t.spts)[k] = p;
-        sx += p.x;
-        sy += p.y;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        sx += __shfl_xor_sync(0xffffffffu, sx, o);
-        sy += __shfl_xor_sync(0xffffffffu, sy, o);
-    }
-    if (lane == 0) {
-        t.leaf_sum[2 * w] = sx;
-        t.leaf_sum[2 * w + 1] = sy;
-    }
-}
-
-__global__ void com_kernel(DevTree t, int nnodes) {
-    int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    int lane = threadIdx.x & 31;
-    if (w >= nnodes) return;
-    int l0 = t.leaf_lo[w], l1 = t.leaf_hi[w];
-    double sx = 0.0, sy = 0.0;
-    for (int k = l0 + lane; k < l1; k += 32) {
-        sx += t.leaf_sum[2 * k];
-        sy += t.leaf_sum[2 * k + 1];
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        sx += __shfl_xor_sync(0xffffffffu, sx, o);
-        sy += __shfl_xor_sync(0xffffffffu, sy, o);
-    }
-    if (lane == 0) {
-        double m = (double)(t.hi[w] - t.lo[w]);
-        t.com[2 * w] = sx / m;
-        t.com[2 * w + 1] = sy / m;
-    }
-}
-
 // ---------------------------------------------------------------------------
 // Small-n sort: one CTA per axis sorts all (key, id) pairs in shared memory
 // (cub::BlockRadixSort, stable -> ties by id), one launch for both axes,
@@ -615,6 +428,9 @@ struct BuildArgs {
     int32_t *flag, *oflag, *prefix, *blocksum;
 };
 
+// Node stats: bbox from the ends of the node's sorted runs (exact min/max),
+// size = hypot(extent) (bhtree.py:47-48), mass = count, split axis
+// argmax(extent) with ties -> x (bhtree.py:56).
 __device__ __forceinline__ void stats_for(const BuildArgs &a, int node, const int32_t *X, const int32_t *Y) {
     const DevTree &t = a.t;
     int lo = t.lo[node], hi = t.hi[node];
@@ -630,8 +446,12 @@ __device__ __forceinline__ void stats_for(const BuildArgs &a, int node, const in
     t.axis[node] = ey > ex ? 1 : 0;
 }
 
-// SINGLE = one CTA does the whole walk (small n): block barriers instead of
-// grid-wide ones, same code otherwise.
+// The per-level walk (membership = the reference's argpartition under the
+// (coord, id) order): phase 1 node stats + left flags through each splitting
+// node's primary run, phase 2/3 flag prefix over the other run, phase 4 stable
+// partition.  MODE picks the barrier between phases: one CTA (small n,
+// __syncthreads), one thread-block cluster (barrier.cluster), or the whole
+// cooperative grid (grid.sync); the code is otherwise identical.
 template <int NTH, int MODE>
 __global__ void __launch_bounds__(NTH) build_levels_kernel(BuildArgs a) {
     constexpr int BUILD_THREADS = NTH;

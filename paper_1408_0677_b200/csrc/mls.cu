@@ -521,7 +521,10 @@ size_t mls_tc_workspace_bytes(int d, int64_t n);
 int launch_mls_tc(const KArgs &k, void *ws, cudaStream_t s);
 
 static bool tc_eligible(const MdcMlsArgs *a) {
-    return a->dtype == MDC_F32 && a->variant == MDC_AFFINE && a->d >= 8 && !(a->flags & MDC_FLAG_NO_TC);
+#ifndef MDC_TC_MIN_D
+#define MDC_TC_MIN_D 8
+#endif
+    return a->dtype == MDC_F32 && a->variant == MDC_AFFINE && a->d >= MDC_TC_MIN_D && !(a->flags & MDC_FLAG_NO_TC);
 }
 
 }  // namespace mdc
