@@ -611,11 +611,10 @@ __global__ void __launch_bounds__(NTH) build_levels_kernel(BuildArgs a) {
 #ifndef MDC_BH_WARPS
 #define MDC_BH_WARPS 4
 #endif
-#ifndef MDC_BH_UNROLL
-#define MDC_BH_UNROLL 8
+#ifndef MDC_BH_SPLIT
+#define MDC_BH_SPLIT 1
 #endif
 constexpr int BH_WARPS = MDC_BH_WARPS;
-constexpr int BH_UNROLL = MDC_BH_UNROLL;
 constexpr int BH_STACK = 64;
 
 // fp64 reciprocal / reciprocal square root: MUFU seed + one third-order
@@ -720,18 +719,34 @@ __global__ void __launch_bounds__(BH_WARPS * 32) bh_kernel(int64_t n, int64_t k0
                 // coincident distinct points also contribute 0 in the reference.
                 if (on) {
                     if (COUNT) n_leaf += (unsigned long long)(tp.y - tp.x);
-#pragma unroll BH_UNROLL
-                    for (int q = tp.x; q < tp.y; ++q) {
+                    // + 1e-300 keeps the self term finite (r2 = 0) and is
+                    // absorbed exactly by any r2 > ~1e-284.
+                    auto pair = [&](int q, double &ax, double &ay) {
                         double2 pj = __ldg(sp2 + q);
                         double dx = xi - pj.x, dy = yi - pj.y;
-                        // + 1e-300 keeps the self term finite (r2 = 0) and is
-                        // absorbed exactly by any r2 > ~1e-284.
                         double r2 = fma(dx, dx, fma(dy, dy, 1e-300));
                         double y = rsqrt_nr(r2);
                         double w = rcp_nr(r2 * (r2 * y) + eta);
-                        fx = fma(w, dx, fx);
-                        fy = fma(w, dy, fy);
+                        ax = fma(w, dx, ax);
+                        ay = fma(w, dy, ay);
+                    };
+#if MDC_BH_SPLIT
+                    // two independent accumulation chains (even / odd q),
+                    // merged per leaf: more fp64 ILP per lane
+                    double gx = 0.0, gy = 0.0;
+                    int q = tp.x;
+#pragma unroll 4
+                    for (; q + 1 < tp.y; q += 2) {
+                        pair(q, fx, fy);
+                        pair(q + 1, gx, gy);
                     }
+                    if (q < tp.y) pair(q, fx, fy);
+                    fx += gx;
+                    fy += gy;
+#else
+#pragma unroll 8
+                    for (int q = tp.x; q < tp.y; ++q) pair(q, fx, fy);
+#endif
                 }
                 continue;
             }
