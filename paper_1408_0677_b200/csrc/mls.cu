@@ -80,6 +80,11 @@ __global__ void __launch_bounds__(NT, MDC_MLS_MINB) mls_kernel(KArgs a) {
         vy[r] = to_t<T>(vyg[r] - oy);
     }
     const int64_t ntiles = (a.n + NT - 1) / NT;
+    // fp32 with two pixels per thread: the two pixels are the two lanes of
+    // packed f32x2 arithmetic (FFMA2/FADD2/FMUL2, one issue slot for both);
+    // control data is a broadcast operand.  Lane-wise identical to the scalar
+    // code below except for the per-tile accumulation, which is also per lane.
+    constexpr bool PK = sizeof(T) == 4 && R == 2;
 
     // Generic streaming loop over all control tiles; body(sxy, sq, count).
     auto stream_controls = [&](int c0, bool need_q, auto &&body) {
@@ -116,30 +121,55 @@ __global__ void __launch_bounds__(NT, MDC_MLS_MINB) mls_kernel(KArgs a) {
             tsw[r] = tmx[r] = tmy[r] = tsxx[r] = tsxy[r] = tsyy[r] = 0.0;
         }
         stream_controls(0, false, [&](const T *, int cnt) {
+            if constexpr (PK) {
+                const float2 nvx = make_float2(-vx[0], -vx[1]), nvy = make_float2(-vy[0], -vy[1]);
+                float2 w2s = make_float2(0.f, 0.f), mx2 = w2s, my2 = w2s, xx2 = w2s, xy2 = w2s, yy2 = w2s;
 #pragma unroll 4
-            for (int j = 0; j < cnt; ++j) {
-                T2 p = sxy[j];
+                for (int j = 0; j < cnt; ++j) {
+                    const T2 p = sxy[j];
+                    const float2 dx = __fadd2_rn(make_float2(p.x, p.x), nvx);
+                    const float2 dy = __fadd2_rn(make_float2(p.y, p.y), nvy);
+                    const float2 w = weight2<AM>(__ffma2_rn(dy, dy, __fmul2_rn(dx, dx)), neg_alpha);
+                    const float2 wdx = __fmul2_rn(w, dx), wdy = __fmul2_rn(w, dy);
+                    w2s = __fadd2_rn(w2s, w);
+                    mx2 = __fadd2_rn(mx2, wdx);
+                    my2 = __fadd2_rn(my2, wdy);
+                    xx2 = __ffma2_rn(wdx, dx, xx2);
+                    xy2 = __ffma2_rn(wdx, dy, xy2);
+                    yy2 = __ffma2_rn(wdy, dy, yy2);
+                }
+                tsw[0] += w2s.x; tsw[1] += w2s.y;
+                tmx[0] += mx2.x; tmx[1] += mx2.y;
+                tmy[0] += my2.x; tmy[1] += my2.y;
+                tsxx[0] += xx2.x; tsxx[1] += xx2.y;
+                tsxy[0] += xy2.x; tsxy[1] += xy2.y;
+                tsyy[0] += yy2.x; tsyy[1] += yy2.y;
+            } else {
+#pragma unroll 4
+                for (int j = 0; j < cnt; ++j) {
+                    T2 p = sxy[j];
+#pragma unroll
+                    for (int r = 0; r < R; ++r) {
+                        T dx = p.x - vx[r], dy = p.y - vy[r];
+                        T w = weight<AM>(dx * dx + dy * dy, neg_alpha);
+                        T wdx = w * dx, wdy = w * dy;
+                        sw[r] += w;
+                        mx[r] += wdx;
+                        my[r] += wdy;
+                        sxx[r] += wdx * dx;
+                        sxy_[r] += wdx * dy;
+                        syy[r] += wdy * dy;
+                    }
+                }
 #pragma unroll
                 for (int r = 0; r < R; ++r) {
-                    T dx = p.x - vx[r], dy = p.y - vy[r];
-                    T w = weight<AM>(dx * dx + dy * dy, neg_alpha);
-                    T wdx = w * dx, wdy = w * dy;
-                    sw[r] += w;
-                    mx[r] += wdx;
-                    my[r] += wdy;
-                    sxx[r] += wdx * dx;
-                    sxy_[r] += wdx * dy;
-                    syy[r] += wdy * dy;
+                    run_flush(sw[r], tsw[r]);
+                    run_flush(mx[r], tmx[r]);
+                    run_flush(my[r], tmy[r]);
+                    run_flush(sxx[r], tsxx[r]);
+                    run_flush(sxy_[r], tsxy[r]);
+                    run_flush(syy[r], tsyy[r]);
                 }
-            }
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-                run_flush(sw[r], tsw[r]);
-                run_flush(mx[r], tmx[r]);
-                run_flush(my[r], tmy[r]);
-                run_flush(sxx[r], tsxx[r]);
-                run_flush(sxy_[r], tsxy[r]);
-                run_flush(syy[r], tsyy[r]);
             }
         });
         // per-pixel solve in fp64: c = (A + diag(0, reg, reg))^{-1} e0
@@ -175,25 +205,52 @@ __global__ void __launch_bounds__(NT, MDC_MLS_MINB) mls_kernel(KArgs a) {
                     tacc[r][k] = 0.0;
                 }
             stream_controls(c0ch, true, [&](const T *sq, int cnt) {
+                if constexpr (PK) {
+                    const float2 nvx = make_float2(-vx[0], -vx[1]), nvy = make_float2(-vy[0], -vy[1]);
+                    const float2 c0v = make_float2(c0[0], c0[1]), c1v = make_float2(c1[0], c1[1]),
+                                 c2v = make_float2(c2[0], c2[1]);
+                    float2 acc2[DC];
+#pragma unroll
+                    for (int k = 0; k < DC; ++k) acc2[k] = make_float2(0.f, 0.f);
 #pragma unroll 2
-                for (int j = 0; j < cnt; ++j) {
-                    T2 p = sxy[j];
-                    T qv[DC];
+                    for (int j = 0; j < cnt; ++j) {
+                        const T2 p = sxy[j];
+                        const float2 dx = __fadd2_rn(make_float2(p.x, p.x), nvx);
+                        const float2 dy = __fadd2_rn(make_float2(p.y, p.y), nvy);
+                        const float2 w = weight2<AM>(__ffma2_rn(dy, dy, __fmul2_rn(dx, dx)), neg_alpha);
+                        const float2 g = __fmul2_rn(w, __ffma2_rn(c2v, dy, __ffma2_rn(c1v, dx, c0v)));
 #pragma unroll
-                    for (int k = 0; k < DC; ++k) qv[k] = sq[j * QE + k];
-#pragma unroll
-                    for (int r = 0; r < R; ++r) {
-                        T dx = p.x - vx[r], dy = p.y - vy[r];
-                        T w = weight<AM>(dx * dx + dy * dy, neg_alpha);
-                        T g = w * (c0[r] + c1[r] * dx + c2[r] * dy);
-#pragma unroll
-                        for (int k = 0; k < DC; ++k) acc[r][k] += g * qv[k];
+                        for (int k = 0; k < DC; ++k) {
+                            const float q = sq[j * QE + k];
+                            acc2[k] = __ffma2_rn(g, make_float2(q, q), acc2[k]);
+                        }
                     }
+#pragma unroll
+                    for (int k = 0; k < DC; ++k) {
+                        tacc[0][k] += acc2[k].x;
+                        tacc[1][k] += acc2[k].y;
+                    }
+                } else {
+#pragma unroll 2
+                    for (int j = 0; j < cnt; ++j) {
+                        T2 p = sxy[j];
+                        T qv[DC];
+#pragma unroll
+                        for (int k = 0; k < DC; ++k) qv[k] = sq[j * QE + k];
+#pragma unroll
+                        for (int r = 0; r < R; ++r) {
+                            T dx = p.x - vx[r], dy = p.y - vy[r];
+                            T w = weight<AM>(dx * dx + dy * dy, neg_alpha);
+                            T g = w * (c0[r] + c1[r] * dx + c2[r] * dy);
+#pragma unroll
+                            for (int k = 0; k < DC; ++k) acc[r][k] += g * qv[k];
+                        }
+                    }
+#pragma unroll
+                    for (int r = 0; r < R; ++r)
+#pragma unroll
+                        for (int k = 0; k < DC; ++k) run_flush(acc[r][k], tacc[r][k]);
                 }
-#pragma unroll
-                for (int r = 0; r < R; ++r)
-#pragma unroll
-                    for (int k = 0; k < DC; ++k) run_flush(acc[r][k], tacc[r][k]);
             });
             // epilogue: add back qm, write, bands
 #pragma unroll
@@ -241,26 +298,53 @@ __global__ void __launch_bounds__(NT, MDC_MLS_MINB) mls_kernel(KArgs a) {
                 }
             }
             stream_controls(c0ch, true, [&](const T *sq, int cnt) {
-#pragma unroll 2
-                for (int j = 0; j < cnt; ++j) {
-                    T2 p = sxy[j];
-                    T qv[DC];
+                if constexpr (PK) {
+                    const float2 nvx = make_float2(-vx[0], -vx[1]), nvy = make_float2(-vy[0], -vy[1]);
+                    float2 sw2 = make_float2(0.f, 0.f), acc2[DC];
 #pragma unroll
-                    for (int k = 0; k < DC; ++k) qv[k] = sq[j * QE + k];
+                    for (int k = 0; k < DC; ++k) acc2[k] = sw2;
+#pragma unroll 2
+                    for (int j = 0; j < cnt; ++j) {
+                        const T2 p = sxy[j];
+                        const float2 dx = __fadd2_rn(make_float2(p.x, p.x), nvx);
+                        const float2 dy = __fadd2_rn(make_float2(p.y, p.y), nvy);
+                        const float2 w = weight2<AM>(__ffma2_rn(dy, dy, __fmul2_rn(dx, dx)), neg_alpha);
+                        sw2 = __fadd2_rn(sw2, w);
+#pragma unroll
+                        for (int k = 0; k < DC; ++k) {
+                            const float q = sq[j * QE + k];
+                            acc2[k] = __ffma2_rn(w, make_float2(q, q), acc2[k]);
+                        }
+                    }
+                    tsw[0] += sw2.x;
+                    tsw[1] += sw2.y;
+#pragma unroll
+                    for (int k = 0; k < DC; ++k) {
+                        tacc[0][k] += acc2[k].x;
+                        tacc[1][k] += acc2[k].y;
+                    }
+                } else {
+#pragma unroll 2
+                    for (int j = 0; j < cnt; ++j) {
+                        T2 p = sxy[j];
+                        T qv[DC];
+#pragma unroll
+                        for (int k = 0; k < DC; ++k) qv[k] = sq[j * QE + k];
+#pragma unroll
+                        for (int r = 0; r < R; ++r) {
+                            T dx = p.x - vx[r], dy = p.y - vy[r];
+                            T w = weight<AM>(dx * dx + dy * dy, neg_alpha);
+                            sw[r] += w;
+#pragma unroll
+                            for (int k = 0; k < DC; ++k) acc[r][k] += w * qv[k];
+                        }
+                    }
 #pragma unroll
                     for (int r = 0; r < R; ++r) {
-                        T dx = p.x - vx[r], dy = p.y - vy[r];
-                        T w = weight<AM>(dx * dx + dy * dy, neg_alpha);
-                        sw[r] += w;
+                        run_flush(sw[r], tsw[r]);
 #pragma unroll
-                        for (int k = 0; k < DC; ++k) acc[r][k] += w * qv[k];
+                        for (int k = 0; k < DC; ++k) run_flush(acc[r][k], tacc[r][k]);
                     }
-                }
-#pragma unroll
-                for (int r = 0; r < R; ++r) {
-                    run_flush(sw[r], tsw[r]);
-#pragma unroll
-                    for (int k = 0; k < DC; ++k) run_flush(acc[r][k], tacc[r][k]);
                 }
             });
 #pragma unroll
@@ -301,37 +385,68 @@ __global__ void __launch_bounds__(NT, MDC_MLS_MINB) mls_kernel(KArgs a) {
             for (int i = 0; i < 9; ++i) t_[i][r] = 0.0;
         }
         stream_controls(0, true, [&](const T *sq, int cnt) {
+            if constexpr (PK) {
+                const float2 nvx = make_float2(-vx[0], -vx[1]), nvy = make_float2(-vy[0], -vy[1]);
+                float2 v[9];
+#pragma unroll
+                for (int i = 0; i < 9; ++i) v[i] = make_float2(0.f, 0.f);
 #pragma unroll 2
-            for (int j = 0; j < cnt; ++j) {
-                T2 p = sxy[j];
-                T qx = sq[j * QE + 0], qy = sq[j * QE + 1];
+                for (int j = 0; j < cnt; ++j) {
+                    const T2 p = sxy[j];
+                    const float2 qx = make_float2(sq[j * QE + 0], sq[j * QE + 0]);
+                    const float2 qy = make_float2(sq[j * QE + 1], sq[j * QE + 1]);
+                    const float2 dx = __fadd2_rn(make_float2(p.x, p.x), nvx);
+                    const float2 dy = __fadd2_rn(make_float2(p.y, p.y), nvy);
+                    const float2 w = weight2<AM>(__ffma2_rn(dy, dy, __fmul2_rn(dx, dx)), neg_alpha);
+                    const float2 wdx = __fmul2_rn(w, dx), wdy = __fmul2_rn(w, dy);
+                    v[0] = __fadd2_rn(v[0], w);
+                    v[1] = __fadd2_rn(v[1], wdx);
+                    v[2] = __fadd2_rn(v[2], wdy);
+                    v[3] = __ffma2_rn(w, qx, v[3]);
+                    v[4] = __ffma2_rn(w, qy, v[4]);
+                    v[5] = __ffma2_rn(wdx, qx, v[5]);
+                    v[6] = __ffma2_rn(wdx, qy, v[6]);
+                    v[7] = __ffma2_rn(wdy, qx, v[7]);
+                    v[8] = __ffma2_rn(wdy, qy, v[8]);
+                }
+#pragma unroll
+                for (int i = 0; i < 9; ++i) {
+                    t_[i][0] += v[i].x;
+                    t_[i][1] += v[i].y;
+                }
+            } else {
+#pragma unroll 2
+                for (int j = 0; j < cnt; ++j) {
+                    T2 p = sxy[j];
+                    T qx = sq[j * QE + 0], qy = sq[j * QE + 1];
+#pragma unroll
+                    for (int r = 0; r < R; ++r) {
+                        T dx = p.x - vx[r], dy = p.y - vy[r];
+                        T w = weight<AM>(dx * dx + dy * dy, neg_alpha);
+                        T wdx = w * dx, wdy = w * dy;
+                        sw[r] += w;
+                        mx[r] += wdx;
+                        my[r] += wdy;
+                        bqx[r] += w * qx;
+                        bqy[r] += w * qy;
+                        b00[r] += wdx * qx;
+                        b01[r] += wdx * qy;
+                        b10[r] += wdy * qx;
+                        b11[r] += wdy * qy;
+                    }
+                }
 #pragma unroll
                 for (int r = 0; r < R; ++r) {
-                    T dx = p.x - vx[r], dy = p.y - vy[r];
-                    T w = weight<AM>(dx * dx + dy * dy, neg_alpha);
-                    T wdx = w * dx, wdy = w * dy;
-                    sw[r] += w;
-                    mx[r] += wdx;
-                    my[r] += wdy;
-                    bqx[r] += w * qx;
-                    bqy[r] += w * qy;
-                    b00[r] += wdx * qx;
-                    b01[r] += wdx * qy;
-                    b10[r] += wdy * qx;
-                    b11[r] += wdy * qy;
+                    run_flush(sw[r], t_[0][r]);
+                    run_flush(mx[r], t_[1][r]);
+                    run_flush(my[r], t_[2][r]);
+                    run_flush(bqx[r], t_[3][r]);
+                    run_flush(bqy[r], t_[4][r]);
+                    run_flush(b00[r], t_[5][r]);
+                    run_flush(b01[r], t_[6][r]);
+                    run_flush(b10[r], t_[7][r]);
+                    run_flush(b11[r], t_[8][r]);
                 }
-            }
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-                run_flush(sw[r], t_[0][r]);
-                run_flush(mx[r], t_[1][r]);
-                run_flush(my[r], t_[2][r]);
-                run_flush(bqx[r], t_[3][r]);
-                run_flush(bqy[r], t_[4][r]);
-                run_flush(b00[r], t_[5][r]);
-                run_flush(b01[r], t_[6][r]);
-                run_flush(b10[r], t_[7][r]);
-                run_flush(b11[r], t_[8][r]);
             }
         });
         int cnt_bad = 0;
