@@ -642,8 +642,15 @@ __device__ __forceinline__ bool far_node(const double4 g0, double size, double x
     double gy = g0.y - yi;
     if (gy < 0.0) gy = yi - g0.w;
     if (gy < 0.0) gy = 0.0;
-    double box_dist = __dsqrt_rn(__dadd_rn(__dmul_rn(gx, gx), __dmul_rn(gy, gy)));
-    return size < __dmul_rn(theta, box_dist);
+    const double d2 = __dadd_rn(__dmul_rn(gx, gx), __dmul_rn(gy, gy));
+    // The reference decides size < theta * sqrt(d2) with both roundings.
+    // Squared comparison with a 2^-40 relative guard band settles every case
+    // outside the band identically (rounding moves either side by < 2^-51);
+    // only cases inside the band take the exact IEEE-sqrt path.
+    const double lhs = __dmul_rn(size, size), rhs = __dmul_rn(__dmul_rn(theta, theta), d2);
+    if (lhs < rhs * (1.0 - 0x1p-40)) return true;
+    if (lhs > rhs * (1.0 + 0x1p-40)) return false;
+    return size < __dmul_rn(theta, __dsqrt_rn(d2));
 }
 
 // Accumulates mass * (x_i - com) / (r^3 + eta); the caller scales by c once.
