@@ -426,6 +426,7 @@ struct BuildArgs {
     int max_depth, nnodes;
     int32_t *xs0, *xs1, *ys0, *ys1;
     int32_t *flag, *oflag, *prefix, *blocksum;
+    int l_end = 1 << 30;  // walk levels [0, l_end) only (the rest: build_subtree_kernel)
 };
 
 // Node stats: bbox from the ends of the node's sorted runs (exact min/max),
@@ -444,6 +445,35 @@ __device__ __forceinline__ void stats_for(const BuildArgs &a, int node, const in
     t.size[node] = hypot(ex, ey);
     t.mass[node] = (double)(hi - lo);
     t.axis[node] = ey > ex ? 1 : 0;
+}
+
+// Centroid (ordered sum of the node's leaf sums / count) and the packed node
+// records, warp per node over nodes [gw, nnodes) step nw.
+__device__ __forceinline__ void node_centroids(const BuildArgs &a, int64_t gw, int64_t nw) {
+    const DevTree &t = a.t;
+    const int lane = threadIdx.x & 31;
+    for (int64_t w = gw; w < a.nnodes; w += nw) {
+        int l0 = t.leaf_lo[w], l1 = t.leaf_hi[w];
+        double sx = 0.0, sy = 0.0;
+        for (int k = l0 + lane; k < l1; k += 32) {
+            sx += t.leaf_sum[2 * k];
+            sy += t.leaf_sum[2 * k + 1];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            sx += __shfl_xor_sync(0xffffffffu, sx, o);
+            sy += __shfl_xor_sync(0xffffffffu, sy, o);
+        }
+        if (lane == 0) {
+            double m = (double)(t.hi[w] - t.lo[w]);
+            double cx = sx / m, cy = sy / m;
+            t.com[2 * w] = cx;
+            t.com[2 * w + 1] = cy;
+            t.geo[2 * w] = make_double4(t.bmin[2 * w], t.bmin[2 * w + 1], t.bmax[2 * w], t.bmax[2 * w + 1]);
+            t.geo[2 * w + 1] = make_double4(cx, cy, t.size[w], t.mass[w]);
+            t.topo[w] = make_int4(t.lo[w], t.hi[w], t.left[w], t.right[w]);
+        }
+    }
 }
 
 // The per-level walk (membership = the reference's argpartition under the
@@ -483,6 +513,7 @@ __global__ void __launch_bounds__(NTH) build_levels_kernel(BuildArgs a) {
     const int64_t c_lo = min((int64_t)blockIdx.x * chunk, n), c_hi = min(c_lo + chunk, n);
     int32_t *X = a.xs0, *Y = a.ys0, *Xn = a.xs1, *Yn = a.ys1;
     for (int L = 0; L <= a.max_depth; ++L) {
+        if (L >= a.l_end) return;  // deeper levels and the tail run per subtree
         // ---- phase 1
         const int d0 = t.nd_off[L], dn = t.nd_off[L + 1] - d0;
         for (int64_t e = gtid; e < dn; e += gsz) stats_for(a, t.nd_list[d0 + e], X, Y);
@@ -582,12 +613,123 @@ __global__ void __launch_bounds__(NTH) build_levels_kernel(BuildArgs a) {
         }
     }
     grid.sync();
-    for (int64_t w = gw; w < a.nnodes; w += nw) {
-        int l0 = t.leaf_lo[w], l1 = t.leaf_hi[w];
+    node_centroids(a, gw, nw);
+}
+
+// Deep levels of the large-n walk: once every frontier segment is small,
+// each segment's subtree is independent (its points occupy the same [lo, hi)
+// in both axis runs), so one CTA finishes the walk for one segment with block
+// barriers, its working set L1-resident -- instead of paying a grid-wide
+// barrier and L2 latency per phase for levels with tiny segments.  Same
+// phases, same arithmetic, same ping-pong parity as build_levels_kernel.
+#ifndef MDC_SUBTREE_THREADS
+#define MDC_SUBTREE_THREADS 512
+#endif
+constexpr int SUBTREE_THREADS = MDC_SUBTREE_THREADS;
+#ifndef MDC_SUBTREE_MAX
+#define MDC_SUBTREE_MAX 512
+#endif
+constexpr int SUBTREE_MAX = MDC_SUBTREE_MAX;  // largest segment a CTA takes over (0: off)
+
+__device__ __forceinline__ int first_node_at_or_after(const DevTree &t, int L, int lo) {
+    int a = t.nd_off[L], b = t.nd_off[L + 1];  // nd_list[a, b): depth-L nodes sorted by lo
+    while (a < b) {
+        int m = (a + b) >> 1;
+        if (t.lo[t.nd_list[m]] < lo)
+            a = m + 1;
+        else
+            b = m;
+    }
+    return a;
+}
+
+__global__ void __launch_bounds__(SUBTREE_THREADS) build_subtree_kernel(BuildArgs a, int L0) {
+    typedef cub::BlockScan<int, SUBTREE_THREADS> BS;
+    __shared__ typename BS::TempStorage scan_tmp;
+    __shared__ int s_carry;
+    const DevTree &t = a.t;
+    const int64_t n = a.n;
+    const int tid = threadIdx.x;
+    const int g = t.seg_off[L0] + blockIdx.x;
+    const int seg_lo = t.seg_lo[g], seg_hi = t.seg_hi[g];
+    int32_t *X = (L0 & 1) ? a.xs1 : a.xs0, *Y = (L0 & 1) ? a.ys1 : a.ys0;
+    int32_t *Xn = (L0 & 1) ? a.xs0 : a.xs1, *Yn = (L0 & 1) ? a.ys0 : a.ys1;
+    for (int L = L0; L <= a.max_depth; ++L) {
+        for (int e = first_node_at_or_after(t, L, seg_lo) + tid; e < t.nd_off[L + 1]; e += SUBTREE_THREADS) {
+            const int node = t.nd_list[e];
+            if (t.lo[node] >= seg_hi) break;
+            stats_for(a, node, X, Y);
+        }
+        if (L == a.max_depth) break;
+        for (int k = seg_lo + tid; k < seg_hi; k += SUBTREE_THREADS) {
+            int s = t.seg_of[(int64_t)L * n + k];
+            if (!t.seg_split[s]) continue;
+            int lo = t.seg_lo[s], hi = t.seg_hi[s];
+            double ex = a.pts[2 * X[hi - 1]] - a.pts[2 * X[lo]];
+            double ey = a.pts[2 * Y[hi - 1] + 1] - a.pts[2 * Y[lo] + 1];
+            const int32_t *P = ey > ex ? Y : X;
+            a.flag[P[k]] = (k - lo) < (hi - lo) / 2 ? 1 : 0;
+        }
+        if (tid == 0) s_carry = 0;
+        __syncthreads();
+        // other-run flags and their exclusive prefix over [seg_lo, seg_hi)
+        for (int b0 = seg_lo; b0 < seg_hi; b0 += SUBTREE_THREADS) {
+            const int k = b0 + tid;
+            int v = 0;
+            if (k < seg_hi) {
+                int s = t.seg_of[(int64_t)L * n + k];
+                if (t.seg_split[s]) {
+                    const int32_t *O = t.axis[t.seg_node[s]] ? X : Y;
+                    v = a.flag[O[k]];
+                }
+            }
+            int ex, agg;
+            BS(scan_tmp).ExclusiveSum(v, ex, agg);
+            if (k < seg_hi) a.prefix[k] = s_carry + ex;
+            __syncthreads();
+            if (tid == 0) s_carry += agg;
+            __syncthreads();
+        }
+        for (int k = seg_lo + tid; k < seg_hi; k += SUBTREE_THREADS) {
+            int s = t.seg_of[(int64_t)L * n + k];
+            if (!t.seg_split[s]) {
+                Xn[k] = X[k];
+                Yn[k] = Y[k];
+                continue;
+            }
+            int lo = t.seg_lo[s], hi = t.seg_hi[s];
+            int mid = (hi - lo) / 2;
+            int ax = t.axis[t.seg_node[s]];
+            const int32_t *P = ax ? Y : X;
+            const int32_t *O = ax ? X : Y;
+            int32_t *Pn = ax ? Yn : Xn;
+            int32_t *On = ax ? Xn : Yn;
+            Pn[k] = P[k];
+            int id = O[k];
+            int left_before = a.prefix[k] - a.prefix[lo];
+            int dest = a.flag[id] ? lo + left_before : lo + mid + (k - lo - left_before);
+            On[dest] = id;
+        }
+        __syncthreads();
+        int32_t *tx = X, *ty = Y;
+        X = Xn;
+        Y = Yn;
+        Xn = tx;
+        Yn = ty;
+    }
+    __syncthreads();
+    // leaf sums + gather into leaf order for this subtree's leaves (warp per leaf)
+    const int lane = tid & 31, wid = tid >> 5;
+    const int root = t.seg_node[g];
+    for (int w = t.leaf_lo[root] + wid; w < t.leaf_hi[root]; w += SUBTREE_THREADS / 32) {
+        int node = t.leaves[w];
+        int lo = t.lo[node], hi = t.hi[node];
         double sx = 0.0, sy = 0.0;
-        for (int k = l0 + lane; k < l1; k += 32) {
-            sx += t.leaf_sum[2 * k];
-            sy += t.leaf_sum[2 * k + 1];
+        for (int k = lo + lane; k < hi; k += 32) {
+            double2 p = reinterpret_cast<const double2 *>(a.pts)[X[k]];
+            reinterpret_cast<double2 *>(t.spts)[k] = p;
+            sx += p.x;
+            sy += p.y;
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -595,15 +737,15 @@ __global__ void __launch_bounds__(NTH) build_levels_kernel(BuildArgs a) {
             sy += __shfl_xor_sync(0xffffffffu, sy, o);
         }
         if (lane == 0) {
-            double m = (double)(t.hi[w] - t.lo[w]);
-            double cx = sx / m, cy = sy / m;
-            t.com[2 * w] = cx;
-            t.com[2 * w + 1] = cy;
-            t.geo[2 * w] = make_double4(t.bmin[2 * w], t.bmin[2 * w + 1], t.bmax[2 * w], t.bmax[2 * w + 1]);
-            t.geo[2 * w + 1] = make_double4(cx, cy, t.size[w], t.mass[w]);
-            t.topo[w] = make_int4(t.lo[w], t.hi[w], t.left[w], t.right[w]);
+            t.leaf_sum[2 * w] = sx;
+            t.leaf_sum[2 * w + 1] = sy;
         }
     }
+}
+
+__global__ void centroid_kernel(BuildArgs a) {
+    const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    node_centroids(a, gtid >> 5, ((int64_t)gridDim.x * blockDim.x) >> 5);
 }
 
 // ---------------------------------------------------------------------------
@@ -947,6 +1089,8 @@ struct MdcLayoutPlan {
     int build_blocks = 0;
     // profiling (mdc_layout_profile): events recorded between step phases
     bool cluster_ok = false;  // the device can co-schedule one BUILD_CLUSTER cluster
+    int subtree_l0 = -1;      // grid walk: first level handed to build_subtree_kernel (-1: none)
+    int subtree_nseg = 0;
     cudaEvent_t ev[8] = {};
     int nev = 0;
     bool timing = false;
@@ -1017,9 +1161,15 @@ static int build_tree(MdcLayoutPlan *p, const double *pts, cudaStream_t s, const
         cfg.numAttrs = 1;
         MDC_CHECK_CUDA(cudaLaunchKernelEx(&cfg, build_levels_kernel<BUILD_CLUSTER_THREADS, BUILD_ONE_CLUSTER>, ba));
     } else {
+        if (p->subtree_l0 >= 0) ba.l_end = p->subtree_l0;
         void *kargs[] = {&ba};
         MDC_CHECK_CUDA(cudaLaunchCooperativeKernel((const void *)build_levels_kernel<BUILD_THREADS, BUILD_GRID>,
                                                    dim3(p->build_blocks), dim3(BUILD_THREADS), kargs, 0, s));
+        if (p->subtree_l0 >= 0) {
+            build_subtree_kernel<<<p->subtree_nseg, SUBTREE_THREADS, 0, s>>>(ba, p->subtree_l0);
+            centroid_kernel<<<(unsigned)(((int64_t)ba.nnodes * 32 + 255) / 256), 256, 0, s>>>(ba);
+            MDC_CHECK_LAUNCH();
+        }
     }
     p->mark(s);  // tree levels + centroids done
     int cur = sh.max_depth & 1;
@@ -1168,6 +1318,17 @@ extern "C" int mdc_layout_plan_create(const MdcLayoutArgs *a, MdcLayoutPlan **pl
         int want = (int)((p->shape.n + BUILD_THREADS - 1) / BUILD_THREADS);
         p->build_blocks = std::max(1, std::min(std::max(1, per_sm) * sms, want));
         if (p->build_blocks > 1024) p->build_blocks = 1024;  // blocksum capacity below
+        // first level whose frontier segments all fit one subtree CTA
+        const TreeShape &sh2 = p->shape;
+        for (int L = 0; L < sh2.max_depth && SUBTREE_MAX > 0; ++L) {
+            int mx = 0;
+            for (int g = sh2.seg_off[L]; g < sh2.seg_off[L + 1]; ++g) mx = std::max(mx, sh2.seg_hi[g] - sh2.seg_lo[g]);
+            if (mx <= SUBTREE_MAX) {
+                p->subtree_l0 = L;
+                p->subtree_nseg = sh2.seg_off[L + 1] - sh2.seg_off[L];
+                break;
+            }
+        }
         auto ck = build_levels_kernel<BUILD_CLUSTER_THREADS, BUILD_ONE_CLUSTER>;
         if (BUILD_CLUSTER > 8)
             cudaFuncSetAttribute(ck, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
