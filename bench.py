@@ -303,6 +303,9 @@ def main():
                          "share one GPU for a functional check of the N>1 path; never a bench number)")
     ap.add_argument("--layout-partition", action="store_true",
                     help="vertex-partition the layout over the ranks (default for config 4)")
+    ap.add_argument("--layout-exchange", default="p2p", choices=["p2p", "allreduce"],
+                    help="partitioned layout: step kernel stores into every rank's buffer over NVLink "
+                         "(p2p, cudaIpc) or a SUM all-reduce per iteration")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -343,20 +346,34 @@ def main():
     positions = mesh.original_pos
     partition = world > 1 and (args.layout_partition or args.config == 4)
     if not args.no_layout:
-        eng = L.LayoutEngine(mesh, params, part=(rank, world) if partition else (0, 1))
         temps = L.temperature_schedule(params.initial_temp, params.decay_lambda, cfg["iters"])
+        p2p = partition and args.layout_exchange == "p2p"
+        if p2p:  # the step kernel stores its slice into every rank's buffer
+            run = L.P2PLayout(mesh, params, temps)
+            eng = run.eng
+        else:
+            eng = L.LayoutEngine(mesh, params, part=(rank, world) if partition else (0, 1))
+
+        def reset():
+            if p2p:
+                run.reset(mesh.original_pos)
+            else:
+                eng.set_positions(mesh.original_pos)
 
         def layout_pass(k):
-            if partition:  # one SUM all-reduce of positions per iteration
+            if p2p:
+                for _ in range(k):
+                    run.step()
+            elif partition:  # one SUM all-reduce of positions per iteration
                 for it in range(k):
                     eng.run(temps[it:it + 1])
                     dist.all_reduce(eng.pos, op=dist.ReduceOp.SUM)
             else:
                 eng.run(temps[:k])
 
-        eng.set_positions(mesh.original_pos)
+        reset()
         layout_pass(min(5, cfg["iters"]))  # warm-up + graph capture
-        eng.set_positions(mesh.original_pos)
+        reset()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -366,7 +383,7 @@ def main():
         e1.record()
         e1.synchronize()
         lay_ms = e0.elapsed_time(e1)
-        positions = eng.pos.cpu().numpy()
+        positions = (run.positions() if p2p else eng.pos).cpu().numpy()
         flips = L.count_orientation_flips(mesh, positions)
         t = torch.tensor([lay_ms], device=dev)
         if world > 1:
@@ -376,10 +393,18 @@ def main():
                       "value": units / (t.item() * 1e-3),
                       "ms_total": t.item(), "iterations": cfg["iters"], "points": cfg["n"],
                       "orientation_flips": flips,
-                      "scaling": "strong (vertex-partitioned, SUM all-reduce per iteration)" if partition
+                      "scaling": ("strong (vertex-partitioned, step kernel stores into peer buffers over "
+                                  "NVLink, host barrier per iteration)" if p2p else
+                                  "strong (vertex-partitioned, SUM all-reduce per iteration)") if partition
                       else "replicas only"}
+        if p2p:
+            run.close()
         if rank == 0:
-            layout_res["roofline"] = layout_roofline(eng, params, lib, torch)
+            # rooflines of one whole-mesh step (a partitioned plan covers a slice)
+            peng = L.LayoutEngine(mesh, params) if partition else eng
+            if partition:
+                peng.set_positions(positions)
+            layout_res["roofline"] = layout_roofline(peng, params, lib, torch)
 
     # ---- MLS frame: d dims, row band per rank ---------------------------
     from paper_1408_0677_b200.field import MlsProblem

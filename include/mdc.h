@@ -281,6 +281,28 @@ MDC_API int mdc_layout_steps(MdcLayoutPlan *plan, int32_t k, const double *temps
  * step.  Synchronizes the stream. */
 MDC_API int mdc_layout_profile(MdcLayoutPlan *plan, const double *temps, float *ms_out, int64_t *counts_out,
                                void *stream);
+/* Peer-memory exchange for the vertex partition:
+ * instead of zero-filling the non-owned vertices for a SUM all-reduce, every
+ * rank's step kernel stores its owned vertices' new positions straight into
+ * ALL ranks' next-parity position buffers (NVLink stores into buffers mapped
+ * with mdc_ipc_open).  peers0[r] / peers1[r] = rank r's parity-0 / parity-1
+ * position buffer (n x 2 fp64) as mapped in this process; peers0[rank] must
+ * be the plan's `pos`, peers1[rank] becomes its second buffer; 2 <= world
+ * <= 8 = part_world.  Steps then run with mdc_layout_step_parity, and the
+ * caller orders them across ranks (stream sync + host barrier per step). */
+MDC_API int mdc_layout_set_peers(MdcLayoutPlan *plan, int32_t world, double *const *peers0, double *const *peers1);
+/* One step reading the parity-p buffer (0 = pos, 1 = the second buffer) and
+ * writing the other one; no copy-back.  mdc_layout_reset_counter restarts
+ * the temps index (the step count into `temps`). */
+MDC_API int mdc_layout_step_parity(MdcLayoutPlan *plan, int32_t parity, const double *temps, int32_t use_graph,
+                                   void *stream);
+MDC_API int mdc_layout_reset_counter(MdcLayoutPlan *plan, void *stream);
+/* Inter-process device buffers (cudaIpc): allocate + 64-byte handle, open a
+ * peer's handle in this process, close an opened mapping, free an allocation. */
+MDC_API int mdc_ipc_alloc(size_t bytes, void **ptr, void *handle64);
+MDC_API int mdc_ipc_open(const void *handle64, void **ptr);
+MDC_API int mdc_ipc_close(void *ptr);
+MDC_API int mdc_ipc_free(void *ptr);
 /* Barnes-Hut repulsion alone for positions pts (bhtree.py:69-95). */
 MDC_API int mdc_layout_repulsion(MdcLayoutPlan *plan, const double *pts, double *out, void *stream);
 /* kd-tree of pts: node arrays (count = mdc_layout_node_count) copied out. */

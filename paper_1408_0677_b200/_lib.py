@@ -115,6 +115,13 @@ SIGNATURES = {
                                        _vp, ctypes.c_int32, _vp, _vp, _vp, _vp, _vp, ctypes.c_size_t, _vp]),
     "mdc_copy_2d_async": (ctypes.c_int, [_vp, ctypes.c_size_t, _vp, ctypes.c_size_t, ctypes.c_size_t,
                                          ctypes.c_size_t, _vp]),
+    "mdc_layout_set_peers": (ctypes.c_int, [_vp, ctypes.c_int32, _vp, _vp]),
+    "mdc_layout_step_parity": (ctypes.c_int, [_vp, ctypes.c_int32, _vp, ctypes.c_int32, _vp]),
+    "mdc_layout_reset_counter": (ctypes.c_int, [_vp, _vp]),
+    "mdc_ipc_alloc": (ctypes.c_int, [ctypes.c_size_t, _vp, _vp]),
+    "mdc_ipc_open": (ctypes.c_int, [_vp, _vp]),
+    "mdc_ipc_close": (ctypes.c_int, [_vp]),
+    "mdc_ipc_free": (ctypes.c_int, [_vp]),
     "mdc_layout_profile": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp]),
     "mdc_layout_repulsion": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
     "mdc_layout_node_count": (_c_i64, [_vp]),

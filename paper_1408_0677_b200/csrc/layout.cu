@@ -23,6 +23,7 @@
 #include <cooperative_groups.h>
 #include <cub/cub.cuh>
 #include <algorithm>
+#include <cstring>
 #include <vector>
 
 #include "common.cuh"
@@ -952,6 +953,8 @@ __global__ void bh_combine_kernel(int64_t n, int64_t k0, int64_t k1, DevTree t, 
 // ---------------------------------------------------------------------------
 // Fused per-vertex step.  Written with explicit _rn intrinsics so every
 // operation is one IEEE rounding in the reference's order (numpy never fuses).
+constexpr int MDC_MAX_PEERS = 8;
+
 struct LocalArgs {
     int64_t n;
     const double *pos;
@@ -964,6 +967,10 @@ struct LocalArgs {
     double *dbg_bh, *dbg_force, *dbg_scale;
     const int32_t *perm;  // partitioned step: vertex = perm[k0 + idx]
     int64_t k0, k1;
+    // peer-memory exchange: the new position goes to every rank's
+    // next-parity buffer (NVLink stores) instead of pos_out
+    int npeer;
+    double *peer_out[MDC_MAX_PEERS];
 };
 
 __device__ __forceinline__ double2 ld2(const double *p, int i) {
@@ -1069,8 +1076,13 @@ __global__ void local_kernel(LocalArgs a) {
     }
     double s = smin == INFINITY ? 1.0 : fmin(fmax(smin, 0.0), 1.0);
     if (a.dbg_scale) a.dbg_scale[i] = s;
-    reinterpret_cast<double2 *>(a.pos_out)[i] =
-        make_double2(dadd(pi.x, dmul(s, f.x)), dadd(pi.y, dmul(s, f.y)));
+    const double2 np = make_double2(dadd(pi.x, dmul(s, f.x)), dadd(pi.y, dmul(s, f.y)));
+    if (a.npeer) {
+        for (int r = 0; r < a.npeer; ++r) reinterpret_cast<double2 *>(a.peer_out[r])[i] = np;
+        __threadfence_system();  // visible to the peers once the step is over
+    } else {
+        reinterpret_cast<double2 *>(a.pos_out)[i] = np;
+    }
 }
 
 __global__ void incr_kernel(int32_t *ctr) { ctr[0] += 1; }
@@ -1093,6 +1105,9 @@ struct MdcLayoutPlan {
     int subtree_nseg = 0;
     cudaEvent_t ev[8] = {};
     int nev = 0;
+    // peer-memory exchange (mdc_layout_set_peers)
+    int npeer = 0;
+    double *peers[2][MDC_MAX_PEERS] = {};
     bool timing = false;
     unsigned long long *count = nullptr;  // non-null: instrumented BH launch
     void mark(cudaStream_t s) {
@@ -1241,10 +1256,17 @@ static int enqueue_step(MdcLayoutPlan *p, const double *pin, double *pout, const
     la.perm = nullptr;
     la.k0 = 0;
     la.k1 = n;
+    la.npeer = 0;
     if (p->a.part_world > 1 && perm) {
         part_range(p, la.k0, la.k1);
         la.perm = perm;
-        MDC_CHECK_CUDA(cudaMemsetAsync(pout, 0, sizeof(double) * 2 * (size_t)n, s));
+        if (p->npeer) {
+            const int par_out = pout == p->a.pos ? 0 : 1;  // which parity buffer the step writes
+            la.npeer = p->npeer;
+            for (int r = 0; r < p->npeer; ++r) la.peer_out[r] = p->peers[par_out][r];
+        } else {
+            MDC_CHECK_CUDA(cudaMemsetAsync(pout, 0, sizeof(double) * 2 * (size_t)n, s));
+        }
     }
     if (la.k1 > la.k0) local_kernel<<<(unsigned)((la.k1 - la.k0 + 127) / 128), 128, 0, s>>>(la);
     p->mark(s);  // local forces + update done
@@ -1441,6 +1463,88 @@ extern "C" int mdc_layout_profile(MdcLayoutPlan *p, const double *temps, float *
     MDC_CHECK_CUDA(cudaStreamSynchronize(s));
     MDC_REQUIRE(p->nev == 6, "unexpected phase count");
     for (int i = 0; i < 5; ++i) MDC_CHECK_CUDA(cudaEventElapsedTime(&ms_out[i], p->ev[i], p->ev[i + 1]));
+    return MDC_OK;
+}
+
+extern "C" int mdc_layout_set_peers(MdcLayoutPlan *p, int32_t world, double *const *peers0, double *const *peers1) {
+    MDC_REQUIRE(p && peers0 && peers1, "null pointer");
+    MDC_REQUIRE(world == p->a.part_world && world >= 2 && world <= MDC_MAX_PEERS,
+                "world must equal the plan's part_world (2..8)");
+    MDC_REQUIRE(peers0[p->a.part_rank] == p->a.pos, "peers0[rank] must be this plan's position buffer");
+    for (int r = 0; r < world; ++r) MDC_REQUIRE(peers0[r] && peers1[r], "null peer buffer");
+    for (auto &g : p->graph)
+        if (g) {
+            cudaGraphExecDestroy(g);
+            g = nullptr;
+        }
+    p->npeer = world;
+    for (int r = 0; r < world; ++r) {
+        p->peers[0][r] = peers0[r];
+        p->peers[1][r] = peers1[r];
+    }
+    p->b.pos_b = peers1[p->a.part_rank];  // the second parity buffer is this rank's shared one
+    return MDC_OK;
+}
+
+extern "C" int mdc_layout_step_parity(MdcLayoutPlan *p, int32_t parity, const double *temps, int32_t use_graph,
+                                      void *stream) {
+    MDC_REQUIRE(p && temps && (parity == 0 || parity == 1), "bad arguments");
+    cudaStream_t s = (cudaStream_t)stream;
+    double *bufs[2] = {p->a.pos, p->b.pos_b};
+    if (!use_graph) return enqueue_step(p, bufs[parity], bufs[parity ^ 1], temps, s);
+    if (!p->graph[parity]) {
+        if (!p->cap_stream) MDC_CHECK_CUDA(cudaStreamCreateWithFlags(&p->cap_stream, cudaStreamNonBlocking));
+        MDC_CHECK_CUDA(cudaStreamBeginCapture(p->cap_stream, cudaStreamCaptureModeThreadLocal));
+        int rc = enqueue_step(p, bufs[parity], bufs[parity ^ 1], temps, p->cap_stream);
+        cudaGraph_t g;
+        cudaError_t e = cudaStreamEndCapture(p->cap_stream, &g);
+        if (rc) return rc;
+        MDC_CHECK_CUDA(e);
+        e = cudaGraphInstantiate(&p->graph[parity], g, 0);
+        cudaGraphDestroy(g);
+        MDC_CHECK_CUDA(e);
+        p->graph_temps = temps;
+    }
+    MDC_REQUIRE(p->graph_temps == temps, "temps pointer changed after graph capture");
+    MDC_CHECK_CUDA(cudaGraphLaunch(p->graph[parity], s));
+    return MDC_OK;
+}
+
+extern "C" int mdc_layout_reset_counter(MdcLayoutPlan *p, void *stream) {
+    MDC_REQUIRE(p, "null pointer");
+    MDC_CHECK_CUDA(cudaMemsetAsync(p->b.ctr, 0, sizeof(int32_t), (cudaStream_t)stream));
+    return MDC_OK;
+}
+
+extern "C" int mdc_ipc_alloc(size_t bytes, void **ptr, void *handle) {
+    MDC_REQUIRE(ptr && handle && bytes > 0, "bad arguments");
+    MDC_CHECK_CUDA(cudaMalloc(ptr, bytes));
+    cudaIpcMemHandle_t h;
+    cudaError_t e = cudaIpcGetMemHandle(&h, *ptr);
+    if (e != cudaSuccess) {
+        cudaFree(*ptr);
+        *ptr = nullptr;
+        MDC_CHECK_CUDA(e);
+    }
+    memcpy(handle, &h, sizeof(h));
+    return MDC_OK;
+}
+
+extern "C" int mdc_ipc_open(const void *handle, void **ptr) {
+    MDC_REQUIRE(ptr && handle, "bad arguments");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    MDC_CHECK_CUDA(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    return MDC_OK;
+}
+
+extern "C" int mdc_ipc_close(void *ptr) {
+    MDC_CHECK_CUDA(cudaIpcCloseMemHandle(ptr));
+    return MDC_OK;
+}
+
+extern "C" int mdc_ipc_free(void *ptr) {
+    MDC_CHECK_CUDA(cudaFree(ptr));
     return MDC_OK;
 }
 

@@ -102,7 +102,7 @@ LEAF_SIZE = 32  # bhtree.py:74 passes leaf_size=32 on the layout path
 class LayoutEngine:
     """Device-resident topology + libmdc plan for one mesh and parameter set."""
 
-    def __init__(self, mesh, params: LayoutParams, device=None, leaf: int = LEAF_SIZE, part=(0, 1)):
+    def __init__(self, mesh, params: LayoutParams, device=None, leaf: int = LEAF_SIZE, part=(0, 1), pos=None):
         lib = _lib.require_cuda()
         self.lib = lib
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
@@ -112,7 +112,9 @@ class LayoutEngine:
         dev = self.device
         self.topo = {k: torch.as_tensor(v).to(dev) for k, v in topo.items()}
         self.ntri = int(topo["tris"].shape[0])
-        self.pos = torch.empty((self.n, 2), dtype=torch.float64, device=dev)
+        # `pos` may be an external (n, 2) fp64 device tensor, e.g. an
+        # inter-process buffer for the peer-memory exchange
+        self.pos = torch.empty((self.n, 2), dtype=torch.float64, device=dev) if pos is None else pos
         self.ws = torch.empty(int(lib.mdc_layout_workspace_bytes(self.n, leaf)), dtype=torch.uint8, device=dev)
         self.leaf = leaf
         self.part = (int(part[0]), int(part[1]))
@@ -258,12 +260,58 @@ def layout_debug_step(mesh, pos: np.ndarray, params: LayoutParams, temperature: 
     return eng.pos.cpu().numpy(), bh, force, s
 
 
-def layout_run_partitioned(mesh, params: LayoutParams, group=None) -> LayoutState:
+class IpcBuffer:
+    """A device buffer shareable with other processes (cudaIpc, mdc_ipc_*):
+    ``tensor`` views it in this process, ``handle`` (64 bytes) opens it in a
+    peer process (``IpcBuffer.open``)."""
+
+    def __init__(self, shape, dtype=torch.float64):
+        self.lib = _lib.require_cuda()
+        self.shape, self.dtype = tuple(shape), dtype
+        nbytes = int(np.prod(self.shape)) * torch.empty((), dtype=dtype).element_size()
+        ptr, handle = ctypes.c_void_p(), ctypes.create_string_buffer(64)
+        _lib.check(self.lib.mdc_ipc_alloc(nbytes, ctypes.byref(ptr), handle), "mdc_ipc_alloc")
+        self.ptr, self.handle = ptr.value, handle.raw
+        self.tensor = _wrap_device(self.ptr, self.shape, dtype)
+
+    @staticmethod
+    def open(handle: bytes) -> int:
+        lib = _lib.require_cuda()
+        ptr = ctypes.c_void_p()
+        _lib.check(lib.mdc_ipc_open(ctypes.create_string_buffer(handle, 64), ctypes.byref(ptr)), "mdc_ipc_open")
+        return ptr.value
+
+    @staticmethod
+    def close(ptr: int) -> None:
+        _lib.check(_lib.require_cuda().mdc_ipc_close(ctypes.c_void_p(ptr)), "mdc_ipc_close")
+
+    def free(self) -> None:
+        if self.ptr:
+            self.tensor = None
+            _lib.check(self.lib.mdc_ipc_free(ctypes.c_void_p(self.ptr)), "mdc_ipc_free")
+            self.ptr = None
+
+
+def _wrap_device(ptr: int, shape, dtype) -> torch.Tensor:
+    """A torch view of raw device memory (__cuda_array_interface__, no copy)."""
+    typestr = {torch.float64: "<f8", torch.float32: "<f4", torch.int32: "<i4"}[dtype]
+
+    class _View:
+        __cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (int(ptr), False),
+                                    "version": 3, "strides": None}
+
+    return torch.as_tensor(_View(), device=torch.device("cuda", torch.cuda.current_device()))
+
+
+def layout_run_partitioned(mesh, params: LayoutParams, group=None, exchange: str = "allreduce") -> LayoutState:
     """layout_run with the vertices partitioned over the ranks of ``group``
     (SURVEY.md §8e, config 4): every rank rebuilds the kd-tree from the full
-    snapshot, updates its leaf-order slice of the vertices, and one SUM
-    all-reduce per iteration (non-owned entries are exactly 0.0) reassembles
-    the step -- bit-identical to the single-GPU trajectory."""
+    snapshot and updates its leaf-order slice of the vertices; the slices are
+    reassembled each iteration either by one SUM all-reduce (``allreduce``:
+    non-owned entries are exactly 0.0) or by the step kernel itself storing
+    its slice into every rank's next position buffer over NVLink (``p2p``:
+    cudaIpc-mapped peer buffers, one host barrier per step).  Both are
+    bit-identical to the single-GPU trajectory."""
     import torch.distributed as dist
 
     world = dist.get_world_size(group) if dist.is_initialized() else 1
@@ -271,15 +319,96 @@ def layout_run_partitioned(mesh, params: LayoutParams, group=None) -> LayoutStat
     state = initial_state(mesh, params)
     k = params.iterations
     temps = temperature_schedule(state.temperature, params.decay_lambda, k + 1)
-    eng = LayoutEngine(mesh, params, part=(rank, world))
-    eng.set_positions(mesh.current_pos)
-    for it in range(k):
-        eng.run(temps[it:it + 1], use_graph=True)
-        if world > 1:
-            dist.all_reduce(eng.pos, op=dist.ReduceOp.SUM, group=group)
-    mesh.current_pos = eng.pos.cpu().numpy()
+    if exchange == "p2p" and world > 1:
+        pos = _run_p2p(mesh, params, temps[:k], world, rank, group)
+    else:
+        if exchange not in ("allreduce", "p2p"):
+            raise ValueError(f"exchange must be 'allreduce' or 'p2p', got {exchange!r}")
+        eng = LayoutEngine(mesh, params, part=(rank, world))
+        eng.set_positions(mesh.current_pos)
+        for it in range(k):
+            eng.run(temps[it:it + 1], use_graph=True)
+            if world > 1:
+                dist.all_reduce(eng.pos, op=dist.ReduceOp.SUM, group=group)
+        pos = eng.pos.cpu().numpy()
+    mesh.current_pos = pos
     return LayoutState(mesh=mesh, iteration=k, temperature=float(temps[k]) if k else params.initial_temp,
                        relaxed_pos=mesh.current_pos.copy())
+
+
+class P2PLayout:
+    """Vertex-partitioned layout whose per-iteration exchange is done by the
+    step kernel itself: each rank stores its owned vertices' new positions
+    into every rank's next-parity buffer (cudaIpc-mapped, NVLink stores);
+    one stream sync + host barrier per step orders the ranks."""
+
+    def __init__(self, mesh, params: LayoutParams, temps, group=None):
+        import torch.distributed as dist
+
+        self.dist, self.group = dist, group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        n = int(mesh.node_count)
+        self.bufs = [IpcBuffer((n, 2)), IpcBuffer((n, 2))]
+        handles = [None] * self.world
+        dist.all_gather_object(handles, (self.bufs[0].handle, self.bufs[1].handle), group=group)
+        self.opened = []
+        peers = [[0] * self.world, [0] * self.world]
+        for r in range(self.world):
+            for par in (0, 1):
+                if r == self.rank:
+                    peers[par][r] = self.bufs[par].ptr
+                else:
+                    ptr = IpcBuffer.open(handles[r][par])
+                    self.opened.append(ptr)
+                    peers[par][r] = ptr
+        self.eng = LayoutEngine(mesh, params, part=(self.rank, self.world), pos=self.bufs[0].tensor)
+        self.plan = self.eng.plan()
+        arr0 = (ctypes.c_void_p * self.world)(*peers[0])
+        arr1 = (ctypes.c_void_p * self.world)(*peers[1])
+        _lib.check(self.eng.lib.mdc_layout_set_peers(self.plan, self.world, arr0, arr1), "mdc_layout_set_peers")
+        self.temps = torch.as_tensor(np.asarray(temps, dtype=np.float64)).to(self.eng.device)
+        self.it = 0
+
+    def reset(self, positions) -> None:
+        """Start a trajectory from ``positions`` (every rank passes the same)."""
+        self.eng.set_positions(positions)
+        _lib.check(self.eng.lib.mdc_layout_reset_counter(self.plan, _lib.stream_ptr()), "mdc_layout_reset_counter")
+        self.it = 0
+        torch.cuda.current_stream().synchronize()
+        self.dist.barrier(group=self.group)
+
+    def step(self) -> None:
+        _lib.check(self.eng.lib.mdc_layout_step_parity(self.plan, self.it & 1, _lib.ptr(self.temps), 1,
+                                                       _lib.stream_ptr()), "mdc_layout_step_parity")
+        self.it += 1
+        torch.cuda.current_stream().synchronize()  # this rank's peer stores are done
+        self.dist.barrier(group=self.group)         # ... and every other rank's
+
+    def positions(self) -> torch.Tensor:
+        """The current snapshot (a view of this rank's buffer)."""
+        return self.bufs[self.it & 1].tensor
+
+    def close(self) -> None:
+        self.eng = None
+        self.dist.barrier(group=self.group)  # nobody frees while a peer still maps the buffers
+        for ptr in self.opened:
+            IpcBuffer.close(ptr)
+        self.opened = []
+        torch.cuda.synchronize()
+        for b in self.bufs:
+            b.free()
+
+
+def _run_p2p(mesh, params, temps, world, rank, group):
+    run = P2PLayout(mesh, params, temps, group)
+    try:
+        run.reset(mesh.current_pos)
+        for _ in range(len(temps)):
+            run.step()
+        return run.positions().cpu().numpy()
+    finally:
+        run.close()
 
 
 def interpolate_layout(state: LayoutState, t: float) -> np.ndarray:
