@@ -1125,12 +1125,7 @@ static int build_tree(MdcLayoutPlan *p, const double *pts, cudaStream_t s, const
     if (n <= BSORT_MAX) {
         size_t smem = sizeof(typename cub::BlockRadixSort<unsigned long long, BSORT_THREADS, BSORT_ITEMS,
                                                            int32_t>::TempStorage);
-        static bool attr = false;
-        if (!attr) {
-            MDC_CHECK_CUDA(cudaFuncSetAttribute(block_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                (int)smem));
-            attr = true;
-        }
+        MDC_CHECK_CUDA(ensure_dynamic_smem((const void *)block_sort_kernel, (int)smem));
         block_sort_kernel<<<2, BSORT_THREADS, smem, s>>>(pts, (int)n, b.xs[0], b.ys[0]);
         MDC_CHECK_LAUNCH();
     } else {

@@ -505,11 +505,7 @@ template <typename T, int VAR, int AM, int DC, int R>
 static int launch_t(const KArgs &k, cudaStream_t s) {
     auto fn = mls_kernel<T, VAR, AM, DC, R>;
     size_t smem = smem_bytes<T, DC>();
-    static bool attr_set = false;
-    if (!attr_set) {
-        MDC_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr_set = true;
-    }
+    MDC_CHECK_CUDA(ensure_dynamic_smem((const void *)fn, (int)smem));
     KArgs kk = k;
     const int64_t tile = NT * R;
     kk.tile0 = kk.p_begin / tile;

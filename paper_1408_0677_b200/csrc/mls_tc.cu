@@ -414,11 +414,7 @@ static int launch_tc_nc(const KArgs &k, void *ws, cudaStream_t s) {
                                                                    k.ldq, k.d, NC, nchunk, ntiles, img);
     auto fn = mls_tc_kernel<AM, NC>;
     size_t smem = tc_smem_bytes<NC>();
-    static bool attr = false;
-    if (!attr) {
-        MDC_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
-    }
+    MDC_CHECK_CUDA(ensure_dynamic_smem((const void *)fn, (int)smem));
     KArgs kk = k;
     kk.tile0 = kk.p_begin / TPB;
     int64_t blocks = (kk.p_end + TPB - 1) / TPB - kk.tile0;
