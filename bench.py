@@ -521,7 +521,7 @@ def main():
                 "kernel_share_of_step": kernel_ms / ms_step}
 
     cpu = None
-    if not args.no_cpu:
+    if not args.no_cpu and world == 1:  # the CPU baseline is quoted at N=1 only
         cpu = cpu_mls_sample(positions, raw, cfg, target_s=args.cpu_seconds)
         cpu.pop("seconds", None)
         if layout_res is not None:
