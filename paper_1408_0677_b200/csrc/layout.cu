@@ -195,7 +195,7 @@ static size_t cub_sort_bytes(int64_t n) {
     size_t bytes = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, bytes, (unsigned long long *)nullptr,
                                     (unsigned long long *)nullptr, (int32_t *)nullptr,
-                                    (int32_t *)nullptr, (int)(2 * n), 0, 33);
+                                    (int32_t *)nullptr, (int)(2 * n), 0, 32);
     return bytes;
 }
 
@@ -266,8 +266,9 @@ __device__ __forceinline__ unsigned long long order_key(double x) {
     return (b & 0x8000000000000000ULL) ? ~b : (b | 0x8000000000000000ULL);
 }
 
-// Both axes in ONE radix sort of 2n 33-bit keys {axis bit, order-preserving
-// bits of (float)coord}: 5 digit passes instead of 2 x 8 for fp64 keys.  The
+// Both axes in ONE radix sort of 2n 32-bit keys {axis bit, top 31
+// order-preserving bits of (float)coord}: 4 digit passes instead of 2 x 8
+// for fp64 keys.  The
 // float rounding is monotone, so the result is already ordered by the exact
 // (coord, id) key except inside runs of equal float keys (distinct doubles
 // within one float ulp); those runs are detected and re-sorted by the exact
@@ -284,7 +285,7 @@ __global__ void keys_kernel(const double *pts, int64_t n, unsigned long long *ke
     if (i >= 2 * n) return;
     const int axis = i >= n;
     const int64_t j = i - axis * n;
-    keys[i] = ((unsigned long long)axis << 32) | order_key32(pts[2 * j + axis]);
+    keys[i] = ((unsigned long long)axis << 31) | (order_key32(pts[2 * j + axis]) >> 1);
     ids[i] = (int32_t)j;
 }
 
@@ -300,7 +301,7 @@ __global__ void run_mark_kernel(int64_t n, const unsigned long long *keys, const
                                 int32_t *runflag) {
     int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x + 1;
     if (k >= 2 * n || keys[k] != keys[k - 1]) return;
-    const int axis = (int)(keys[k] >> 32);
+    const int axis = (int)(keys[k] >> 31);
     if (!exact_less(pts, axis, ids[k], ids[k - 1])) return;
     int64_t s0 = k - 1;
     while (s0 > 0 && keys[s0 - 1] == keys[k]) --s0;
@@ -315,7 +316,7 @@ __global__ void run_sort_kernel(int64_t n, const unsigned long long *keys, int32
     if (s0 >= 2 * n || !runflag[s0]) return;
     runflag[s0] = 0;
     const unsigned long long key = keys[s0];
-    const int axis = (int)(key >> 32);
+    const int axis = (int)(key >> 31);
     int64_t e = s0 + 1;
     while (e < 2 * n && keys[e] == key) ++e;
     int32_t *r = ids + s0;
@@ -1134,7 +1135,7 @@ static int build_tree(MdcLayoutPlan *p, const double *pts, cudaStream_t s, const
         MDC_CHECK_LAUNCH();
         size_t bytes = b.cub_bytes;
         MDC_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(b.cub_tmp, bytes, b.kx, b.kx_out, b.ids, b.xs[0],
-                                                       (int)(2 * n), 0, 33, s));
+                                                       (int)(2 * n), 0, 32, s));
         run_mark_kernel<<<nb2, 256, 0, s>>>(n, b.kx_out, b.xs[0], pts, b.runflag);
         run_sort_kernel<<<nb2, 256, 0, s>>>(n, b.kx_out, b.xs[0], pts, b.runflag);
         MDC_CHECK_LAUNCH();
