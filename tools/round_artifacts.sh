@@ -13,4 +13,7 @@ ncu --set full --import-source on --clock-control none -k regex:mls_tc_kernel -s
     python bench.py --steps 1 --warmup 1 --no-cpu --no-e2e --no-layout > gpurun_out/ncu_mls.log 2>&1
 ncu --set full --import-source on --clock-control none -k regex:bh_kernel -s 20 -c 1 -o gpurun_out/bh_full -f \
     python bench.py --steps 1 --warmup 0 --no-cpu --no-e2e --layout-iters 30 > gpurun_out/ncu_bh.log 2>&1
+ncu --set full --import-source on --clock-control none -k regex:mls_kernel -s 1 -c 1 -o gpurun_out/mls_simt_full -f \
+    python bench.py --steps 1 --warmup 1 --no-cpu --no-e2e --no-layout --no-tc --frame 1024x512 > gpurun_out/ncu_simt.log 2>&1
+python -m pytest tests/test_gpu_parity_report.py -q -s -m gpu > gpurun_out/parity.log 2>&1
 ls -la gpurun_out
