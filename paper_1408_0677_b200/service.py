@@ -21,7 +21,6 @@ import threading
 from dataclasses import dataclass, field as dc_field
 from typing import Optional
 
-import numpy as np
 import torch
 from pydantic import BaseModel, Field
 

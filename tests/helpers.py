@@ -1,5 +1,4 @@
 """Shared test helpers: golden meshes as TriMesh objects."""
-import numpy as np
 
 from paper_1408_0677_b200.mesh import TriMesh
 

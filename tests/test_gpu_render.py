@@ -2,10 +2,8 @@
 and the oracle's restatement of render.py's compositing."""
 import numpy as np
 import pytest
-import torch
 
 import oracle as O
-from helpers import golden_mesh
 
 from paper_1408_0677_b200 import field as F
 from paper_1408_0677_b200 import render as R
