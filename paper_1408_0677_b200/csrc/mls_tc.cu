@@ -54,6 +54,7 @@ constexpr int KT = MDC_TC_KT;          // controls per K tile (multiple of 8 = t
 constexpr int STAGES = MDC_TC_STAGES;  // ring depth
 constexpr int FLUSH = MDC_TC_FLUSH;
 constexpr int A_SBO = (KT / 4) * 128;  // bytes between 8-row core-matrix groups of a Q tile
+static_assert(KT % 8 == 0 && XYR % KT == 0, "K tiles are whole tf32 K steps and tile a staging round");
 constexpr int NC_MAX = 32;             // channels per pass-2 chunk (fp64 totals in shared memory)
 
 // ---------------------------------------------------------------------------

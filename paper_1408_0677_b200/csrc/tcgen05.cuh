@@ -92,6 +92,11 @@ __device__ __forceinline__ void tmem_st<16>(uint32_t taddr, const uint32_t (&v)[
         : "memory");
 }
 template <>
+__device__ __forceinline__ void tmem_st<24>(uint32_t taddr, const uint32_t (&v)[24]) {
+    tmem_st<16>(taddr, reinterpret_cast<const uint32_t(&)[16]>(v[0]));
+    tmem_st<8>(taddr + 16, reinterpret_cast<const uint32_t(&)[8]>(v[16]));
+}
+template <>
 __device__ __forceinline__ void tmem_st<32>(uint32_t taddr, const uint32_t (&v)[32]) {
     tmem_st<16>(taddr, reinterpret_cast<const uint32_t(&)[16]>(v[0]));
     tmem_st<16>(taddr + 16, reinterpret_cast<const uint32_t(&)[16]>(v[16]));
