@@ -303,6 +303,13 @@ MDC_API int mdc_ipc_alloc(size_t bytes, void **ptr, void *handle64);
 MDC_API int mdc_ipc_open(const void *handle64, void **ptr);
 MDC_API int mdc_ipc_close(void *ptr);
 MDC_API int mdc_ipc_free(void *ptr);
+/* clamp_factors (layout.py:160-184) for an arbitrary displacement field:
+ * s_out[i] = largest factor in [0, 1] keeping node i eta clear of the three
+ * mid-segment limiting lines of each incident triangle (inc_off/inc as in
+ * MdcLayoutArgs) when it moves by disp[i].  Same operations as the step. */
+MDC_API int mdc_layout_clamp_factors(int64_t n, const double *pos, const double *disp, const int32_t *tris,
+                                     const int32_t *inc_off, const int32_t *inc, double eta, double *s_out,
+                                     void *stream);
 /* Barnes-Hut repulsion alone for positions pts (bhtree.py:69-95). */
 MDC_API int mdc_layout_repulsion(MdcLayoutPlan *plan, const double *pts, double *out, void *stream);
 /* kd-tree of pts: node arrays (count = mdc_layout_node_count) copied out. */

@@ -122,6 +122,8 @@ SIGNATURES = {
     "mdc_ipc_open": (ctypes.c_int, [_vp, _vp]),
     "mdc_ipc_close": (ctypes.c_int, [_vp]),
     "mdc_ipc_free": (ctypes.c_int, [_vp]),
+    "mdc_layout_clamp_factors": (ctypes.c_int, [ctypes.c_int64, _vp, _vp, _vp, _vp, _vp, ctypes.c_double, _vp,
+                                                _vp]),
     "mdc_layout_profile": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp]),
     "mdc_layout_repulsion": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
     "mdc_layout_node_count": (_c_i64, [_vp]),

@@ -978,6 +978,51 @@ __device__ __forceinline__ double2 ld2(const double *p, int i) {
     return reinterpret_cast<const double2 *>(p)[i];
 }
 
+// Per-node clamp factor (layout.py:160-184 clamp_factors, one node): the
+// largest s in [0, 1] keeping the node eta clear of the three mid-segment
+// limiting lines of every incident triangle inc[b0, b1) under displacement f.
+__device__ __forceinline__ double clamp_factor(const double *pos, const int32_t *tris, const int32_t *inc, int b0,
+                                               int b1, double2 pi, double2 f, double eta) {
+    double smin = INFINITY;
+    for (int e = b0; e < b1; ++e) {
+        int tt = inc[e] >> 2;
+        int4 tr = reinterpret_cast<const int4 *>(tris)[tt];
+        double2 A = ld2(pos, tr.x), B = ld2(pos, tr.y), C = ld2(pos, tr.z);
+        double mabx = dmul(0.5, dadd(A.x, B.x)), maby = dmul(0.5, dadd(A.y, B.y));
+        double mbcx = dmul(0.5, dadd(B.x, C.x)), mbcy = dmul(0.5, dadd(B.y, C.y));
+        double mcax = dmul(0.5, dadd(C.x, A.x)), mcay = dmul(0.5, dadd(C.y, A.y));
+        const double ptx[3] = {mabx, mabx, mbcx}, pty[3] = {maby, maby, mbcy};
+        const double drx[3] = {dsub(mcax, mabx), dsub(mbcx, mabx), dsub(mcax, mbcx)};
+        const double dry[3] = {dsub(mcay, maby), dsub(mbcy, maby), dsub(mcay, mbcy)};
+#pragma unroll
+        for (int l = 0; l < 3; ++l) {
+            double nx = -dry[l], ny = drx[l];
+            double ln = hypot(nx, ny);
+            if (ln == 0.0) ln = 1.0;
+            nx = __ddiv_rn(nx, ln);
+            ny = __ddiv_rn(ny, ln);
+            double relx = dsub(pi.x, ptx[l]), rely = dsub(pi.y, pty[l]);
+            double sg = dadd(dmul(relx, nx), dmul(rely, ny));
+            double side = sg >= 0.0 ? 1.0 : -1.0;
+            double dist = fabs(sg);
+            double allowed = fmax(0.0, dsub(dist, eta));
+            double toward = dmul(-side, dadd(dmul(f.x, nx), dmul(f.y, ny)));
+            if (toward > allowed) {
+                double fac = __ddiv_rn(allowed, toward);
+                if (fac < smin) smin = fac;
+            }
+        }
+    }
+    return smin == INFINITY ? 1.0 : fmin(fmax(smin, 0.0), 1.0);
+}
+
+__global__ void clamp_factors_kernel(int64_t n, const double *pos, const double *disp, const int32_t *tris,
+                                     const int32_t *inc_off, const int32_t *inc, double eta, double *s_out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    s_out[i] = clamp_factor(pos, tris, inc, inc_off[i], inc_off[i + 1], ld2(pos, (int)i), ld2(disp, (int)i), eta);
+}
+
 __global__ void local_kernel(LocalArgs a) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (a.perm) {
@@ -1045,37 +1090,7 @@ __global__ void local_kernel(LocalArgs a) {
         f.y = dmul(f.y, k);
     }
     // limiting-line clamp (layout.py:119-184): 3 rows per incident triangle
-    double smin = INFINITY;
-    for (int e = b0; e < b1; ++e) {
-        int tt = a.inc[e] >> 2;
-        int4 tr = reinterpret_cast<const int4 *>(a.tris)[tt];
-        double2 A = ld2(a.pos, tr.x), B = ld2(a.pos, tr.y), C = ld2(a.pos, tr.z);
-        double mabx = dmul(0.5, dadd(A.x, B.x)), maby = dmul(0.5, dadd(A.y, B.y));
-        double mbcx = dmul(0.5, dadd(B.x, C.x)), mbcy = dmul(0.5, dadd(B.y, C.y));
-        double mcax = dmul(0.5, dadd(C.x, A.x)), mcay = dmul(0.5, dadd(C.y, A.y));
-        const double ptx[3] = {mabx, mabx, mbcx}, pty[3] = {maby, maby, mbcy};
-        const double drx[3] = {dsub(mcax, mabx), dsub(mbcx, mabx), dsub(mcax, mbcx)};
-        const double dry[3] = {dsub(mcay, maby), dsub(mbcy, maby), dsub(mcay, mbcy)};
-#pragma unroll
-        for (int l = 0; l < 3; ++l) {
-            double nx = -dry[l], ny = drx[l];
-            double ln = hypot(nx, ny);
-            if (ln == 0.0) ln = 1.0;
-            nx = __ddiv_rn(nx, ln);
-            ny = __ddiv_rn(ny, ln);
-            double relx = dsub(pi.x, ptx[l]), rely = dsub(pi.y, pty[l]);
-            double sg = dadd(dmul(relx, nx), dmul(rely, ny));
-            double side = sg >= 0.0 ? 1.0 : -1.0;
-            double dist = fabs(sg);
-            double allowed = fmax(0.0, dsub(dist, a.eta));
-            double toward = dmul(-side, dadd(dmul(f.x, nx), dmul(f.y, ny)));
-            if (toward > allowed) {
-                double fac = __ddiv_rn(allowed, toward);
-                if (fac < smin) smin = fac;
-            }
-        }
-    }
-    double s = smin == INFINITY ? 1.0 : fmin(fmax(smin, 0.0), 1.0);
+    const double s = clamp_factor(a.pos, a.tris, a.inc, b0, b1, pi, f, a.eta);
     if (a.dbg_scale) a.dbg_scale[i] = s;
     const double2 np = make_double2(dadd(pi.x, dmul(s, f.x)), dadd(pi.y, dmul(s, f.y)));
     if (a.npeer) {
@@ -1541,6 +1556,17 @@ extern "C" int mdc_ipc_close(void *ptr) {
 
 extern "C" int mdc_ipc_free(void *ptr) {
     MDC_CHECK_CUDA(cudaFree(ptr));
+    return MDC_OK;
+}
+
+extern "C" int mdc_layout_clamp_factors(int64_t n, const double *pos, const double *disp, const int32_t *tris,
+                                        const int32_t *inc_off, const int32_t *inc, double eta, double *s_out,
+                                        void *stream) {
+    MDC_REQUIRE(n >= 0 && pos && disp && inc_off && s_out, "null pointer");
+    if (n == 0) return MDC_OK;
+    clamp_factors_kernel<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(n, pos, disp, tris, inc_off,
+                                                                                       inc, eta, s_out);
+    MDC_CHECK_LAUNCH();
     return MDC_OK;
 }
 

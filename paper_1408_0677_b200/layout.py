@@ -411,6 +411,124 @@ def _run_p2p(mesh, params, temps, world, rank, group):
         run.close()
 
 
+# ---- scalar force laws (layout.py:87-116; Eqs. 1-3 of the paper) ----------
+# Per-pair restatements for tests and inspection; the step evaluates the same
+# laws on the GPU (bh_kernel / local_kernel).
+
+def repulsive_force(v, vi, params: LayoutParams) -> np.ndarray:
+    """Softened inverse-square push of v away from vi: C d / (|d|^3 + eta)."""
+    d = np.asarray(v, dtype=float) - np.asarray(vi, dtype=float)
+    r = float(np.hypot(d[0], d[1]))
+    return params.repulsion_c / (r ** 3 + params.softening_eta) * d
+
+
+def spring_force(v, vi, params: LayoutParams) -> np.ndarray:
+    """Log spring along a mesh edge, zero at the desired edge length D."""
+    d = np.asarray(v, dtype=float) - np.asarray(vi, dtype=float)
+    r = float(np.hypot(d[0], d[1]))
+    if r == 0.0:
+        return np.zeros(2)
+    return -params.spring_scale * np.log((r + params.softening_eta) / params.desired_edge_d) * d
+
+
+def node_edge_force(v, vi, vj, params: LayoutParams) -> np.ndarray:
+    """Push of v away from the line through its opposite edge (vi, vj)."""
+    v = np.asarray(v, dtype=float)
+    a = np.asarray(vi, dtype=float)
+    e = np.asarray(vj, dtype=float) - a
+    ee = float(e @ e)
+    if ee == 0.0:
+        return np.zeros(2)
+    r = a + float((v - a) @ e) / ee * e - v  # foot of the perpendicular minus v
+    nr = float(np.hypot(r[0], r[1]))
+    if nr < 1e-12:
+        return np.zeros(2)
+    return -params.repulsion_c / (nr ** 2 + params.softening_eta) * (r / nr)
+
+
+def clamp_displacement(node_idx: int, proposed, mesh, params: LayoutParams) -> np.ndarray:
+    """layout.py:187-213, one node: ``proposed`` scaled so the node crosses no
+    limiting line of an incident triangle (direction kept)."""
+    proposed = np.asarray(proposed, dtype=float)
+    if not proposed.any():
+        return proposed.copy()
+    pos = mesh.current_pos
+    p = pos[node_idx]
+    factor = 1.0
+    for tri in mesh.triangles[np.any(mesh.triangles == node_idx, axis=1)]:
+        a, b, c = pos[tri[0]], pos[tri[1]], pos[tri[2]]
+        mab, mbc, mca = 0.5 * (a + b), 0.5 * (b + c), 0.5 * (c + a)
+        for pt, other in ((mab, mca), (mab, mbc), (mbc, mca)):
+            nrm = np.array([pt[1] - other[1], other[0] - pt[0]])
+            ln = float(np.hypot(nrm[0], nrm[1]))
+            if ln == 0.0:
+                continue
+            nrm = nrm / ln
+            signed = float((p - pt) @ nrm)
+            allowed = max(0.0, abs(signed) - params.softening_eta)
+            toward = -(1.0 if signed >= 0.0 else -1.0) * float(proposed @ nrm)
+            if toward > allowed:
+                factor = min(factor, allowed / toward)
+    return proposed * max(factor, 0.0)
+
+
+def clamp_factors(pos: np.ndarray, disp: np.ndarray, tris: np.ndarray, eta: float, groups=None) -> np.ndarray:
+    """layout.py:160-184 on the GPU (mdc_layout_clamp_factors): per-node factor
+    in [0, 1] keeping every node eta clear of every limiting line of every
+    triangle it belongs to.  ``groups`` (the reference's cached grouping) is
+    accepted and unused."""
+    lib = _lib.require_cuda()
+    pos = np.ascontiguousarray(pos, dtype=np.float64)
+    disp = np.ascontiguousarray(disp, dtype=np.float64)
+    tris = np.asarray(tris, dtype=np.int64).reshape(-1, 3)
+    n = len(pos)
+    if len(tris) == 0:
+        return np.ones(n)
+    corner = np.repeat(np.arange(3, dtype=np.int64)[None, :], len(tris), axis=0).ravel()
+    tri_id = np.repeat(np.arange(len(tris), dtype=np.int64), 3)
+    node = tris.ravel()
+    order = np.argsort(node, kind="stable")
+    inc = ((tri_id << 2) | corner)[order].astype(np.int32)
+    inc_off = np.concatenate([[0], np.cumsum(np.bincount(node, minlength=n))]).astype(np.int32)
+    tris4 = np.zeros((len(tris), 4), dtype=np.int32)
+    tris4[:, :3] = tris
+    dev = torch.device("cuda", torch.cuda.current_device())
+    t = [torch.as_tensor(x).to(dev) for x in (pos, disp, tris4, inc_off, inc)]
+    out = torch.empty(n, dtype=torch.float64, device=dev)
+    _lib.check(lib.mdc_layout_clamp_factors(n, *(_lib.ptr(x) for x in t), float(eta), _lib.ptr(out),
+                                            _lib.stream_ptr()), "mdc_layout_clamp_factors")
+    return out.cpu().numpy()
+
+
+def total_forces(pos: np.ndarray, mesh, params: LayoutParams) -> np.ndarray:
+    """layout.py:259-263 on the GPU: Barnes-Hut + spring + node-edge forces at
+    ``pos`` (the step's force before the temperature cap and the clamp)."""
+    _, _, force, _ = layout_debug_step(mesh, np.asarray(pos, dtype=np.float64), params, params.initial_temp)
+    return force
+
+
+def dump_layout_text(state: LayoutState) -> str:
+    """layout.py:323-329: the mesh dump followed by "layout <iteration>
+    <temperature>" and one "r x y" row per node (floats repr-exact)."""
+    rows = [state.mesh.dump_text().rstrip("\n"), f"layout {state.iteration} {state.temperature!r}"]
+    rows += [f"r {float(x)!r} {float(y)!r}" for x, y in state.relaxed_pos]
+    return "\n".join(rows) + "\n"
+
+
+def parse_layout_text(text: str) -> LayoutState:
+    """layout.py:332-350: inverse of dump_layout_text."""
+    from .mesh import parse_mesh_text
+
+    rows = [r for r in text.splitlines() if r.strip()]
+    k = next(i for i, r in enumerate(rows) if r.startswith("layout "))
+    mesh = parse_mesh_text("\n".join(rows[:k]))
+    _, iteration, temperature = rows[k].split()
+    relaxed = np.array([[float(v) for v in r.split()[1:3]] for r in rows[k + 1:]], dtype=np.float64)
+    if len(relaxed) != mesh.node_count:
+        raise ValueError("relaxed position count does not match the mesh")
+    return LayoutState(mesh=mesh, iteration=int(iteration), temperature=float(temperature), relaxed_pos=relaxed)
+
+
 def interpolate_layout(state: LayoutState, t: float) -> np.ndarray:
     """layout.py:305-309."""
     if not 0.0 <= t <= 1.0:

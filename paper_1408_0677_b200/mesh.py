@@ -91,6 +91,29 @@ class TriMesh:
         return 0.5 * ((b[:, 0] - a[:, 0]) * (c[:, 1] - a[:, 1])
                       - (b[:, 1] - a[:, 1]) * (c[:, 0] - a[:, 0]))
 
+    def fan_entries(self, i: int) -> np.ndarray:
+        """mesh.py:157-158: the fan-stored second vertices of node i's anchored triangles."""
+        return self.fan_nodes[self.fan_offsets[i]: self.fan_offsets[i + 1]]
+
+    def node_triangles(self, i: int) -> list[tuple[int, int, int]]:
+        """mesh.py:160-176: every triangle incident to node i as a CCW triple
+        starting at its smallest vertex (the fan anchor)."""
+        rows = self.triangles[np.any(self.triangles == i, axis=1)]
+        out = []
+        for t in rows:
+            k = int(np.argmin(t))
+            out.append((int(t[k]), int(t[(k + 1) % 3]), int(t[(k + 2) % 3])))
+        return out
+
+    def dump_text(self) -> str:
+        """mesh.py:189-198: line-based debug dump ("mesh n t", one "p ox oy cx cy"
+        row per node, one "t a b c" row per triangle; floats repr-exact)."""
+        rows = [f"mesh {self.node_count} {self.triangle_count}"]
+        rows += [f"p {float(o[0])!r} {float(o[1])!r} {float(c[0])!r} {float(c[1])!r}"
+                 for o, c in zip(self.original_pos, self.current_pos)]
+        rows += [f"t {int(a)} {int(b)} {int(c)}" for a, b, c in self.triangles]
+        return "\n".join(rows) + "\n"
+
     def hull_nodes(self) -> np.ndarray:
         e = np.sort(np.concatenate([self.triangles[:, [0, 1]], self.triangles[:, [1, 2]],
                                     self.triangles[:, [2, 0]]]), axis=1)
@@ -171,6 +194,20 @@ def _jitter_duplicates(points: np.ndarray, diag: float, rng: np.random.Generator
             pts[i, 1] += r * np.sin(ang)
         moved += len(dup)
     return pts, moved
+
+
+def parse_mesh_text(text: str) -> TriMesh:
+    """mesh.py:201-217: inverse of TriMesh.dump_text (the CSR / fan arrays are
+    rebuilt by ``assemble``)."""
+    rows = [r.split() for r in text.splitlines() if r.strip()]
+    if not rows or rows[0][0] != "mesh" or len(rows[0]) != 3:
+        raise MeshError(f"bad mesh dump header: {' '.join(rows[0]) if rows else ''!r}")
+    n, t = int(rows[0][1]), int(rows[0][2])
+    if len(rows) < 1 + n + t:
+        raise MeshError("truncated mesh dump")
+    pts = np.array([[float(v) for v in r[1:5]] for r in rows[1:1 + n]], dtype=np.float64).reshape(n, 4)
+    tris = np.array([[int(v) for v in r[1:4]] for r in rows[1 + n:1 + n + t]], dtype=np.int64).reshape(t, 3)
+    return assemble(pts[:, :2].copy(), pts[:, 2:].copy(), tris, jitter_count=0)
 
 
 def delaunay(points, seed: int = 0, viewport=None) -> TriMesh:
