@@ -178,6 +178,84 @@ _SNAP_WS: dict[int, torch.Tensor] = {}
 _LIN_WS: dict[int, torch.Tensor] = {}
 
 
+class AtControlPoint:
+    """field.py:42-49: sentinel for samples inside a control's snap radius."""
+
+    def __repr__(self):
+        return "AtControlPoint"
+
+
+AT_CONTROL_POINT = AtControlPoint()
+
+
+def mls_weight(v, pi, alpha: float, epsilon_dist: float = 1e-18):
+    """field.py:188-194: |pi - v|^(-2 alpha), or the sentinel inside the snap radius."""
+    d = np.asarray(pi, dtype=float) - np.asarray(v, dtype=float)
+    d2 = float(d @ d)
+    return AT_CONTROL_POINT if d2 < epsilon_dist else d2 ** (-alpha)
+
+
+def _point_mls(kind: str, v, controls_p, controls_q, params: MlsParams) -> np.ndarray:
+    """Single-point MLS (field.py:208-269) evaluated by the GPU seam kernel
+    (mdc_{mean,affine,rigid}_field on one sample); the snap rule first."""
+    lib = _lib.require_cuda()
+    v = np.asarray(v, dtype=np.float64).reshape(2)
+    p = np.asarray(controls_p, dtype=np.float64).reshape(-1, 2)
+    q = np.asarray(controls_q, dtype=np.float64).reshape(-1, 2)
+    eps = params.epsilon_dist if params.epsilon_dist is not None else 1e-18
+    d2 = ((p - v) ** 2).sum(axis=1)
+    hit = int(np.argmin(d2))
+    if d2[hit] < eps:
+        return q[hit].copy()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    qq = q - p if kind == "mean" else q  # the mean kernel takes dq = q - p (_kernels.py:52-67)
+    t = [torch.as_tensor(np.ascontiguousarray(a)).to(dev)
+         for a in (v[:1], v[1:], p[:, 0], p[:, 1], qq[:, 0], qq[:, 1])]
+    out = torch.empty((1, 2), dtype=torch.float64, device=dev)
+    args = [1, *(_lib.ptr(x) for x in t[:2]), len(p), *(_lib.ptr(x) for x in t[2:]), params.resolved_alpha]
+    if kind == "affine":
+        args.append(params.reg_eps)
+    fn = {"mean": lib.mdc_mean_field, "affine": lib.mdc_affine_field, "rigid": lib.mdc_rigid_field}[kind]
+    _lib.check(fn(*args, _lib.ptr(out), _lib.stream_ptr()), f"mdc_{kind}_field")
+    return out[0].cpu().numpy()
+
+
+def mean_mls(v, controls_p, controls_q, params: MlsParams) -> np.ndarray:
+    """field.py:208-218: v + weighted mean of (q - p), on the GPU."""
+    return _point_mls("mean", v, controls_p, controls_q, params)
+
+
+def affine_mls(v, controls_p, controls_q, params: MlsParams) -> np.ndarray:
+    """field.py:221-240: the weighted affine map through the controls at v, on the GPU."""
+    return _point_mls("affine", v, controls_p, controls_q, params)
+
+
+def rigid_mls(v, controls_p, controls_q, params: MlsParams) -> np.ndarray:
+    """field.py:243-269: the weighted rigid map at v, on the GPU.  Where the
+    rotation estimate vanishes the kernel returns the mean-blend fallback of
+    _kernels.rigid_field (_kernels.py:168-171) instead of raising
+    DegenerateRotation."""
+    return _point_mls("rigid", v, controls_p, controls_q, params)
+
+
+def triangle_neighbors(tris: np.ndarray) -> np.ndarray:
+    """field.py:415-428: neighbour triangle across the edge opposite each
+    vertex (-1 on the hull)."""
+    tris = np.asarray(tris, dtype=np.int64).reshape(-1, 3)
+    t = len(tris)
+    edges = np.stack([tris[:, [1, 2]], tris[:, [2, 0]], tris[:, [0, 1]]], axis=1).reshape(-1, 2)
+    edges.sort(axis=1)
+    slot = np.arange(3 * t)
+    order = np.lexsort((slot, edges[:, 1], edges[:, 0]))
+    e = edges[order]
+    same = np.all(e[1:] == e[:-1], axis=1)
+    nbrs = np.full(3 * t, -1, dtype=np.int64)
+    a, b = order[:-1][same], order[1:][same]
+    nbrs[a] = b // 3
+    nbrs[b] = a // 3
+    return nbrs.reshape(t, 3)
+
+
 def hull_edges(tris: np.ndarray) -> np.ndarray:
     """field.py:440-447 `_hull_edges`, vectorised: (u, v, triangle) per
     boundary edge, u < v, in first-appearance order over triangles' edges

@@ -119,3 +119,26 @@ def test_degenerate_affine_controls_raise_like_the_reference():
     with pytest.raises(F.FieldError):
         F.compute_field(mesh, pos, F.TargetAssignment(targets=np.array([[1.0, 0.0]]), mode="dims", dims=("a",)),
                         F.MlsParams("affine"), 8, 8)
+
+
+def test_point_evaluators_closed_form():
+    """test_field.py:52-93: the single-point MLS evaluators (GPU seam kernels)."""
+    params = F.MlsParams(variant="mean")
+    p, q = np.array([[0.5, 0.5]]), np.array([[3.5, -0.5]])
+    for v in np.random.default_rng(1).uniform(-5, 5, (20, 2)):
+        np.testing.assert_allclose(F.mean_mls(v, p, q, params), v + [3.0, -1.0], atol=1e-12)
+    p2, q2 = np.array([[-1.0, 0.0], [1.0, 0.0]]), np.array([[-1.0, 0.0], [1.0, 2.0]])
+    np.testing.assert_allclose(F.mean_mls((0.0, 0.0), p2, q2, F.MlsParams("mean", alpha=1.0)), [0.0, 1.0], atol=1e-12)
+    rng = np.random.default_rng(5)
+    a, b = np.array([[2.0, 0.0], [0.0, 1.0]]), np.array([1.0, 0.0])
+    pa = rng.uniform(-1, 1, (5, 2))
+    for v in rng.uniform(-2, 2, (50, 2)):
+        np.testing.assert_allclose(F.affine_mls(v, pa, pa @ a + b, F.MlsParams("affine")), v @ a + b, atol=1e-6)
+    rot90, t = np.array([[0.0, 1.0], [-1.0, 0.0]]), np.array([1.0, 1.0])
+    pr = np.random.default_rng(6).uniform(-1, 1, (5, 2))
+    for v in np.random.default_rng(7).uniform(-2, 2, (50, 2)):
+        np.testing.assert_allclose(F.rigid_mls(v, pr, pr @ rot90 + t, F.MlsParams("rigid")), v @ rot90 + t, atol=1e-6)
+    # inside the snap radius: the control's own target, exactly
+    assert np.array_equal(F.affine_mls(pa[2], pa, pa @ a + b, F.MlsParams("affine")), (pa @ a + b)[2])
+    assert F.mls_weight((0.0, 0.0), (0.0, 0.0), 1.5) is F.AT_CONTROL_POINT
+    assert F.mls_weight((0.0, 0.0), (2.0, 0.0), 1.0) == 0.25

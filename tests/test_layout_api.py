@@ -107,3 +107,14 @@ def test_total_forces_matches_golden(c1):
         "bh_theta")})
     for k in (0, 25):
         assert normwise(L.total_forces(c1["states"][k], m, params), c1[f"total_{k}"]) <= 1e-13
+
+
+def test_triangle_neighbors_matches_brute_force(c1):
+    from paper_1408_0677_b200 import field as F
+
+    tris = golden_mesh(c1).triangles
+    got = F.triangle_neighbors(tris)
+    for t, (a, b, c) in enumerate(tris):
+        for k, edge in enumerate(({b, c}, {c, a}, {a, b})):
+            others = [u for u in range(len(tris)) if u != t and edge <= set(tris[u].tolist())]
+            assert got[t, k] == (others[0] if others else -1)
