@@ -401,6 +401,10 @@ class MlsProblem:
         if tv_t0.ndim == 1:
             tv_t0 = tv_t0[:, None]
         n, d = tv_t0.shape
+        if n == 0 or d == 0:
+            raise FieldError("MLS needs at least one control point and one target channel")
+        if pos_t0.ndim != 2 or pos_t0.shape[1] != 2:
+            raise ValueError(f"positions must be (n, 2), got {tuple(pos_t0.shape)}")
         if pos_t0.shape[0] != n:
             raise ValueError("positions and targets disagree on the control count")
         if variant == "rigid" and d != 2:

@@ -142,3 +142,14 @@ def test_point_evaluators_closed_form():
     assert np.array_equal(F.affine_mls(pa[2], pa, pa @ a + b, F.MlsParams("affine")), (pa @ a + b)[2])
     assert F.mls_weight((0.0, 0.0), (0.0, 0.0), 1.5) is F.AT_CONTROL_POINT
     assert F.mls_weight((0.0, 0.0), (2.0, 0.0), 1.0) == 0.25
+
+
+def test_empty_and_ragged_inputs_raise_cleanly():
+    with pytest.raises(F.FieldError):
+        F.compute_fields(np.zeros((0, 2)), np.zeros((0, 3)), F.MlsParams("affine"), 8, 8)
+    with pytest.raises(F.FieldError):
+        F.compute_fields(np.zeros((4, 2)), np.zeros((4, 0)), F.MlsParams("affine"), 8, 8)
+    with pytest.raises(ValueError):
+        F.compute_fields(np.zeros((4, 3)), np.zeros((4, 1)), F.MlsParams("affine"), 8, 8)
+    with pytest.raises(ValueError):
+        F.compute_fields(np.random.rand(4, 2), np.zeros((5, 1)), F.MlsParams("affine"), 8, 8)
