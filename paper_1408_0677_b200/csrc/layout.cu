@@ -402,7 +402,7 @@ __global__ void __launch_bounds__(BSORT_THREADS) block_sort_kernel(const double 
 // then leaf sums + leaf-order gather, and centroids.
 namespace cg = cooperative_groups;
 #ifndef MDC_BUILD_THREADS
-#define MDC_BUILD_THREADS 256
+#define MDC_BUILD_THREADS 1024
 #endif
 constexpr int BUILD_THREADS = MDC_BUILD_THREADS;  // cooperative (multi-CTA) walk
 constexpr int BUILD_SINGLE_THREADS = 1024;
