@@ -174,8 +174,16 @@ def field_gradient(fld: CoordinateField, x: int, y: int) -> np.ndarray:
 # GPU evaluation
 
 
-_SNAP_WS: dict[int, torch.Tensor] = {}
-_LIN_WS: dict[int, torch.Tensor] = {}
+# Sentinel-filled scratch, one per (device, stream): kernels restore the
+# sentinel before they finish, so calls on one stream can share it, while
+# calls on different streams (threads) never race on it.
+_SNAP_WS: dict[tuple[int, int], torch.Tensor] = {}
+_LIN_WS: dict[tuple[int, int], torch.Tensor] = {}
+
+
+def _ws_key(device: torch.device) -> tuple[int, int]:
+    idx = device.index if device.index is not None else torch.cuda.current_device()
+    return idx, int(torch.cuda.current_stream(idx).cuda_stream)
 
 
 class AtControlPoint:
@@ -272,7 +280,7 @@ def hull_edges(tris: np.ndarray) -> np.ndarray:
 
 
 def _linear_workspace(nbytes: int, device: torch.device) -> torch.Tensor:
-    key = device.index if device.index is not None else torch.cuda.current_device()
+    key = _ws_key(device)
     ws = _LIN_WS.get(key)
     if ws is None or ws.numel() * 4 < nbytes:
         ws = torch.full((max(nbytes // 4, 1),), 2**31 - 1, dtype=torch.int32, device=device)
@@ -318,8 +326,8 @@ def linear_device(positions, tvals, triangles, width, height, row_range=None, dt
 
 
 def _snap_workspace(nbytes: int, device: torch.device) -> torch.Tensor:
-    """Per-device scratch for mdc_mls_snap, kept all-0xFF between calls."""
-    key = device.index if device.index is not None else torch.cuda.current_device()
+    """Per-(device, stream) scratch for mdc_mls_snap, kept all-0xFF between calls."""
+    key = _ws_key(device)
     ws = _SNAP_WS.get(key)
     if ws is None or ws.numel() < nbytes:
         ws = torch.full((max(nbytes, 1),), 255, dtype=torch.uint8, device=device)
