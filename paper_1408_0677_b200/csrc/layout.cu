@@ -356,42 +356,6 @@ __global__ void run_sort_kernel(int64_t n, const unsigned long long *keys, int32
 }
 
 // ---------------------------------------------------------------------------
-// Small-n sort: one CTA per axis sorts all (key, id) pairs in shared memory
-// (cub::BlockRadixSort, stable -> ties by id), one launch for both axes,
-// instead of 2 x ~10 device-wide radix passes.
-constexpr int BSORT_THREADS = 512;
-constexpr int BSORT_ITEMS = 24;
-constexpr int BSORT_MAX = BSORT_THREADS * BSORT_ITEMS;  // 12288 points
-
-__global__ void __launch_bounds__(BSORT_THREADS) block_sort_kernel(const double *pts, int n, int32_t *xs,
-                                                                   int32_t *ys) {
-    typedef cub::BlockRadixSort<unsigned long long, BSORT_THREADS, BSORT_ITEMS, int32_t> BRS;
-    extern __shared__ __align__(16) unsigned char bsort_smem[];
-    typename BRS::TempStorage &tmp = *reinterpret_cast<typename BRS::TempStorage *>(bsort_smem);
-    const int axis = blockIdx.x;
-    unsigned long long keys[BSORT_ITEMS];
-    int32_t vals[BSORT_ITEMS];
-#pragma unroll
-    for (int e = 0; e < BSORT_ITEMS; ++e) {
-        int i = threadIdx.x * BSORT_ITEMS + e;  // blocked arrangement keeps input (id) order for stability
-        if (i < n) {
-            keys[e] = order_key(pts[2 * i + axis]);
-            vals[e] = i;
-        } else {
-            keys[e] = ~0ULL;  // after every real key (real keys never reach all-ones: NaN excluded)
-            vals[e] = INT32_MAX;
-        }
-    }
-    BRS(tmp).Sort(keys, vals);
-    int32_t *out = axis ? ys : xs;
-#pragma unroll
-    for (int e = 0; e < BSORT_ITEMS; ++e) {
-        int i = threadIdx.x * BSORT_ITEMS + e;
-        if (i < n) out[i] = vals[e];
-    }
-}
-
-// ---------------------------------------------------------------------------
 // The whole level walk as ONE cooperative kernel (grid-wide syncs between
 // phases) instead of ~6 launches per level: per level
 //   phase 1  node stats for this depth; left-flags through each splitting
@@ -1302,23 +1266,18 @@ static int build_tree(MdcLayoutPlan *p, const double *pts, cudaStream_t s, const
     const TreeShape &sh = p->shape;
     Buffers &b = p->b;
     int64_t n = sh.n;
-    if (n <= BSORT_MAX) {
-        size_t smem = sizeof(typename cub::BlockRadixSort<unsigned long long, BSORT_THREADS, BSORT_ITEMS,
-                                                           int32_t>::TempStorage);
-        MDC_CHECK_CUDA(ensure_dynamic_smem((const void *)block_sort_kernel, (int)smem));
-        block_sort_kernel<<<2, BSORT_THREADS, smem, s>>>(pts, (int)n, b.xs[0], b.ys[0]);
-        MDC_CHECK_LAUNCH();
-    } else {
-        const int nb2 = (int)((2 * n + 255) / 256);
-        keys_kernel<<<nb2, 256, 0, s>>>(pts, n, b.kx, b.ids);
-        MDC_CHECK_LAUNCH();
-        size_t bytes = b.cub_bytes;
-        MDC_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(b.cub_tmp, bytes, b.kx, b.kx_out, b.ids, b.xs[0],
-                                                       (int)(2 * n), 0, 32, s));
-        run_mark_kernel<<<nb2, 256, 0, s>>>(n, b.kx_out, b.xs[0], pts, b.runflag);
-        run_sort_kernel<<<nb2, 256, 0, s>>>(n, b.kx_out, b.xs[0], pts, b.runflag);
-        MDC_CHECK_LAUNCH();
-    }
+    // one 32-bit key radix sort for both axes + exact-order fixup of equal-key
+    // runs (a one-CTA 64-bit block sort was tried for small n: 143 us at any n
+    // up to 12k vs ~25 us for this path)
+    const int nb2 = (int)((2 * n + 255) / 256);
+    keys_kernel<<<nb2, 256, 0, s>>>(pts, n, b.kx, b.ids);
+    MDC_CHECK_LAUNCH();
+    size_t bytes = b.cub_bytes;
+    MDC_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(b.cub_tmp, bytes, b.kx, b.kx_out, b.ids, b.xs[0],
+                                                   (int)(2 * n), 0, 32, s));
+    run_mark_kernel<<<nb2, 256, 0, s>>>(n, b.kx_out, b.xs[0], pts, b.runflag);
+    run_sort_kernel<<<nb2, 256, 0, s>>>(n, b.kx_out, b.xs[0], pts, b.runflag);
+    MDC_CHECK_LAUNCH();
     p->mark(s);  // sorts done
     BuildArgs ba;
     ba.pts = pts;
