@@ -182,6 +182,7 @@ struct Buffers {
     unsigned long long *kx, *ky, *kx_out, *ky_out;  // kx|ky and kx_out|ky_out are contiguous (2n keys)
     int32_t *ids, *xs[2], *ys[2];                    // ids: 2n sort values; xs[0]|ys[0] contiguous
     int32_t *runflag;                                // 2n, all-zero between steps
+    int32_t *rank;                                   // 2n, all-zero between steps (small-n rank sort)
     int32_t *flag, *blocksum;
     double *pos_b, *bh;
     int32_t *ctr;
@@ -247,6 +248,7 @@ static size_t carve(Buffers &b, char *base, const TreeShape &s) {
     b.xs[1] = c.take<int32_t>(n);
     b.ys[1] = c.take<int32_t>(n);
     b.runflag = c.take<int32_t>(2 * n);
+    b.rank = c.take<int32_t>(2 * n);
     b.flag = c.take<int32_t>(n);
     b.blocksum = c.take<int32_t>(std::max<int64_t>((n + SCAN_BLOCK - 1) / SCAN_BLOCK + 1, 1024));
     b.pos_b = c.take<double>(2 * n);
@@ -353,6 +355,55 @@ __global__ void run_sort_kernel(int64_t n, const unsigned long long *keys, int32
         r[end] = t;
         sift(0, end);
     }
+}
+
+// Small n: the same 32-bit keys, sorted by counting ranks instead of radix
+// passes -- rank(i) = #{j : (k_j, j) < (k_i, i)}, split as k_j <= k_i over
+// j < i plus k_j < k_i over j > i (the stable sort's tie order).  grid.z
+// splits the j range (partial ranks added atomically: integers, so the
+// result is order-independent), then a scatter writes the sorted keys / ids
+// exactly as the radix sort would, and the same run fixup follows.
+#ifndef MDC_RANK_SORT_MAX
+#define MDC_RANK_SORT_MAX 16384  // O(n^2) work: beats the radix passes only for small n
+#endif
+constexpr int RANK_THREADS = 128;
+constexpr int RANK_TILE = 1024;
+
+__device__ __forceinline__ uint32_t axis_key32(const double *pts, int64_t j, int axis) {
+    return ((uint32_t)axis << 31) | (order_key32(pts[2 * j + axis]) >> 1);
+}
+
+__global__ void __launch_bounds__(RANK_THREADS) rank_count_kernel(const double *pts, int n, int span,
+                                                                  int32_t *rank) {
+    __shared__ uint32_t tile[RANK_TILE];
+    const int axis = blockIdx.y;
+    const int i = blockIdx.x * RANK_THREADS + threadIdx.x;
+    const uint32_t ki = i < n ? axis_key32(pts, i, axis) : 0u;
+    const int j0 = blockIdx.z * span, j1 = min(n, j0 + span);
+    int r = 0;
+    for (int t0 = j0; t0 < j1; t0 += RANK_TILE) {
+        const int cnt = min(RANK_TILE, j1 - t0);
+        __syncthreads();
+        for (int e = threadIdx.x; e < cnt; e += RANK_THREADS) tile[e] = axis_key32(pts, t0 + e, axis);
+        __syncthreads();
+        const int m = min(max(i - t0, 0), cnt);  // tile entries with j < i
+        for (int e = 0; e < m; ++e) r += tile[e] <= ki;
+        for (int e = m; e < cnt; ++e) r += tile[e] < ki;
+    }
+    // the self comparison (j == i) counted 0: k_i < k_i is false
+    if (i < n && r) atomicAdd(rank + (int64_t)axis * n + i, r);
+}
+
+__global__ void rank_scatter_kernel(const double *pts, int64_t n, int32_t *rank, unsigned long long *keys_out,
+                                    int32_t *ids_out) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= 2 * n) return;
+    const int axis = k >= n;
+    const int64_t i = k - axis * n;
+    const int64_t dst = axis * n + rank[k];
+    keys_out[dst] = axis_key32(pts, i, axis);
+    ids_out[dst] = (int32_t)i;
+    rank[k] = 0;  // ready for the next step
 }
 
 // ---------------------------------------------------------------------------
@@ -1243,6 +1294,7 @@ struct MdcLayoutPlan {
     cudaStream_t cap_stream = nullptr;
     const double *graph_temps = nullptr;
     int build_blocks = 0;
+    int sms = 148;
     // profiling (mdc_layout_profile): events recorded between step phases
     bool cluster_ok = false;  // the device can co-schedule one BUILD_CLUSTER cluster
     int subtree_l0 = -1;      // grid walk: first level handed to build_subtree_kernel (-1: none)
@@ -1270,11 +1322,23 @@ static int build_tree(MdcLayoutPlan *p, const double *pts, cudaStream_t s, const
     // runs (a one-CTA 64-bit block sort was tried for small n: 143 us at any n
     // up to 12k vs ~25 us for this path)
     const int nb2 = (int)((2 * n + 255) / 256);
-    keys_kernel<<<nb2, 256, 0, s>>>(pts, n, b.kx, b.ids);
-    MDC_CHECK_LAUNCH();
-    size_t bytes = b.cub_bytes;
-    MDC_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(b.cub_tmp, bytes, b.kx, b.kx_out, b.ids, b.xs[0],
-                                                   (int)(2 * n), 0, 32, s));
+    if (n <= MDC_RANK_SORT_MAX) {
+        // b.rank (2n) is all-zero between steps: the scatter clears it
+        const int bx = (int)((n + RANK_THREADS - 1) / RANK_THREADS);
+        int chunks = (4 * p->sms + 2 * bx - 1) / (2 * bx);
+        chunks = std::max(1, std::min(chunks, (int)((n + RANK_TILE - 1) / RANK_TILE) * 8));
+        const int span = (int)((n + chunks - 1) / chunks);
+        chunks = (int)((n + span - 1) / span);
+        rank_count_kernel<<<dim3(bx, 2, chunks), RANK_THREADS, 0, s>>>(pts, (int)n, span, b.rank);
+        rank_scatter_kernel<<<nb2, 256, 0, s>>>(pts, n, b.rank, b.kx_out, b.xs[0]);
+        MDC_CHECK_LAUNCH();
+    } else {
+        keys_kernel<<<nb2, 256, 0, s>>>(pts, n, b.kx, b.ids);
+        MDC_CHECK_LAUNCH();
+        size_t bytes = b.cub_bytes;
+        MDC_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(b.cub_tmp, bytes, b.kx, b.kx_out, b.ids, b.xs[0],
+                                                       (int)(2 * n), 0, 32, s));
+    }
     run_mark_kernel<<<nb2, 256, 0, s>>>(n, b.kx_out, b.xs[0], pts, b.runflag);
     run_sort_kernel<<<nb2, 256, 0, s>>>(n, b.kx_out, b.xs[0], pts, b.runflag);
     MDC_CHECK_LAUNCH();
@@ -1475,6 +1539,7 @@ extern "C" int mdc_layout_plan_create(const MdcLayoutArgs *a, MdcLayoutPlan **pl
         int dev = 0, sms = 0, per_sm = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms > 0) p->sms = sms;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, build_levels_kernel<BUILD_THREADS, BUILD_GRID>,
                                                       BUILD_THREADS, 0);
         int want = (int)((p->shape.n + BUILD_THREADS - 1) / BUILD_THREADS);
@@ -1509,6 +1574,7 @@ extern "C" int mdc_layout_plan_create(const MdcLayoutArgs *a, MdcLayoutPlan **pl
         cudaGetLastError();  // a refused query leaves the cooperative path in charge
     }
     cudaMemsetAsync(p->b.runflag, 0, sizeof(int32_t) * 2 * (size_t)p->shape.n, s);
+    cudaMemsetAsync(p->b.rank, 0, sizeof(int32_t) * 2 * (size_t)p->shape.n, s);
     // host vectors must outlive the async copies
     cudaError_t e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) {
