@@ -434,6 +434,9 @@ constexpr int BUILD_CLUSTER_THREADS = 1024;
 #define MDC_BUILD_CLUSTER_MAX 16384
 #endif
 constexpr int64_t BUILD_CLUSTER_MAX = MDC_BUILD_CLUSTER_MAX;
+#ifndef MDC_BUILD_CLUSTER_SUB
+#define MDC_BUILD_CLUSTER_SUB 1  // cluster walk only down to the subtree hand-off level
+#endif
 enum BuildMode { BUILD_ONE_CTA = 0, BUILD_ONE_CLUSTER = 1, BUILD_GRID = 2 };
 
 struct BuildArgs {
@@ -640,11 +643,11 @@ __global__ void __launch_bounds__(NTH) build_levels_kernel(BuildArgs a) {
 // barrier and L2 latency per phase for levels with tiny segments.  Same
 // phases, same arithmetic, same ping-pong parity as build_levels_kernel.
 #ifndef MDC_SUBTREE_THREADS
-#define MDC_SUBTREE_THREADS 512
+#define MDC_SUBTREE_THREADS 1024
 #endif
 constexpr int SUBTREE_THREADS = MDC_SUBTREE_THREADS;
 #ifndef MDC_SUBTREE_MAX
-#define MDC_SUBTREE_MAX 512
+#define MDC_SUBTREE_MAX 1024
 #endif
 constexpr int SUBTREE_MAX = MDC_SUBTREE_MAX;  // largest segment a CTA takes over (0: off)
 
@@ -1361,6 +1364,8 @@ static int build_tree(MdcLayoutPlan *p, const double *pts, cudaStream_t s, const
         build_levels_kernel<BUILD_SINGLE_THREADS, BUILD_ONE_CTA><<<1, BUILD_SINGLE_THREADS, 0, s>>>(ba);
         MDC_CHECK_LAUNCH();
     } else if (n <= BUILD_CLUSTER_MAX && p->cluster_ok) {
+        const bool sub = MDC_BUILD_CLUSTER_SUB && p->subtree_l0 >= 0;
+        if (sub) ba.l_end = p->subtree_l0;  // the cluster walks the top levels, one CTA per subtree the rest
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(BUILD_CLUSTER);
         cfg.blockDim = dim3(BUILD_CLUSTER_THREADS);
@@ -1373,6 +1378,11 @@ static int build_tree(MdcLayoutPlan *p, const double *pts, cudaStream_t s, const
         cfg.attrs = attr;
         cfg.numAttrs = 1;
         MDC_CHECK_CUDA(cudaLaunchKernelEx(&cfg, build_levels_kernel<BUILD_CLUSTER_THREADS, BUILD_ONE_CLUSTER>, ba));
+        if (sub) {
+            build_subtree_kernel<<<p->subtree_nseg, SUBTREE_THREADS, 0, s>>>(ba, p->subtree_l0);
+            centroid_kernel<<<(unsigned)(((int64_t)ba.nnodes * 32 + 255) / 256), 256, 0, s>>>(ba);
+            MDC_CHECK_LAUNCH();
+        }
     } else {
         if (p->subtree_l0 >= 0) ba.l_end = p->subtree_l0;
         void *kargs[] = {&ba};

@@ -18,6 +18,7 @@ from __future__ import annotations
 
 import ctypes
 import struct
+import threading
 from dataclasses import dataclass, field as dc_field
 
 import numpy as np
@@ -174,16 +175,30 @@ def field_gradient(fld: CoordinateField, x: int, y: int) -> np.ndarray:
 # GPU evaluation
 
 
-# Sentinel-filled scratch, one per (device, stream): kernels restore the
-# sentinel before they finish, so calls on one stream can share it, while
-# calls on different streams (threads) never race on it.
+# Sentinel-filled scratch, one per (device, stream): the last kernel of a
+# call restores the sentinel, so calls on one stream can share it as long as
+# their launch sequences do not interleave -- each call enqueues under the
+# scratch's lock (several Python threads may share a stream; ctypes releases
+# the GIL during the launches).  Calls on different streams use different
+# scratch and never race.
 _SNAP_WS: dict[tuple[int, int], torch.Tensor] = {}
 _LIN_WS: dict[tuple[int, int], torch.Tensor] = {}
+_WS_LOCKS: dict[tuple[str, int, int], threading.Lock] = {}
+_WS_LOCKS_GUARD = threading.Lock()
 
 
 def _ws_key(device: torch.device) -> tuple[int, int]:
     idx = device.index if device.index is not None else torch.cuda.current_device()
     return idx, int(torch.cuda.current_stream(idx).cuda_stream)
+
+
+def _ws_lock(kind: str, device: torch.device) -> threading.Lock:
+    key = (kind, *_ws_key(device))
+    with _WS_LOCKS_GUARD:
+        lk = _WS_LOCKS.get(key)
+        if lk is None:
+            lk = _WS_LOCKS[key] = threading.Lock()
+    return lk
 
 
 class AtControlPoint:
@@ -311,7 +326,6 @@ def linear_device(positions, tvals, triangles, width, height, row_range=None, dt
         strides = ((r1 - r0) * width, width, 1)
     t_pos, t_tv = _h2d(pos, dev), _h2d(tv, dev)
     t_tris, t_hull = _h2d(tris.astype(np.int32), dev), _h2d(hull.astype(np.int32), dev)
-    ws = _linear_workspace(int(lib.mdc_linear_workspace_bytes(width, r1 - r0)), dev)
     a = _lib.MdcLinearArgs()
     a.width, a.height, a.row0, a.row1 = width, height, r0, r1
     a.x0, a.y1, a.sx, a.sy = tr.x0, tr.y1, sx, sy
@@ -320,8 +334,10 @@ def linear_device(positions, tvals, triangles, width, height, row_range=None, dt
     a.nhull = len(hull)
     a.out = _lib.ptr(out)
     a.out_cs, a.out_rs, a.out_ps = (int(v) for v in strides)
-    a.workspace = _lib.ptr(ws)
-    _lib.check(lib.mdc_linear_field(ctypes.byref(a), _lib.stream_ptr()), "mdc_linear_field")
+    with _ws_lock("linear", dev):
+        ws = _linear_workspace(int(lib.mdc_linear_workspace_bytes(width, r1 - r0)), dev)
+        a.workspace = _lib.ptr(ws)
+        _lib.check(lib.mdc_linear_field(ctypes.byref(a), _lib.stream_ptr()), "mdc_linear_field")
     return out, tr
 
 
@@ -487,10 +503,11 @@ class MlsProblem:
         _lib.check(self.lib.mdc_mls_field(ctypes.byref(a), stream), "mdc_mls_field")
         if snap:
             rows = a.row1 - a.row0
-            ws = _snap_workspace(int(self.lib.mdc_snap_workspace_bytes(self.width, rows)), self.device)
-            _lib.check(self.lib.mdc_mls_snap(ctypes.byref(a), _lib.ptr(self.pos_t), _lib.ptr(self.tvals_t),
-                                             ctypes.c_double(self.eps), _lib.ptr(ws), stream),
-                       "mdc_mls_snap")
+            with _ws_lock("snap", self.device):
+                ws = _snap_workspace(int(self.lib.mdc_snap_workspace_bytes(self.width, rows)), self.device)
+                _lib.check(self.lib.mdc_mls_snap(ctypes.byref(a), _lib.ptr(self.pos_t), _lib.ptr(self.tvals_t),
+                                                 ctypes.c_double(self.eps), _lib.ptr(ws), stream),
+                           "mdc_mls_snap")
 
 
 def compute_fields(positions, targets, params: MlsParams, width: int, height: int,
