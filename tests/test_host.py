@@ -146,3 +146,18 @@ def test_compute_paths_fail_loudly_without_gpu():
         pytest.skip("GPU present")
     with pytest.raises(RuntimeError):
         _lib.require_cuda()
+
+
+
+def test_row_band_plan():
+    """compute_fields_to_host band planning: contiguous cover of the rows, a
+    small tail band last."""
+    from paper_1408_0677_b200.field import plan_row_bands
+
+    for r0, r1, nb in [(0, 2160, 4), (0, 1080, 4), (100, 2000, 3), (0, 37, 4), (0, 2, 8), (0, 1, 4), (5, 6, 4)]:
+        plan = plan_row_bands(r0, r1, nb)
+        assert plan[0][0] == r0 and plan[-1][1] == r1
+        assert all(a[1] == b[0] for a, b in zip(plan, plan[1:])) and all(a < b for a, b in plan)
+        if r1 - r0 >= 2:
+            assert len(plan) == 2 and plan[1][1] - plan[1][0] <= plan[0][1] - plan[0][0]
+    assert plan_row_bands(0, 2160, 4) == [(0, 1890), (1890, 2160)]
