@@ -773,9 +773,6 @@ __global__ void centroid_kernel(BuildArgs a) {
 #ifndef MDC_BH_WARPS
 #define MDC_BH_WARPS 4
 #endif
-#ifndef MDC_BH_SPLIT
-#define MDC_BH_SPLIT 1
-#endif
 constexpr int BH_WARPS = MDC_BH_WARPS;
 constexpr int BH_STACK = 64;
 
@@ -840,6 +837,7 @@ __global__ void __launch_bounds__(BH_WARPS * 32) bh_kernel(int64_t n, int64_t k0
     unsigned long long n_leaf = 0, n_mono = 0, n_test = 0, n_slot = 0;
     __shared__ int s_node[BH_WARPS][BH_STACK];
     __shared__ unsigned s_mask[BH_WARPS][BH_STACK];
+    __shared__ double2 s_leaf[BH_WARPS][32];  // the leaf being summed
     const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int task = blockIdx.y;
     const int64_t k = k0 + ((int64_t)blockIdx.x * BH_WARPS + wib) * 32 + lane;
@@ -883,39 +881,41 @@ __global__ void __launch_bounds__(BH_WARPS * 32) bh_kernel(int64_t n, int64_t k0
             if (COUNT && lane == 0) n_slot += tp.z < 0 ? 32ull * (unsigned long long)(tp.y - tp.x) : 32ull;
             if (tp.z < 0) {
                 // Leaf: pairwise sum over its points (_kernels.py:194-205).  The
-                // self term is exactly +0 (dx = dy = 0; r2 is floored so the
-                // weight stays finite), so no j != i test is needed --
-                // coincident distinct points also contribute 0 in the reference.
-                if (on) {
-                    if (COUNT) n_leaf += (unsigned long long)(tp.y - tp.x);
-                    // + 1e-300 keeps the self term finite (r2 = 0) and is
-                    // absorbed exactly by any r2 > ~1e-284.
-                    auto pair = [&](int q, double &ax, double &ay) {
-                        double2 pj = __ldg(sp2 + q);
-                        double dx = xi - pj.x, dy = yi - pj.y;
-                        double r2 = fma(dx, dx, fma(dy, dy, 1e-300));
-                        double y = rsqrt_nr(r2);
-                        double w = rcp_nr(r2 * (r2 * y) + eta);
-                        ax = fma(w, dx, ax);
-                        ay = fma(w, dy, ay);
-                    };
-#if MDC_BH_SPLIT
-                    // two independent accumulation chains (even / odd q),
-                    // merged per leaf: more fp64 ILP per lane
-                    double gx = 0.0, gy = 0.0;
-                    int q = tp.x;
+                // self term is exactly +0 (dx = dy = 0; + 1e-300 keeps r2 > 0 and
+                // the weight finite, absorbed exactly by any r2 > ~1e-284), so no
+                // j != i test is needed -- coincident distinct points also
+                // contribute 0 in the reference.
+                // The warp stages the leaf's points in shared memory (one
+                // coalesced load per 32 points), then every active lane sums its
+                // pairs from shared broadcasts in point order, in two
+                // accumulation chains (even / odd points) for fp64 ILP.
+                if (COUNT && on) n_leaf += (unsigned long long)(tp.y - tp.x);
+                for (int base = tp.x; base < tp.y; base += 32) {
+                    const int cnt = min(32, tp.y - base);
+                    if (lane < cnt) s_leaf[wib][lane] = __ldg(sp2 + base + lane);
+                    __syncwarp();
+                    if (on) {
+                        auto pair = [&](int q, double &ax, double &ay) {
+                            const double2 pj = s_leaf[wib][q];
+                            double dx = xi - pj.x, dy = yi - pj.y;
+                            double r2 = fma(dx, dx, fma(dy, dy, 1e-300));
+                            double y = rsqrt_nr(r2);
+                            double w = rcp_nr(r2 * (r2 * y) + eta);
+                            ax = fma(w, dx, ax);
+                            ay = fma(w, dy, ay);
+                        };
+                        double gx = 0.0, gy = 0.0;
+                        int q = 0;
 #pragma unroll 4
-                    for (; q + 1 < tp.y; q += 2) {
-                        pair(q, fx, fy);
-                        pair(q + 1, gx, gy);
+                        for (; q + 1 < cnt; q += 2) {
+                            pair(q, fx, fy);
+                            pair(q + 1, gx, gy);
+                        }
+                        if (q < cnt) pair(q, fx, fy);
+                        fx += gx;
+                        fy += gy;
                     }
-                    if (q < tp.y) pair(q, fx, fy);
-                    fx += gx;
-                    fy += gy;
-#else
-#pragma unroll 8
-                    for (int q = tp.x; q < tp.y; ++q) pair(q, fx, fy);
-#endif
+                    __syncwarp();
                 }
                 continue;
             }
