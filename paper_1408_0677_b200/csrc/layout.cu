@@ -878,6 +878,9 @@ __global__ void __launch_bounds__(BH_WARPS * 32) bh_kernel(int64_t n, int64_t k0
             __syncwarp();
             bool on = (mask >> lane) & 1u;
             int4 tp = t.topo[node];
+            // the node's geometry loads issue with its topology: one L1/L2
+            // round trip per visit instead of two (unused for leaves)
+            const double4 g0 = t.geo[2 * node], g1 = t.geo[2 * node + 1];
             if (COUNT && lane == 0) n_slot += tp.z < 0 ? 32ull * (unsigned long long)(tp.y - tp.x) : 32ull;
             if (tp.z < 0) {
                 // Leaf: pairwise sum over its points (_kernels.py:194-205).  The
@@ -921,7 +924,6 @@ __global__ void __launch_bounds__(BH_WARPS * 32) bh_kernel(int64_t n, int64_t k0
             }
             bool open = false;
             if (on) {
-                double4 g0 = t.geo[2 * node], g1 = t.geo[2 * node + 1];
                 if (COUNT) ++n_test;
                 if (far_node(g0, g1.z, xi, yi, theta)) {
                     monopole(g1, xi, yi, eta, fx, fy);
