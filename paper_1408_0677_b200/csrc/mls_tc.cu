@@ -387,10 +387,292 @@ __global__ void __launch_bounds__(THREADS, MDC_TC_MINB) mls_tc_kernel(KArgs a, c
     }
 }
 
+#ifndef MDC_TC_ONEPASS
+#define MDC_TC_ONEPASS 0
+#endif
+#if MDC_TC_ONEPASS
+// One-pass form (A/B experiment, DESIGN.md "Next" item 0).  Pass 2 depends on
+// pass 1 only through c, so F_k = sum_m c_m T_mk with T_m = (w phi_m) . Q,
+// phi = [1, dx, dy]: one sweep accumulates the 6 moments (SIMT) and the three
+// contractions T_0..T_2 (tcgen05, A = {w, w dx, w dy} hi/lo per control); the
+// epilogue solves for c in fp64 and combines the fp64 run totals.
+template <int AM, int NC>
+__global__ void __launch_bounds__(THREADS, 2) mls_tc1_kernel(KArgs a, const float *qimg, int64_t ntiles, int nchunk) {
+    constexpr int B_HALF = NC * KT * 4;
+    constexpr int B_STAGE = 2 * B_HALF;
+    constexpr int ACOL = 3 * NC;  // T_0 | T_1 | T_2
+    constexpr int GST = 6 * KT;   // ring columns per stage: {w, w dx, w dy} x {hi, lo}
+    constexpr int COLS = ACOL + STAGES * GST;
+    constexpr int TMEM_COLS = COLS <= 32 ? 32 : (COLS <= 64 ? 64 : (COLS <= 128 ? 128 : (COLS <= 256 ? 256 : 512)));
+    constexpr int PER = XYR / TPB;
+    extern __shared__ __align__(128) unsigned char smem[];
+    unsigned char *sB = smem;
+    double *tot = reinterpret_cast<double *>(sB + STAGES * B_STAGE);  // 3 NC x TPB
+    float2 *sxy = reinterpret_cast<float2 *>(tot + 3 * NC * TPB);
+    uint64_t *full = reinterpret_cast<uint64_t *>(sxy + 2 * XYR);
+    uint64_t *empty = full + STAGES;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(empty + STAGES);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const bool issuer = warp == CWARPS;
+    const int64_t tile_base = (a.tile0 + blockIdx.x) * (int64_t)TPB;
+    const float neg_alpha = (float)(-a.alpha);
+
+    if (tid == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], CWARPS + 1);
+            mbar_init(&empty[s], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (issuer) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "n"(TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t idesc = idesc_tf32(NC);
+
+    if (issuer) {
+        if (lane == 0) {
+            uint32_t ring = 0;
+            for (int chunk = 0; chunk < nchunk; ++chunk) {
+                for (int64_t t = 0; t < ntiles; ++t, ++ring) {
+                    const int s = ring % STAGES;
+                    mbar_wait_sleep(&full[s], (ring / STAGES) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+                    const uint32_t b_hi = smem_u32(sB + s * B_STAGE), b_lo = b_hi + B_HALF;
+#pragma unroll
+                    for (int kk = 0; kk < KT / 8; ++kk) {
+                        const uint32_t koff = kk * 256;
+                        const uint32_t acc = (t % FLUSH != 0 || kk > 0) ? 1u : 0u;
+                        const uint64_t dbh = umma_desc(b_hi + koff, 128, A_SBO);
+                        const uint64_t dbl = umma_desc(b_lo + koff, 128, A_SBO);
+#pragma unroll
+                        for (int m = 0; m < 3; ++m) {
+                            const uint32_t ta = tmem + ACOL + s * GST + m * 2 * KT + kk * 8;
+                            const uint32_t td = tmem + m * NC;
+                            mma_tf32_ts(td, ta, dbh, idesc, acc);
+                            mma_tf32_ts(td, ta, dbl, idesc, 1u);
+                            mma_tf32_ts(td, ta + KT, dbh, idesc, 1u);
+                        }
+                    }
+                    asm volatile(
+                        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                            smem_u32(&empty[s]))
+                        : "memory");
+                }
+            }
+        }
+        __syncwarp();
+    } else {
+        double ox, oy;
+        {
+            int64_t mid = tile_base + TPB / 2;
+            if (mid >= a.p_total) mid = a.p_total - 1;
+            pixel_xy(a, mid, ox, oy);
+        }
+        int64_t p = tile_base + tid;
+        const bool active = p >= a.p_begin && p < a.p_end;
+        if (!active) p = p < a.p_begin ? a.p_begin : a.p_end - 1;
+        double vxg, vyg;
+        pixel_xy(a, p, vxg, vyg);
+        const float vx = (float)(vxg - ox), vy = (float)(vyg - oy);
+        const int64_t n = a.n;
+        const int64_t nxy = (n + XYR - 1) / XYR;
+        const uint32_t lane_addr = (uint32_t)(warp * 32) << 16;
+        static_assert(PER % 2 == 0, "controls are staged in pairs");
+        double2 pre[PER];
+        auto fetch = [&](int64_t r) {
+#pragma unroll
+            for (int e = 0; e < PER / 2; ++e) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    int64_t j = r * XYR + 2 * (e * TPB + tid) + h;
+                    pre[2 * e + h] = (r < nxy && j < n) ? reinterpret_cast<const double2 *>(a.pc)[j]
+                                                        : make_double2(1e300, 1e300);
+                }
+            }
+        };
+        auto store = [&](int64_t r) {
+            float4 *buf = reinterpret_cast<float4 *>(sxy + (r & 1) * XYR);
+#pragma unroll
+            for (int e = 0; e < PER / 2; ++e) {
+                float x[2], y[2];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const double2 v = pre[2 * e + h];
+                    x[h] = v.x == 1e300 ? 1e18f : (float)(v.x - ox);
+                    y[h] = v.x == 1e300 ? 1e18f : (float)(v.y - oy);
+                }
+                buf[e * TPB + tid] = make_float4(x[0], x[1], y[0], y[1]);
+            }
+        };
+        auto xy_init = [&]() {
+            compute_bar_sync();
+            fetch(0);
+            store(0);
+            fetch(1);
+        };
+        auto xy_step = [&](int64_t r) {
+            compute_bar_sync();
+            if (r + 1 < nxy) store(r + 1);
+            fetch(r + 2);
+        };
+        const float2 nvx = make_float2(-vx, -vx), nvy = make_float2(-vy, -vy);
+        const int64_t row = p / a.width;
+        const int64_t col = p - row * a.width;
+        const int64_t lr = row - a.row0;
+        constexpr int TPR = XYR / KT;
+        auto flush = [&](bool init) {
+            asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+            for (int c8 = 0; c8 < 3 * NC / 8; ++c8) {
+                uint32_t v[8];
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                    : "r"(tmem + lane_addr + c8 * 8));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    double &tt = tot[(c8 * 8 + e) * TPB + tid];
+                    tt = (init ? 0.0 : tt) + (double)__uint_as_float(v[e]);
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;");
+        };
+        bool bad = false;
+        uint32_t ring = 0;
+        for (int chunk = 0; chunk < nchunk; ++chunk) {
+            const char *qchunk = reinterpret_cast<const char *>(qimg) + (size_t)chunk * ntiles * B_STAGE;
+            double tw = 0.0, tmx = 0.0, tmy = 0.0, txx = 0.0, txy = 0.0, tyy = 0.0;
+            float2 sw2 = make_float2(0.f, 0.f), mx2 = sw2, my2 = sw2, sxx2 = sw2, sxy2 = sw2, syy2 = sw2;
+            auto fold = [&]() {  // fp32 run of one staging round -> fp64 totals
+                tw += (double)sw2.x + (double)sw2.y;
+                tmx += (double)mx2.x + (double)mx2.y;
+                tmy += (double)my2.x + (double)my2.y;
+                txx += (double)sxx2.x + (double)sxx2.y;
+                txy += (double)sxy2.x + (double)sxy2.y;
+                tyy += (double)syy2.x + (double)syy2.y;
+                sw2 = make_float2(0.f, 0.f);
+                mx2 = sw2, my2 = sw2, sxx2 = sw2, sxy2 = sw2, syy2 = sw2;
+            };
+            xy_init();
+            for (int64_t t = 0; t < ntiles; ++t, ++ring) {
+                const int tin = (int)(t % TPR);
+                const int64_t round = t / TPR;
+                if (tin == 0) {
+                    if (t > 0) fold();
+                    xy_step(round);
+                }
+                const int s = ring % STAGES;
+                if (ring >= STAGES) mbar_wait(&empty[s], ((ring - STAGES) / STAGES) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                if (tid == 0) {
+                    mbar_arrive_tx(&full[s], B_STAGE);
+                    bulk_g2s(sB + s * B_STAGE, qchunk + (size_t)t * B_STAGE, B_STAGE, &full[s]);
+                }
+                const float4 *buf = reinterpret_cast<const float4 *>(sxy + (round & 1) * XYR + tin * KT);
+                const int64_t jt = t * KT;  // first control of the tile
+                uint32_t ahi[3][KT], alo[3][KT];
+#pragma unroll
+                for (int h = 0; h < KT / 2; ++h) {
+                    const float4 pp = buf[h];
+                    const float2 dx = __fadd2_rn(make_float2(pp.x, pp.y), nvx);
+                    const float2 dy = __fadd2_rn(make_float2(pp.z, pp.w), nvy);
+                    float2 w = weight2<AM>(__ffma2_rn(dy, dy, __fmul2_rn(dx, dx)), neg_alpha);
+                    if (jt + 2 * h + 1 >= n) {  // parked controls (alpha < 1 does not underflow)
+                        if (jt + 2 * h >= n) w.x = 0.f;
+                        w.y = 0.f;
+                    }
+                    const float2 wdx = __fmul2_rn(w, dx), wdy = __fmul2_rn(w, dy);
+                    sw2 = __fadd2_rn(sw2, w);
+                    mx2 = __fadd2_rn(mx2, wdx);
+                    my2 = __fadd2_rn(my2, wdy);
+                    sxx2 = __ffma2_rn(wdx, dx, sxx2);
+                    sxy2 = __ffma2_rn(wdx, dy, sxy2);
+                    syy2 = __ffma2_rn(wdy, dy, syy2);
+                    const float2 av[3] = {w, wdx, wdy};
+#pragma unroll
+                    for (int m = 0; m < 3; ++m) {
+                        const float2 gh =
+                            make_float2(__uint_as_float(tf32_hi_bits(av[m].x)), __uint_as_float(tf32_hi_bits(av[m].y)));
+                        const float2 gl = __ffma2_rn(gh, make_float2(-1.f, -1.f), av[m]);
+                        ahi[m][2 * h] = __float_as_uint(gh.x);
+                        ahi[m][2 * h + 1] = __float_as_uint(gh.y);
+                        alo[m][2 * h] = __float_as_uint(gl.x);
+                        alo[m][2 * h + 1] = __float_as_uint(gl.y);
+                    }
+                }
+                const uint32_t ta = tmem + lane_addr + ACOL + s * GST;
+#pragma unroll
+                for (int m = 0; m < 3; ++m) {
+                    tmem_st<KT>(ta + m * 2 * KT, ahi[m]);
+                    tmem_st<KT>(ta + m * 2 * KT + KT, alo[m]);
+                }
+                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                asm volatile("tcgen05.fence::before_thread_sync;");
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&full[s]);
+                if (t % FLUSH == FLUSH - 1 || t == ntiles - 1) {
+                    mbar_wait(&empty[s], (ring / STAGES) & 1);
+                    flush(t < FLUSH);
+                }
+            }
+            fold();
+            double c0, c1, c2;
+            {
+                double s = tw, m0 = tmx, m1 = tmy;
+                double a00 = txx - m0 * m0 / s;
+                double a01 = txy - m0 * m1 / s;
+                double a11 = tyy - m1 * m1 / s;
+                double reg = a.reg_eps * (a00 + a11);
+                a00 += reg;
+                a11 += reg;
+                double det = a00 * a11 - a01 * a01;
+                double u0 = (a11 * m0 - a01 * m1) / det;
+                double u1 = (a00 * m1 - a01 * m0) / det;
+                c0 = 1.0 / s + (m0 * u0 + m1 * u1) / (s * s);
+                c1 = -u0 / s;
+                c2 = -u1 / s;
+            }
+            if (active) {
+#pragma unroll 4
+                for (int c = 0; c < NC; ++c) {
+                    const int ch = chunk * NC + c;
+                    if (ch < a.d) {
+                        const double F = c0 * tot[c * TPB + tid] + c1 * tot[(NC + c) * TPB + tid] +
+                                         c2 * tot[(2 * NC + c) * TPB + tid];
+                        float f = (float)(F + a.qm[ch]);
+                        reinterpret_cast<float *>(a.out)[ch * a.out_cs + lr * a.out_rs + col * a.out_ps] = f;
+                        if (!isfinite(f)) bad = true;
+                        if (a.bands)
+                            a.bands[ch * a.band_cs + lr * a.band_rs + col] = (int32_t)floor((double)f / a.spacing[ch]);
+                    }
+                }
+            }
+        }
+        if (a.nonfinite && active && bad) atomicAdd(a.nonfinite, 1);
+    }
+    __syncthreads();
+    if (issuer) {
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS));
+    }
+}
+constexpr int TOT_SETS = 3;
+#else
+constexpr int TOT_SETS = 1;
+#endif
+
 template <int NC>
 static size_t tc_smem_bytes() {
-    return STAGES * (size_t)(2 * NC * KT * 4) + (size_t)NC * TPB * sizeof(double) + 2 * XYR * sizeof(float2) +
-           2 * STAGES * sizeof(uint64_t) + 16;
+    return STAGES * (size_t)(2 * NC * KT * 4) + (size_t)TOT_SETS * NC * TPB * sizeof(double) +
+           2 * XYR * sizeof(float2) + 2 * STAGES * sizeof(uint64_t) + 16;
 }
 
 static int pick_nc(int d) { return d <= 16 ? 16 : NC_MAX; }
@@ -413,7 +695,11 @@ static int launch_tc_nc(const KArgs &k, void *ws, cudaStream_t s) {
     int64_t total = (int64_t)nchunk * ntiles * NC * KT;
     q_image_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(reinterpret_cast<const float *>(k.q), k.n,
                                                                    k.ldq, k.d, NC, nchunk, ntiles, img);
+#if MDC_TC_ONEPASS
+    auto fn = mls_tc1_kernel<AM, NC>;
+#else
     auto fn = mls_tc_kernel<AM, NC>;
+#endif
     size_t smem = tc_smem_bytes<NC>();
     MDC_CHECK_CUDA(ensure_dynamic_smem((const void *)fn, (int)smem));
     KArgs kk = k;
