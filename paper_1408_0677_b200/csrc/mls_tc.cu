@@ -47,6 +47,9 @@ constexpr int XYR = MDC_TC_XYR;   // controls per position staging round
 #ifndef MDC_TC_SLEEPC
 #define MDC_TC_SLEEPC 0  // compute warps park (1) or spin (0) on the ring's empty barriers
 #endif
+#ifndef MDC_TC_TRUNC
+#define MDC_TC_TRUNC 1  // pass-2 G split: truncated hi (1, +5 %) or round-to-nearest hi (0)
+#endif
 #ifndef MDC_TC_FLUSH
 #define MDC_TC_FLUSH 32  // K tiles accumulated in TMEM before the fp64 flush (512 controls)
 #endif
@@ -343,7 +346,13 @@ __global__ void __launch_bounds__(THREADS, MDC_TC_MINB) mls_tc_kernel(KArgs a, c
                     const float2 dy = __fadd2_rn(make_float2(pp.z, pp.w), nvy);
                     const float2 w = weight2<AM>(__ffma2_rn(dy, dy, __fmul2_rn(dx, dx)), neg_alpha);
                     const float2 g = __fmul2_rn(w, __ffma2_rn(c2v, dy, __ffma2_rn(c1v, dx, c0v)));
+#if MDC_TC_TRUNC
+                    // truncated hi (one LOP per value): the residual stays exact in fp32
+                    const float2 gh = make_float2(__uint_as_float(__float_as_uint(g.x) & 0xFFFFE000u),
+                                                  __uint_as_float(__float_as_uint(g.y) & 0xFFFFE000u));
+#else
                     const float2 gh = make_float2(__uint_as_float(tf32_hi_bits(g.x)), __uint_as_float(tf32_hi_bits(g.y)));
+#endif
                     const float2 gl = __ffma2_rn(gh, make_float2(-1.f, -1.f), g);  // g - hi, exact
                     ghi[2 * h] = __float_as_uint(gh.x);
                     ghi[2 * h + 1] = __float_as_uint(gh.y);
