@@ -50,12 +50,16 @@ constexpr int XYR = MDC_TC_XYR;   // controls per position staging round
 #ifndef MDC_TC_TRUNC
 #define MDC_TC_TRUNC 1  // pass-2 G split: truncated hi (1, +5 %) or round-to-nearest hi (0)
 #endif
+#ifndef MDC_TC_P1STATIC
+#define MDC_TC_P1STATIC 32  // pass-1 unroll factor for full staging rounds (0: dynamic loop only)
+#endif
 #ifndef MDC_TC_FLUSH
 #define MDC_TC_FLUSH 32  // K tiles accumulated in TMEM before the fp64 flush (512 controls)
 #endif
 constexpr int KT = MDC_TC_KT;          // controls per K tile (multiple of 8 = tcgen05 tf32 K)
 constexpr int STAGES = MDC_TC_STAGES;  // ring depth
 constexpr int FLUSH = MDC_TC_FLUSH;
+constexpr int P1U = MDC_TC_P1STATIC > 0 ? MDC_TC_P1STATIC : 1;
 constexpr int A_SBO = (KT / 4) * 128;  // bytes between 8-row core-matrix groups of a Q tile
 static_assert(KT % 8 == 0 && XYR % KT == 0, "K tiles are whole tf32 K steps and tile a staging round");
 constexpr int NC_MAX = 32;             // channels per pass-2 chunk (fp64 totals in shared memory)
@@ -260,9 +264,17 @@ __global__ void __launch_bounds__(THREADS, MDC_TC_MINB) mls_tc_kernel(KArgs a, c
                 sxy2 = __ffma2_rn(wdx, dy, sxy2);
                 syy2 = __ffma2_rn(wdy, dy, syy2);
             };
+#if MDC_TC_P1STATIC
+            if (cnt == XYR) {  // full round: static trip count
+#pragma unroll (P1U)
+                for (int j2 = 0; j2 < XYR / 2; ++j2) acc(s4[j2], false);
+            } else
+#endif
+            {
 #pragma unroll 4
-            for (int j2 = 0; j2 < (cnt >> 1); ++j2) acc(s4[j2], false);
-            if (cnt & 1) acc(s4[cnt >> 1], true);
+                for (int j2 = 0; j2 < (cnt >> 1); ++j2) acc(s4[j2], false);
+                if (cnt & 1) acc(s4[cnt >> 1], true);
+            }
             tw += (double)sw2.x + (double)sw2.y;
             tmx += (double)mx2.x + (double)mx2.y;
             tmy += (double)my2.x + (double)my2.y;
