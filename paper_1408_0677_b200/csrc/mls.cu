@@ -26,6 +26,10 @@
 
 #include "mls_common.cuh"
 
+#ifndef MDC_SIMT_STATIC
+#define MDC_SIMT_STATIC 1  // full control tiles run static-trip-count loops (same order)
+#endif
+
 namespace mdc {
 
 // fp32 runs: partial sums cover one control tile (NT controls) and are then
@@ -124,8 +128,7 @@ __global__ void __launch_bounds__(NT, MDC_MLS_MINB) mls_kernel(KArgs a) {
             if constexpr (PK) {
                 const float2 nvx = make_float2(-vx[0], -vx[1]), nvy = make_float2(-vy[0], -vy[1]);
                 float2 w2s = make_float2(0.f, 0.f), mx2 = w2s, my2 = w2s, xx2 = w2s, xy2 = w2s, yy2 = w2s;
-#pragma unroll 4
-                for (int j = 0; j < cnt; ++j) {
+                auto mom = [&](int j) {
                     const T2 p = sxy[j];
                     const float2 dx = __fadd2_rn(make_float2(p.x, p.x), nvx);
                     const float2 dy = __fadd2_rn(make_float2(p.y, p.y), nvy);
@@ -137,6 +140,16 @@ __global__ void __launch_bounds__(NT, MDC_MLS_MINB) mls_kernel(KArgs a) {
                     xx2 = __ffma2_rn(wdx, dx, xx2);
                     xy2 = __ffma2_rn(wdx, dy, xy2);
                     yy2 = __ffma2_rn(wdy, dy, yy2);
+                };
+#if MDC_SIMT_STATIC
+                if (cnt == NT) {  // full tile: static trip count (same order)
+#pragma unroll 16
+                    for (int j = 0; j < NT; ++j) mom(j);
+                } else
+#endif
+                {
+#pragma unroll 4
+                    for (int j = 0; j < cnt; ++j) mom(j);
                 }
                 tsw[0] += w2s.x; tsw[1] += w2s.y;
                 tmx[0] += mx2.x; tmx[1] += mx2.y;
@@ -212,8 +225,7 @@ __global__ void __launch_bounds__(NT, MDC_MLS_MINB) mls_kernel(KArgs a) {
                     float2 acc2[DC];
 #pragma unroll
                     for (int k = 0; k < DC; ++k) acc2[k] = make_float2(0.f, 0.f);
-#pragma unroll 2
-                    for (int j = 0; j < cnt; ++j) {
+                    auto rhs = [&](int j) {
                         const T2 p = sxy[j];
                         const float2 dx = __fadd2_rn(make_float2(p.x, p.x), nvx);
                         const float2 dy = __fadd2_rn(make_float2(p.y, p.y), nvy);
@@ -224,6 +236,16 @@ __global__ void __launch_bounds__(NT, MDC_MLS_MINB) mls_kernel(KArgs a) {
                             const float q = sq[j * QE + k];
                             acc2[k] = __ffma2_rn(g, make_float2(q, q), acc2[k]);
                         }
+                    };
+#if MDC_SIMT_STATIC
+                    if (cnt == NT) {
+#pragma unroll 4
+                        for (int j = 0; j < NT; ++j) rhs(j);
+                    } else
+#endif
+                    {
+#pragma unroll 2
+                        for (int j = 0; j < cnt; ++j) rhs(j);
                     }
 #pragma unroll
                     for (int k = 0; k < DC; ++k) {
