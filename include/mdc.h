@@ -107,6 +107,7 @@ typedef struct MdcMlsArgs {
 } MdcMlsArgs;
 
 #define MDC_FLAG_NO_TC 1
+#define MDC_FLAG_TC_ONEPASS 2 /* A/B only: the experimental one-pass tensor-core kernel (mls_tc2.cu) */
 
 MDC_API int mdc_mls_field(const MdcMlsArgs *a, void *stream);
 MDC_API size_t mdc_mls_workspace_bytes(const MdcMlsArgs *a);

@@ -118,6 +118,63 @@ EXPORT void orc_affine_field(int64_t npix, const double *vx, const double *vy, i
     }
 }
 
+/* d-channel form of _kernels.py:70-124 `affine_field`: channel k equals
+ * channel 0 of the reference's call with targets (q[:, k], 0) -- what the
+ * reference CLI renders once per dimension (cli.py:143-165).  The moment sums
+ * shared by all channels are accumulated once; every channel's own sums and
+ * solve follow orc_affine_field's operation order, so each channel is
+ * bit-identical to a separate 2-channel call.  q: (n, d) row-major,
+ * out: (npix, d) row-major. */
+EXPORT void orc_affine_field_d(int64_t npix, const double *vx, const double *vy, int64_t n,
+                               const double *px, const double *py, int64_t d, const double *q,
+                               double alpha, double reg_eps, double *out) {
+#pragma omp parallel
+    {
+        double *mq = (double *)malloc(sizeof(double) * 3 * (size_t)d);
+#pragma omp for schedule(dynamic, 16)
+        for (int64_t i = 0; i < npix; ++i) {
+            double sw = 0, mpx = 0, mpy = 0, mpxpx = 0, mpxpy = 0, mpypy = 0;
+            double *mqx = mq, *mpxqx = mq + d, *mpyqx = mq + 2 * d;
+            for (int64_t k = 0; k < 3 * d; ++k) mq[k] = 0.0;
+            for (int64_t j = 0; j < n; ++j) {
+                double dx = px[j] - vx[i];
+                double dy = py[j] - vy[i];
+                double w = weight(dx * dx + dy * dy, alpha);
+                sw += w;
+                mpx += w * px[j];
+                mpy += w * py[j];
+                mpxpx += w * px[j] * px[j];
+                mpxpy += w * px[j] * py[j];
+                mpypy += w * py[j] * py[j];
+                const double *qj = q + j * d;
+                for (int64_t k = 0; k < d; ++k) {
+                    mqx[k] += w * qj[k];
+                    mpxqx[k] += w * px[j] * qj[k];
+                    mpyqx[k] += w * py[j] * qj[k];
+                }
+            }
+            double psx = mpx / sw, psy = mpy / sw;
+            double a00 = mpxpx - psx * mpx;
+            double a01 = mpxpy - psx * mpy;
+            double a11 = mpypy - psy * mpy;
+            double reg = reg_eps * (a00 + a11);
+            a00 += reg;
+            a11 += reg;
+            double det = a00 * a11 - a01 * a01;
+            double ddx = vx[i] - psx, ddy = vy[i] - psy;
+            for (int64_t k = 0; k < d; ++k) {
+                double qsx = mqx[k] / sw;
+                double b00 = mpxqx[k] - qsx * mpx;
+                double b10 = mpyqx[k] - qsx * mpy;
+                double m00 = (a11 * b00 - a01 * b10) / det;
+                double m10 = (a00 * b10 - a01 * b00) / det;
+                out[i * d + k] = ddx * m00 + ddy * m10 + qsx;
+            }
+        }
+        free(mq);
+    }
+}
+
 /* _kernels.py:127-175 `rigid_field`: similarity -> rotation, mean fallback. */
 EXPORT void orc_rigid_field(int64_t npix, const double *vx, const double *vy, int64_t n,
                             const double *px, const double *py, const double *qx,

@@ -18,6 +18,7 @@ LIB_PATH = os.environ.get("MDC_LIB_PATH") or os.path.join(HERE, "libmdc.so")  # 
 MDC_MEAN, MDC_AFFINE, MDC_RIGID = 1, 2, 3
 MDC_F32, MDC_F64 = 0, 1
 MDC_FLAG_NO_TC = 1
+MDC_FLAG_TC_ONEPASS = 2  # A/B only: the experimental one-pass tensor-core kernel
 VARIANT_CODE = {"mean": MDC_MEAN, "affine": MDC_AFFINE, "rigid": MDC_RIGID}
 
 _c_i32 = ctypes.c_int32

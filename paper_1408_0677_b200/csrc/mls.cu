@@ -652,6 +652,14 @@ __global__ void snap_kernel(SnapArgs a) {
 
 size_t mls_tc_workspace_bytes(int d, int64_t n);
 int launch_mls_tc(const KArgs &k, void *ws, cudaStream_t s);
+size_t mls_tc2_workspace_bytes(int d, int64_t n);
+int launch_mls_tc2(const KArgs &k, void *ws, cudaStream_t s);
+
+// Two-pass kernel (mls_tc.cu) by default; MDC_FLAG_TC_ONEPASS selects the
+// experimental one-pass kernel (mls_tc2.cu) for A/B comparisons.
+static size_t tc_ws_bytes(const MdcMlsArgs *a) {
+    return (a->flags & MDC_FLAG_TC_ONEPASS) ? mls_tc2_workspace_bytes(a->d, a->n) : mls_tc_workspace_bytes(a->d, a->n);
+}
 
 static bool tc_eligible(const MdcMlsArgs *a) {
 #ifndef MDC_TC_MIN_D
@@ -666,7 +674,7 @@ using namespace mdc;
 
 extern "C" size_t mdc_mls_workspace_bytes(const MdcMlsArgs *a) {
     if (!a || !tc_eligible(a)) return 0;
-    return mls_tc_workspace_bytes(a->d, a->n);
+    return tc_ws_bytes(a);
 }
 
 extern "C" int mdc_mls_field(const MdcMlsArgs *a, void *stream) {
@@ -724,9 +732,8 @@ extern "C" int mdc_mls_field(const MdcMlsArgs *a, void *stream) {
     k.nonfinite = a->nonfinite;
     if (k.npix == 0) return MDC_OK;
     cudaStream_t s = (cudaStream_t)stream;
-    if (tc_eligible(a) && a->workspace && a->workspace_bytes >= mls_tc_workspace_bytes(a->d, a->n) &&
-        ((uintptr_t)a->workspace % 16) == 0)
-        return launch_mls_tc(k, a->workspace, s);
+    if (tc_eligible(a) && a->workspace && a->workspace_bytes >= tc_ws_bytes(a) && ((uintptr_t)a->workspace % 16) == 0)
+        return (a->flags & MDC_FLAG_TC_ONEPASS) ? launch_mls_tc2(k, a->workspace, s) : launch_mls_tc(k, a->workspace, s);
     if (a->dtype == MDC_F32) {
         switch (a->variant) {
             case MDC_MEAN: return dispatch_alpha<float, MDC_MEAN>(k, s);
