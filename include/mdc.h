@@ -223,6 +223,13 @@ MDC_API int mdc_affine_field(int64_t npix, const double *vx, const double *vy, i
 MDC_API int mdc_rigid_field(int64_t npix, const double *vx, const double *vy, int64_t n, const double *px,
                             const double *py, const double *qx, const double *qy, double alpha, double *out,
                             void *stream);
+/* mdc_rigid_field plus |f| (the rotation estimate's norm) per pixel in
+ * norm_out (npix, device): the scalar rigid_mls (field.py:243-267) raises
+ * DegenerateRotation where it is < 1e-12 instead of taking the per-pixel
+ * mean fallback of _kernels.rigid_field. */
+MDC_API int mdc_rigid_field_norm(int64_t npix, const double *vx, const double *vy, int64_t n,
+                                 const double *px, const double *py, const double *qx, const double *qy,
+                                 double alpha, double *out, double *norm_out, void *stream);
 MDC_API int mdc_bh_forces(int64_t n, const double *points, const int64_t *perm, const int64_t *lo,
                           const int64_t *hi, const int64_t *left, const int64_t *right, const double *com,
                           const double *mass, const double *size, const double *bmin, const double *bmax,

@@ -139,6 +139,7 @@ SIGNATURES = {
     "mdc_mean_field": (ctypes.c_int, [_c_i64, _vp, _vp, _c_i64, _vp, _vp, _vp, _vp, _c_d, _vp, _vp]),
     "mdc_affine_field": (ctypes.c_int, [_c_i64, _vp, _vp, _c_i64, _vp, _vp, _vp, _vp, _c_d, _c_d, _vp, _vp]),
     "mdc_rigid_field": (ctypes.c_int, [_c_i64, _vp, _vp, _c_i64, _vp, _vp, _vp, _vp, _c_d, _vp, _vp]),
+    "mdc_rigid_field_norm": (ctypes.c_int, [_c_i64, _vp, _vp, _c_i64, _vp, _vp, _vp, _vp, _c_d, _vp, _vp, _vp]),
     "mdc_bh_forces": (ctypes.c_int, [_c_i64] + [_vp] * 11 + [_c_d, _c_d, _c_d, _vp, _vp]),
     "mdc_peak_ffma": (ctypes.c_int, [_vp, _c_i32, _c_i32, _vp]),
     "mdc_peak_dfma": (ctypes.c_int, [_vp, _c_i32, _c_i32, _vp]),

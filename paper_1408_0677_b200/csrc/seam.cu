@@ -30,7 +30,7 @@ template <int VAR>
 __global__ void __launch_bounds__(SEAM_T) seam_mls_kernel(int64_t npix, const double *vx, const double *vy,
                                                          int64_t n, const double *px, const double *py,
                                                          const double *qx, const double *qy, double alpha,
-                                                         double reg_eps, double *out) {
+                                                         double reg_eps, double *out, double *norm_out) {
     __shared__ double4 sc[SEAM_T];
     int64_t i = (int64_t)blockIdx.x * SEAM_T + threadIdx.x;
     bool ok = i < npix;
@@ -94,6 +94,7 @@ __global__ void __launch_bounds__(SEAM_T) seam_mls_kernel(int64_t npix, const do
     double s = b00 + b11, d = b10 - b01;
     double fx = dx * s + dy * d, fy = dy * s - dx * d;
     double norm = hypot(fx, fy);
+    if (norm_out) norm_out[i] = norm;  // field.py:263-265: the scalar evaluator raises on it
     if (norm < 1e-12) {
         out[2 * i] = x + (mqx - mpx) / sw;
         out[2 * i + 1] = y + (mqy - mpy) / sw;
@@ -155,12 +156,12 @@ __global__ void seam_bh_kernel(int64_t n, const double *pts, const int64_t *perm
 template <int VAR>
 static int launch_seam(int64_t npix, const double *vx, const double *vy, int64_t n, const double *px,
                        const double *py, const double *qx, const double *qy, double alpha, double reg_eps,
-                       double *out, void *stream) {
+                       double *out, void *stream, double *norm_out = nullptr) {
     MDC_REQUIRE(npix >= 0 && n >= 1, "need at least one control");
     MDC_REQUIRE(vx && vy && px && py && qx && qy && out, "null device pointer");
     if (npix == 0) return MDC_OK;
     seam_mls_kernel<VAR><<<(unsigned)((npix + SEAM_T - 1) / SEAM_T), SEAM_T, 0, (cudaStream_t)stream>>>(
-        npix, vx, vy, n, px, py, qx, qy, alpha, reg_eps, out);
+        npix, vx, vy, n, px, py, qx, qy, alpha, reg_eps, out, norm_out);
     MDC_CHECK_LAUNCH();
     return MDC_OK;
 }
@@ -183,6 +184,13 @@ extern "C" int mdc_rigid_field(int64_t npix, const double *vx, const double *vy,
                                const double *py, const double *qx, const double *qy, double alpha, double *out,
                                void *stream) {
     return mdc::launch_seam<MDC_RIGID>(npix, vx, vy, n, px, py, qx, qy, alpha, 0.0, out, stream);
+}
+
+extern "C" int mdc_rigid_field_norm(int64_t npix, const double *vx, const double *vy, int64_t n,
+                                    const double *px, const double *py, const double *qx, const double *qy,
+                                    double alpha, double *out, double *norm_out, void *stream) {
+    MDC_REQUIRE(norm_out != nullptr, "null norm_out");
+    return mdc::launch_seam<MDC_RIGID>(npix, vx, vy, n, px, py, qx, qy, alpha, 0.0, out, stream, norm_out);
 }
 
 extern "C" int mdc_bh_forces(int64_t n, const double *points, const int64_t *perm, const int64_t *lo,

@@ -238,7 +238,14 @@ def _point_mls(kind: str, v, controls_p, controls_q, params: MlsParams) -> np.nd
     args = [1, *(_lib.ptr(x) for x in t[:2]), len(p), *(_lib.ptr(x) for x in t[2:]), params.resolved_alpha]
     if kind == "affine":
         args.append(params.reg_eps)
-    fn = {"mean": lib.mdc_mean_field, "affine": lib.mdc_affine_field, "rigid": lib.mdc_rigid_field}[kind]
+    if kind == "rigid":
+        norm = torch.empty(1, dtype=torch.float64, device=dev)
+        _lib.check(lib.mdc_rigid_field_norm(*args, _lib.ptr(out), _lib.ptr(norm), _lib.stream_ptr()),
+                   "mdc_rigid_field_norm")
+        if float(norm[0]) < 1e-12:  # field.py:263-265
+            raise DegenerateRotation("rigid MLS rotation estimate vanished")
+        return out[0].cpu().numpy()
+    fn = {"mean": lib.mdc_mean_field, "affine": lib.mdc_affine_field}[kind]
     _lib.check(fn(*args, _lib.ptr(out), _lib.stream_ptr()), f"mdc_{kind}_field")
     return out[0].cpu().numpy()
 
@@ -255,9 +262,9 @@ def affine_mls(v, controls_p, controls_q, params: MlsParams) -> np.ndarray:
 
 def rigid_mls(v, controls_p, controls_q, params: MlsParams) -> np.ndarray:
     """field.py:243-269: the weighted rigid map at v, on the GPU.  Where the
-    rotation estimate vanishes the kernel returns the mean-blend fallback of
-    _kernels.rigid_field (_kernels.py:168-171) instead of raising
-    DegenerateRotation."""
+    rotation estimate vanishes (|f| < 1e-12) it raises DegenerateRotation
+    like the reference's scalar evaluator (field.py:263-265); only the
+    per-pixel field path takes _kernels.rigid_field's mean fallback."""
     return _point_mls("rigid", v, controls_p, controls_q, params)
 
 

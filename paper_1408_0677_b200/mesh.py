@@ -15,7 +15,9 @@ in the per-corner bincount order of layout.py:240-255).
 
 from __future__ import annotations
 
+import warnings
 from dataclasses import dataclass
+from fractions import Fraction
 
 import numpy as np
 
@@ -210,6 +212,63 @@ def parse_mesh_text(text: str) -> TriMesh:
     return assemble(pts[:, :2].copy(), pts[:, 2:].copy(), tris, jitter_count=0)
 
 
+_ORIENT_BOUND = 3.3306690738754716e-16  # Shewchuk's static orient2d bound (mesh.py:30-48)
+
+
+def _orient_signs(ax, ay, bx, by, cx, cy) -> np.ndarray:
+    """Exact orient2d signs, vectorised: the reference's float filter
+    (mesh.py:38-48) on every row, Fraction arithmetic only where it is
+    inconclusive."""
+    ax, ay, bx, by, cx, cy = np.broadcast_arrays(*(np.asarray(v, dtype=np.float64) for v in (ax, ay, bx, by, cx, cy)))
+    detleft = (ax - cx) * (by - cy)
+    detright = (ay - cy) * (bx - cx)
+    det = detleft - detright
+    sign = np.sign(det).astype(np.int64)
+    unsure = np.abs(det) <= _ORIENT_BOUND * (np.abs(detleft) + np.abs(detright))
+    for i in np.flatnonzero(unsure):
+        F = Fraction
+        d = (F(ax[i]) - F(cx[i])) * (F(by[i]) - F(cy[i])) - (F(ay[i]) - F(cy[i])) * (F(bx[i]) - F(cx[i]))
+        sign[i] = (d > 0) - (d < 0)
+    return sign
+
+
+def _cocircular_ties(pts: np.ndarray, simp: np.ndarray) -> int:
+    """Interior edges whose opposite vertex lies exactly on the neighbouring
+    triangle's circumcircle (exact incircle == 0): there the Delaunay
+    triangulation is not unique and Qhull's choice may differ from the
+    reference's Bowyer-Watson insertion order (mesh.py:220-334)."""
+    tri = np.asarray(simp)
+    e = np.concatenate([tri[:, [1, 2]], tri[:, [2, 0]], tri[:, [0, 1]]])
+    opp = np.concatenate([tri[:, 0], tri[:, 1], tri[:, 2]])
+    key = np.sort(e, axis=1)
+    order = np.lexsort((key[:, 1], key[:, 0]))
+    k = key[order]
+    same = np.flatnonzero((k[1:] == k[:-1]).all(axis=1))
+    if len(same) == 0:
+        return 0
+    i0, i1 = order[same], order[same + 1]
+    t = i0 % len(tri)
+    a, b, c = (pts[tri[t, j]] for j in range(3))
+    d = pts[opp[i1]]
+    adx, ady, bdx, bdy, cdx, cdy = a[:, 0] - d[:, 0], a[:, 1] - d[:, 1], b[:, 0] - d[:, 0], b[:, 1] - d[:, 1], \
+        c[:, 0] - d[:, 0], c[:, 1] - d[:, 1]
+    det = (adx * adx + ady * ady) * (bdx * cdy - cdx * bdy) + (bdx * bdx + bdy * bdy) * (cdx * ady - adx * cdy) + \
+        (cdx * cdx + cdy * cdy) * (adx * bdy - bdx * ady)
+    scale = np.abs(adx * adx + ady * ady) * (np.abs(bdx * cdy) + np.abs(cdx * bdy)) + \
+        np.abs(bdx * bdx + bdy * bdy) * (np.abs(cdx * ady) + np.abs(adx * cdy)) + \
+        np.abs(cdx * cdx + cdy * cdy) * (np.abs(adx * bdy) + np.abs(bdx * ady))
+    ties = 0
+    for i in np.flatnonzero(np.abs(det) <= 1.2e-15 * scale):
+        F = Fraction
+        A, B, C, D = (tuple(F(x) for x in p[i]) for p in (a, b, c, d))
+        fa = [A[0] - D[0], A[1] - D[1], B[0] - D[0], B[1] - D[1], C[0] - D[0], C[1] - D[1]]
+        dd = (fa[0] ** 2 + fa[1] ** 2) * (fa[2] * fa[5] - fa[4] * fa[3]) + \
+            (fa[2] ** 2 + fa[3] ** 2) * (fa[4] * fa[1] - fa[0] * fa[5]) + \
+            (fa[4] ** 2 + fa[5] ** 2) * (fa[0] * fa[3] - fa[2] * fa[1])
+        ties += dd == 0
+    return int(ties)
+
+
 def delaunay(points, seed: int = 0, viewport=None) -> TriMesh:
     """Delaunay triangulation into a TriMesh (signature of mesh.py:419).
 
@@ -235,16 +294,27 @@ def delaunay(points, seed: int = 0, viewport=None) -> TriMesh:
         diag = float(np.hypot(viewport[2] - viewport[0], viewport[3] - viewport[1]))
     rng = np.random.default_rng(seed)
     pts, jitter_count = _jitter_duplicates(pts, diag, rng)
-    d = pts - pts[0]
-    j = int(np.argmax(np.hypot(d[:, 0], d[:, 1])))
-    e = pts[j] - pts[0]
-    if not np.any(e[0] * d[:, 1] - e[1] * d[:, 0]):
+    # mesh.py:441-448: exact collinearity against the first two distinct points
+    i1 = 1
+    while i1 < n and pts[i1, 0] == pts[0, 0] and pts[i1, 1] == pts[0, 1]:
+        i1 += 1
+    if i1 >= n or not _orient_signs(pts[0, 0], pts[0, 1], pts[i1, 0], pts[i1, 1], pts[:, 0], pts[:, 1]).any():
         raise DegenerateInput("all points are collinear")
-    simp = Delaunay(pts).simplices.astype(np.int64)
+    try:
+        simp = Delaunay(pts).simplices.astype(np.int64)
+    except Exception as exc:  # scipy.spatial.QhullError: precision failure on near-degenerate input
+        raise DegenerateInput(f"Qhull could not triangulate the (near-degenerate) input: {exc}") from exc
     p = pts[simp]
-    area = (p[:, 1, 0] - p[:, 0, 0]) * (p[:, 2, 1] - p[:, 0, 1]) - (p[:, 1, 1] - p[:, 0, 1]) * (p[:, 2, 0] - p[:, 0, 0])
-    simp = np.where((area < 0)[:, None], simp[:, [0, 2, 1]], simp)
-    simp = simp[area != 0]
+    sign = _orient_signs(p[:, 0, 0], p[:, 0, 1], p[:, 1, 0], p[:, 1, 1], p[:, 2, 0], p[:, 2, 1])
+    if (sign == 0).any():
+        raise ZeroAreaTriangle(f"Qhull returned {int((sign == 0).sum())} zero-area triangle(s)")
+    simp = np.where((sign < 0)[:, None], simp[:, [0, 2, 1]], simp)
+    if len(np.unique(simp)) != n:
+        raise MeshError(f"triangulation left {n - len(np.unique(simp))} vertex/vertices isolated")
+    ties = _cocircular_ties(pts, simp)
+    if ties:
+        warnings.warn(f"{ties} exactly cocircular edge(s): the Delaunay triangulation is not unique there and "
+                      "may differ from the reference's Bowyer-Watson tie-breaking", RuntimeWarning, stacklevel=2)
     return assemble(pts.copy(), pts.copy(), simp, jitter_count)
 
 

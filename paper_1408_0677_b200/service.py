@@ -18,6 +18,7 @@ bundle is not shipped.
 from __future__ import annotations
 
 import threading
+from collections import OrderedDict
 from dataclasses import dataclass, field as dc_field
 from typing import Optional
 
@@ -52,6 +53,14 @@ class Snapshot:
     params: layout.LayoutParams
 
 
+# Field-cache bounds.  The reference's cache is an unbounded dict of host
+# arrays; here every entry can also hold a GPU fp64 copy (H*W*16 bytes), so
+# the cache is an LRU over entries and only the most recent DEVICE_KEEP
+# entries keep their device copy (older hits re-upload on render).
+CACHE_MAX_ENTRIES = 64
+DEVICE_KEEP = 4
+
+
 @dataclass
 class Session:
     """service.py:50-72 (field cache keyed by the full parameter tuple)."""
@@ -62,22 +71,36 @@ class Session:
     snapshot: Snapshot
     lock: threading.Lock = dc_field(default_factory=threading.Lock)
     recomputing: bool = dc_field(default=False)
-    _field_cache: dict = dc_field(default_factory=dict)
+    _field_cache: OrderedDict = dc_field(default_factory=OrderedDict)
     cache_hits: int = 0
     cache_misses: int = 0
+
+    def _touch(self, key):  # caller holds the lock
+        self._field_cache.move_to_end(key)
+        for i, k in enumerate(reversed(self._field_cache)):
+            if i >= DEVICE_KEEP:
+                self._field_cache[k].device_coords = None
+        while len(self._field_cache) > CACHE_MAX_ENTRIES:
+            self._field_cache.popitem(last=False)
 
     def cached_field(self, key, build):
         with self.lock:
             hit = self._field_cache.get(key)
             if hit is not None:
                 self.cache_hits += 1
+                self._touch(key)
         if hit is not None:
             return hit
         fld = build()
         with self.lock:
             self.cache_misses += 1
+            if key[0] != self.snapshot.revision:
+                # built from a snapshot that was swapped out meanwhile: serve it, do not cache it
+                return fld
             # identical keys reuse bit-identical fields: first write wins
-            return self._field_cache.setdefault(key, fld)
+            fld = self._field_cache.setdefault(key, fld)
+            self._touch(key)
+            return fld
 
     def swap_snapshot(self, snap: Snapshot):
         with self.lock:
@@ -166,8 +189,9 @@ def render_png(session: Session, dim: str = "", dim2: str = "", variant: Optiona
             errors["spacing"] = "must be a number or 'auto'"
     if errors:
         raise RequestError(400, {"errors": errors})
-    for name in (dim, dim2):
-        if name and name != "projection" and name not in session.ds.names:
+    # service.py:183-192: 'projection' is a valid dim only; any unknown dim2 is a 404
+    for name, allow_projection in ((dim, True), (dim2, False)):
+        if name and not (allow_projection and name == "projection") and name not in session.ds.names:
             raise RequestError(404, {"error": f"unknown dimension {name!r}", "columns": session.ds.names})
 
     if not dim or dim == "projection":
@@ -212,6 +236,8 @@ def relayout(session: Session, iterations: int = 500, decay_lambda: float = 0.99
             raise RequestError(409, {"error": "layout recompute already in progress"})
         session.recomputing = True
         target_revision = session.snapshot.revision + 1
+    # the worker thread starts on the default device: pin the caller's (the session's) device
+    dev = torch.cuda.current_device() if torch.cuda.is_available() else None
 
     def work():
         try:
@@ -222,8 +248,8 @@ def relayout(session: Session, iterations: int = 500, decay_lambda: float = 0.99
                 overrides["desired_edge_d"] = edge_length
             params = layout.LayoutParams.defaults_for(session.mesh, iterations=iterations, **overrides)
             session.mesh.current_pos = session.mesh.original_pos.copy()
-            if torch.cuda.is_available():
-                torch.cuda.set_device(torch.cuda.current_device())
+            if dev is not None:
+                torch.cuda.set_device(dev)
             state = layout.layout_run(session.mesh, params)
             session.swap_snapshot(Snapshot(target_revision, state, params))
         finally:

@@ -153,3 +153,16 @@ def test_empty_and_ragged_inputs_raise_cleanly():
         F.compute_fields(np.zeros((4, 3)), np.zeros((4, 1)), F.MlsParams("affine"), 8, 8)
     with pytest.raises(ValueError):
         F.compute_fields(np.random.rand(4, 2), np.zeros((5, 1)), F.MlsParams("affine"), 8, 8)
+
+
+def test_rigid_degenerate_raises():
+    """Reference test_field.py:108-113: a symmetric pinch cancels the rotation
+    estimate at the midpoint; the scalar rigid evaluator raises (field.py:263-265)
+    while the field path keeps _kernels.rigid_field's per-pixel mean fallback."""
+    p = np.array([[-1.0, 0.0], [1.0, 0.0]])
+    q = np.array([[0.0, -1.0], [0.0, 1.0]])
+    with pytest.raises(F.DegenerateRotation):
+        F.rigid_mls(np.array([0.0, 0.0]), p, q, F.MlsParams(variant="rigid", alpha=1.0))
+    # off the pinch the rotation is well defined
+    out = F.rigid_mls(np.array([0.3, 0.2]), p, q, F.MlsParams(variant="rigid", alpha=1.0))
+    assert np.isfinite(out).all()

@@ -198,3 +198,34 @@ def test_viewer_loop_acceptance(tmp_path):
     dt = sorted(times)[1]
     print("alpha slider round trips (s):", [round(t, 4) for t in times])
     assert dt < 1.0
+
+
+def test_dim2_projection_is_404(client, session):
+    """service.py:188-192: 'projection' is accepted as dim only; an unknown dim2
+    (including 'projection') is a 404, never a 500."""
+    r = client.get("/api/render.png", params={"dim": session.ds.names[0], "dim2": "projection"})
+    assert r.status_code == 404
+    assert client.get("/api/render.png", params={"dim": "projection"}).status_code == 200
+
+
+def test_field_cache_is_bounded_and_drops_stale_revisions(session, monkeypatch):
+    """The cache is an LRU (CACHE_MAX_ENTRIES) and only the DEVICE_KEEP most
+    recent entries keep their GPU copy; a field built for a revision that was
+    swapped out meanwhile is served but not cached."""
+    monkeypatch.setattr(service, "CACHE_MAX_ENTRIES", 5)
+    monkeypatch.setattr(service, "DEVICE_KEEP", 2)
+    rev = session.snapshot.revision
+    dim = session.ds.names[0]
+    for i in range(8):
+        service.render_png(session, dim=dim, alpha=0.5 + 0.1 * i, w=32, h=24)
+    with session.lock:
+        entries = list(session._field_cache.values())
+    assert len(entries) == 5
+    assert sum(e.device_coords is not None for e in entries) == 2
+    assert entries[-1].device_coords is not None
+    # a build for a stale revision is returned but not inserted
+    before = len(session._field_cache)
+    stale_key = (rev - 1, dim, "", "mean", 1.0, 1.0, 32, 24)
+    out = session.cached_field(stale_key, lambda: entries[-1])
+    assert out is entries[-1]
+    assert stale_key not in session._field_cache and len(session._field_cache) == before

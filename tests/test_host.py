@@ -161,3 +161,32 @@ def test_row_band_plan():
         if r1 - r0 >= 2:
             assert len(plan) == 2 and plan[1][1] - plan[1][0] <= plan[0][1] - plan[0][0]
     assert plan_row_bands(0, 2160, 4) == [(0, 1890), (1890, 2160)]
+
+
+def test_delaunay_degenerate_inputs():
+    """Robust host preprocessing (reference mesh.py:419-467): exact
+    collinearity test, every vertex triangulated, and exactly cocircular
+    lattices flagged (the triangulation is not unique there; Qhull's tie-break
+    may differ from the reference's Bowyer-Watson insertion order)."""
+    import warnings
+
+    with pytest.raises(mesh.DegenerateInput):
+        mesh.delaunay(np.column_stack([np.arange(6.0), 3.0 * np.arange(6.0) + 1.0]))
+    # nearly collinear but not exactly: triangulates, or fails as a MeshError (never a raw QhullError)
+    pts = np.column_stack([np.arange(6.0), np.zeros(6)])
+    pts[3, 1] = 1e-12
+    m = mesh.delaunay(pts)
+    assert len(np.unique(m.triangles)) == 6
+    pts[3, 1] = 1e-300
+    with pytest.raises(mesh.MeshError):
+        mesh.delaunay(pts)
+    xs, ys = np.meshgrid(np.arange(5.0), np.arange(4.0))
+    with warnings.catch_warnings(record=True) as w:
+        warnings.simplefilter("always")
+        m = mesh.delaunay(np.column_stack([xs.ravel(), ys.ravel()]))
+    assert any("cocircular" in str(x.message) for x in w)
+    assert len(np.unique(m.triangles)) == 20 and (m.signed_areas() > 0).all()
+    rng = np.random.default_rng(0)
+    with warnings.catch_warnings():
+        warnings.simplefilter("error")
+        mesh.delaunay(rng.normal(size=(500, 2)))
