@@ -110,65 +110,92 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # CPU arm (oracle = C restatement of the reference, all host threads)
 
-def cpu_mls_sample(positions, raw, cfg, target_s=10.0, dims=1):
-    """Time the reference's affine kernel restated in C on a band of rows
-    through the frame centre, `dims` dims, sized to ~target_s seconds."""
+def cpu_mls_sample(positions, raw, cfg, target_s=10.0, dims=4, nrows=16):
+    """Time the reference's affine kernel (_kernels.affine_field, restated in
+    C: oracle/mdc_oracle.c, all host threads) the way the reference renders:
+    one call per dimension with targets (q_k, 0) (cli.py:143-165), on
+    `nrows` rows spread top to bottom over the frame (every `stride`-th
+    column when a full row would overrun the time budget), `dims` dims."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as O
 
     O.set_threads(os.cpu_count() or 1)
     W, H = cfg["W"], cfg["H"]
-    mid = H // 2
-    tv = np.column_stack([raw[:, 0], np.zeros(len(raw))])
+    rows = sorted({int(r) for r in np.linspace(0, H - 1, nrows)})
+    vp = O.viewport(positions, W, H)
+    xs, ys = O.pixel_centers(vp, W, H)
+    pm = positions.mean(axis=0)
+    pc = positions - pm
+
+    def run(cols, k):
+        tv = np.column_stack([raw[:, k], np.zeros(len(raw))])
+        qm = tv.mean(axis=0)
+        O.mls_kernel("affine", xs[rows][:, cols].ravel() - pm[0], ys[rows][:, cols].ravel() - pm[1], pc,
+                     tv - qm, 1.5)
+
+    probe = np.arange(0, W, max(1, W // 64))
     t0 = time.perf_counter()
-    O.compute_field(positions, tv, "affine", W, H, rows=(mid, mid + 1))
-    t_row = time.perf_counter() - t0
-    rows = int(max(1, min(H // 2, round(target_s / max(t_row * dims, 1e-6)))))
+    run(probe, 0)
+    per_px = (time.perf_counter() - t0) / (len(rows) * len(probe))
+    stride = max(1, int(np.ceil(per_px * len(rows) * W * dims / target_s)))
+    cols = np.arange(0, W, stride)
     t0 = time.perf_counter()
     for k in range(dims):
-        tv = np.column_stack([raw[:, k], np.zeros(len(raw))])
-        O.compute_field(positions, tv, "affine", W, H, rows=(mid - rows // 2, mid - rows // 2 + rows))
+        run(cols, k)
     dt = time.perf_counter() - t0
-    return {"value": rows * W * dims / dt / 1e6, "unit": UNIT, "cores": O.max_threads(),
+    px = len(rows) * len(cols)
+    return {"value": px * dims / dt / 1e6, "unit": UNIT, "cores": O.max_threads(),
             "kind": "port", "seconds": dt,
-            "sample": f"affine_field restated in C (oracle/mdc_oracle.c), {rows} rows x {W} px "
-                      f"through the frame centre, {dims} dim(s), N={len(positions)} controls, fp64"}
+            "sample": f"affine_field restated in C (oracle/mdc_oracle.c), one call per dim: {len(rows)} rows "
+                      f"spread over the frame x {len(cols)} px (every {stride}th column), {dims} dims, "
+                      f"N={len(positions)} controls at the laid-out positions, fp64"}
 
 
-def cpu_layout_sample(mesh, params, steps=2):
+def cpu_layout_sample(mesh, params, states, steps=10):
+    """layout_step restated in C (oracle, all host threads): `steps` steps from
+    iteration 0 and `steps` from iteration 250."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as O
 
     p = {k: getattr(params, k) for k in ("repulsion_c", "spring_scale", "desired_edge_d",
                                          "softening_eta", "bh_theta", "initial_temp", "decay_lambda")}
-    t0 = time.perf_counter()
-    O.layout_run(mesh.original_pos, mesh.csr_offsets, mesh.csr_targets, mesh.triangles, p, steps)
-    dt = time.perf_counter() - t0
-    return {"value": mesh.node_count * steps / dt, "unit": "vertex-iters/s",
+    dt, done = 0.0, []
+    for it, pos in sorted(states.items()):
+        temp = params.initial_temp * params.decay_lambda ** it
+        t0 = time.perf_counter()
+        O.layout_run(pos, mesh.csr_offsets, mesh.csr_targets, mesh.triangles, p, steps, temperature=temp)
+        dt += time.perf_counter() - t0
+        done.append(it)
+    nsteps = steps * len(done)
+    return {"value": mesh.node_count * nsteps / dt, "unit": "vertex-iters/s",
             "cores": O.max_threads(), "kind": "port",
-            "sample": f"{steps} layout_step(s) restated in C, N={mesh.node_count}"}
+            "sample": f"{steps} layout_steps restated in C from each of iterations {done}, N={mesh.node_count}"}
 
 
-# ---------------------------------------------------------------------------
+def config_dict(cfg, world):
+    """One config dict for both arms (the driver compares them)."""
+    return {"workload": workload_name(cfg), "points": cfg["n"], "dims": cfg["d"], "width": cfg["W"],
+            "height": cfg["H"], "layout_iterations": cfg["iters"], "parallelism": f"rowband{world}",
+            "l2": "flushed between frames (256 MiB write)"}
 
 
-def build_scene(cfg, device_pca=True):
-    from paper_1408_0677_b200 import dataset as D
-    from paper_1408_0677_b200 import mesh as M
-    from paper_1408_0677_b200 import projection as P
-
-    X = gmm(cfg["n"], cfg["d"], cfg["seed"])
-    ds = D.normalize(D.Dataset(names=[f"d{i}" for i in range(cfg["d"])], data=X))
-    if device_pca:
-        model, cloud = P.pca_project(ds)
-        positions = cloud.positions
-    else:
-        sys.path.insert(0, os.path.join(ROOT, "oracle"))
-        import oracle as O
-        positions = O.pca_project(ds.data)[3]
-    mesh = M.delaunay(positions, seed=0)
-    raw = np.column_stack([ds.raw_column(nm) for nm in ds.names])
-    return ds, mesh, raw
+def laid_out_positions(cfg, mesh):
+    """The GPU arm's positions after 250 and `iters` layout iterations, from
+    bench_data/ (written by tools/make_bench_positions.py from this repo's
+    deterministic GPU layout); PCA positions when no fixture matches."""
+    path = os.path.join(ROOT, "bench_data", f"config{cfg['id']}_positions.npz")
+    try:
+        z = np.load(path)
+        # the CPU arm's PCA (oracle) may differ from the GPU's in the last bits:
+        # same mesh topology and positions equal to 1e-9 of the extent
+        ext = float(np.ptp(mesh.original_pos))
+        if int(z["iters"]) == cfg["iters"] and z["pos_final"].shape == mesh.original_pos.shape and \
+                np.array_equal(z["triangles"], mesh.triangles) and \
+                np.allclose(z["original_pos"], mesh.original_pos, rtol=0, atol=1e-9 * ext):
+            return {0: mesh.original_pos, 250: z["pos_250"]}, z["pos_final"]
+    except (OSError, KeyError):
+        pass
+    return {0: mesh.original_pos}, mesh.original_pos
 
 
 def run_reference(args, cfg, rank):
@@ -178,7 +205,7 @@ def run_reference(args, cfg, rank):
 
     ds, mesh, raw = build_scene(cfg, device_pca=False)
     params = LayoutParams.defaults_for(mesh, iterations=cfg["iters"])
-    positions = mesh.original_pos
+    states, positions = laid_out_positions(cfg, mesh)
     sample_s = max(1.0, args.cpu_seconds / max(1, args.steps + args.warmup))
     for _ in range(args.warmup):
         cpu_mls_sample(positions, raw, cfg, target_s=sample_s)
@@ -188,14 +215,13 @@ def run_reference(args, cfg, rank):
         vals.append(s["value"])
         secs.append(s["seconds"])
     value = statistics.median(vals)
-    lay = cpu_layout_sample(mesh, params, steps=1)
+    lay = cpu_layout_sample(mesh, params, states, steps=10 if cfg["n"] <= 200_000 else 1)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * statistics.median(secs), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload_name(cfg), "points": cfg["n"], "dims": cfg["d"],
-                   "width": cfg["W"], "height": cfg["H"], "layout_iterations": cfg["iters"]},
+        "config": config_dict(cfg, args.gpus),
         "cpu_baseline": {k: s[k] for k in ("value", "unit", "cores", "kind", "sample")} | {"value": value},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "layout": {"metric": "vertex-iters/s", **lay},
@@ -298,12 +324,13 @@ def main():
     ap.add_argument("--frame", default=None, help="override the raster, WxH (profiling only)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-tc", action="store_true", help="force the SIMT MLS kernel (A/B)")
+    ap.add_argument("--no-fp64", action="store_true", help="skip the fp64 (reference precision) line")
     ap.add_argument("--dist-backend", default="nccl",
                     help="torch.distributed backend (gloo: host-mediated collectives, lets several ranks "
                          "share one GPU for a functional check of the N>1 path; never a bench number)")
     ap.add_argument("--layout-partition", action="store_true",
                     help="vertex-partition the layout over the ranks (default for config 4)")
-    ap.add_argument("--layout-exchange", default="p2p", choices=["p2p", "allreduce"],
+    ap.add_argument("--layout-exchange", default="allgather", choices=["allgather", "p2p", "allreduce"],
                     help="partitioned layout: step kernel stores into every rank's buffer over NVLink "
                          "(p2p, cudaIpc) or a SUM all-reduce per iteration")
     args = ap.parse_args()
@@ -348,9 +375,13 @@ def main():
     if not args.no_layout:
         temps = L.temperature_schedule(params.initial_temp, params.decay_lambda, cfg["iters"])
         p2p = partition and args.layout_exchange == "p2p"
+        ag = partition and args.layout_exchange == "allgather"
         if p2p:  # the step kernel stores its slice into every rank's buffer
             run = L.P2PLayout(mesh, params, temps)
             eng = run.eng
+        elif ag:  # packed owned slices, one NCCL all-gather per iteration
+            gat = L.GatherLayout(mesh, params)
+            eng = gat.eng
         else:
             eng = L.LayoutEngine(mesh, params, part=(rank, world) if partition else (0, 1))
 
@@ -364,7 +395,10 @@ def main():
             if p2p:
                 for _ in range(k):
                     run.step()
-            elif partition:  # one SUM all-reduce of positions per iteration (SURVEY.md §8e)
+            elif ag:
+                for it in range(k):
+                    gat.step(temps[it:it + 1])
+            elif partition:  # one SUM all-reduce of positions per iteration
                 for it in range(k):
                     eng.run(temps[it:it + 1])
                     dist.all_reduce(eng.pos, op=dist.ReduceOp.SUM)
@@ -388,15 +422,19 @@ def main():
         t = torch.tensor([lay_ms], device=dev)
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        units = cfg["n"] * cfg["iters"] * (1 if partition else world)
+        # the whole mesh advances `iters` steps; replicas repeat the same work, so
+        # they are not counted as extra throughput
+        units = cfg["n"] * cfg["iters"]
         layout_res = {"metric": "vertex-iters/s", "unit": "vertex-iters/s",
                       "value": units / (t.item() * 1e-3),
                       "ms_total": t.item(), "iterations": cfg["iters"], "points": cfg["n"],
                       "orientation_flips": flips,
                       "scaling": ("strong (vertex-partitioned, step kernel stores into peer buffers over "
                                   "NVLink, host barrier per iteration)" if p2p else
+                                  "strong (vertex-partitioned, one all-gather of the packed owned slices per "
+                                  "iteration)" if ag else
                                   "strong (vertex-partitioned, SUM all-reduce per iteration)") if partition
-                      else "replicas only"}
+                      else "replicas only (each rank runs the whole layout; value is one replica's)"}
         if p2p:
             run.close()
         if rank == 0:
@@ -520,30 +558,82 @@ def main():
                 "fp64_peak_tflops": peaks["fp64"] / 1e12,
                 "kernel_share_of_step": kernel_ms / ms_step}
 
+    fp64 = None if args.no_fp64 else run_fp64(positions, raw, cfg, W, H, d, dev, lib, peaks)
+
     cpu = None
     if not args.no_cpu and world == 1:  # the CPU baseline is quoted at N=1 only
         cpu = cpu_mls_sample(positions, raw, cfg, target_s=args.cpu_seconds)
         cpu.pop("seconds", None)
         if layout_res is not None:
-            layout_res["cpu_baseline"] = cpu_layout_sample(mesh, params, steps=1)
+            states, fixture = laid_out_positions(cfg, mesh)
+            layout_res["cpu_baseline"] = cpu_layout_sample(mesh, params, states, steps=2)
+            layout_res["positions_equal_cpu_arm_fixture"] = bool(np.array_equal(fixture, positions))
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": workload_name(cfg), "points": cfg["n"], "dims": d, "width": W,
-                   "height": H, "layout_iterations": cfg["iters"], "parallelism": f"rowband{world}",
-                   "l2": "flushed between frames (256 MiB write)"},
+        "config": config_dict(cfg, world),
         "gpu_launches": (6 if use_tc else 5) * args.steps,
         "clocks": clk.summary(),
         "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": e2e,
+        "fp64": fp64,
         "layout": layout_res,
     }
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_fp64(positions, raw, cfg, W, H, d, dev, lib, peaks, band_div=8):
+    """The reference's own precision: the same workload through the fp64
+    parity kernel (mls_kernel<double>, reference arithmetic _kernels.py:70-124,
+    1e-10 contract), on a band of H/band_div rows through the frame centre
+    (per-pixel cost is uniform; a full 4K frame takes seconds in fp64),
+    CUDA-event timed, L2 flushed first.  Roofline: executed fp64 lane-ops per
+    (pixel, control) pair from the committed ncu capture
+    (profiles/r02_mls_fp64_ops.json) x 2 / kernel time vs the live DFMA peak."""
+    import torch
+
+    from paper_1408_0677_b200 import _lib
+    from paper_1408_0677_b200.field import MlsProblem
+
+    prob = MlsProblem(positions, raw, "affine", W, H, dtype="f64")
+    rows = max(1, H // band_div)
+    r0 = (H - rows) // 2
+    out = torch.empty((d, rows, W), dtype=torch.float64, device=dev)
+    warm = prob.args(out, (rows * W, W, 1), r0, r0 + min(rows, 8))
+    a = prob.args(out, (rows * W, W, 1), r0, r0 + rows)
+    stream = torch.cuda.current_stream()
+    _lib.check(lib.mdc_mls_field(ctypes.byref(warm), stream.cuda_stream), "mdc_mls_field")
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    flush.fill_(1)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    _lib.check(lib.mdc_mls_field(ctypes.byref(a), stream.cuda_stream), "mdc_mls_field")
+    e1.record(stream)
+    e1.synchronize()
+    ms = e0.elapsed_time(e1)
+    pairs = rows * W * cfg["n"]
+    res = {"value": rows * W * d / (ms * 1e-3) / 1e6, "unit": UNIT, "dtype": "f64", "kernel_ms": ms,
+           "sample": f"{rows} rows x {W} px through the frame centre (1/{band_div} of the frame), all {d} dims, "
+                     f"N={cfg['n']} controls",
+           "kernel": "mls_kernel<double, AFFINE, alpha=1.5> (SIMT, fp64 parity mode)"}
+    try:
+        ops = json.load(open(os.path.join(ROOT, "profiles", "r02_mls_fp64_ops.json")))
+        if ops.get("d") == d:
+            achieved = 2 * pairs * ops["fp64_lane_ops_per_pair"] / (ms * 1e-3)
+            res["roofline"] = {"bound": "fp64", "achieved": achieved / 1e12, "peak": peaks["fp64"] / 1e12,
+                               "unit": "TFLOP/s", "frac": achieved / peaks["fp64"],
+                               "fp64_lane_ops_per_pair": ops["fp64_lane_ops_per_pair"],
+                               "achieved_def": "executed fp64 lane-ops (ncu SASS count, DFMA/DADD/DMUL) x 2 / "
+                                               "kernel time", "peak_source": "measured DFMA microbenchmark"}
+    except (OSError, ValueError, KeyError):
+        pass
+    return res
 
 
 def run_e2e(args, positions, raw, spacing, W, H, d, r0, r1, dev, world):

@@ -304,6 +304,17 @@ MDC_API int mdc_layout_set_peers(MdcLayoutPlan *plan, int32_t world, double *con
  * the temps index (the step count into `temps`). */
 MDC_API int mdc_layout_step_parity(MdcLayoutPlan *plan, int32_t parity, const double *temps, int32_t use_graph,
                                    void *stream);
+/* Vertex-partitioned plans (part_world > 1), all-gather exchange (SURVEY.md
+ * §8e "positions NCCL-allgathered once per iteration"): after
+ * mdc_layout_set_gather(plan, send) -- before the first step -- each step
+ * writes this rank's owned slice (leaf order n*r/w .. n*(r+1)/w of the step's
+ * kd-tree) packed into send (ceil(n/w) x 2 fp64, device) instead of pos; the
+ * caller all-gathers the send buffers of all ranks into recv (w x chunk x 2,
+ * rank-major, e.g. ncclAllGather) and mdc_layout_scatter(plan, recv, chunk)
+ * writes every vertex's new position into pos through the step's
+ * permutation.  Bit-identical to the single-GPU step. */
+MDC_API int mdc_layout_set_gather(MdcLayoutPlan *p, double *send);
+MDC_API int mdc_layout_scatter(MdcLayoutPlan *p, const double *recv, int64_t chunk, void *stream);
 MDC_API int mdc_layout_reset_counter(MdcLayoutPlan *plan, void *stream);
 /* Inter-process device buffers (cudaIpc): allocate + 64-byte handle, open a
  * peer's handle in this process, close an opened mapping, free an allocation. */

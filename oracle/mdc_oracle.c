@@ -125,7 +125,10 @@ EXPORT void orc_affine_field(int64_t npix, const double *vx, const double *vy, i
  * solve follow orc_affine_field's operation order, so each channel is
  * bit-identical to a separate 2-channel call.  q: (n, d) row-major,
  * out: (npix, d) row-major. */
-EXPORT void orc_affine_field_d(int64_t npix, const double *vx, const double *vy, int64_t n,
+/* -O3 lets gcc vectorise the per-channel loop; each channel's accumulator
+ * still sees the same operations in the same order (no reassociation, no
+ * contraction: -ffp-contract=off), so results are bit-identical. */
+__attribute__((optimize("O3"))) EXPORT void orc_affine_field_d(int64_t npix, const double *vx, const double *vy, int64_t n,
                                const double *px, const double *py, int64_t d, const double *q,
                                double alpha, double reg_eps, double *out) {
 #pragma omp parallel

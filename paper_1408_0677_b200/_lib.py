@@ -119,6 +119,8 @@ SIGNATURES = {
     "mdc_layout_set_peers": (ctypes.c_int, [_vp, ctypes.c_int32, _vp, _vp]),
     "mdc_layout_step_parity": (ctypes.c_int, [_vp, ctypes.c_int32, _vp, ctypes.c_int32, _vp]),
     "mdc_layout_reset_counter": (ctypes.c_int, [_vp, _vp]),
+    "mdc_layout_set_gather": (ctypes.c_int, [_vp, _vp]),
+    "mdc_layout_scatter": (ctypes.c_int, [_vp, _vp, _c_i64, _vp]),
     "mdc_ipc_alloc": (ctypes.c_int, [ctypes.c_size_t, _vp, _vp]),
     "mdc_ipc_open": (ctypes.c_int, [_vp, _vp]),
     "mdc_ipc_close": (ctypes.c_int, [_vp]),

@@ -992,6 +992,9 @@ struct LocalArgs {
     // next-parity buffer (NVLink stores) instead of pos_out
     int npeer;
     double *peer_out[MDC_MAX_PEERS];
+    // all-gather exchange: the owned slice's new positions, packed in leaf
+    // order (send[idx] for vertex perm[k0 + idx]), instead of pos_out
+    double *send;
 };
 
 __device__ __forceinline__ double2 ld2(const double *p, int i) {
@@ -1052,6 +1055,7 @@ __global__ void clamp_factors_kernel(int64_t n, const double *pos, const double 
 
 __global__ void local_kernel(LocalArgs a) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t idx = i;
     if (a.perm) {
         if (a.k0 + i >= a.k1) return;
         i = a.perm[a.k0 + i];
@@ -1120,7 +1124,9 @@ __global__ void local_kernel(LocalArgs a) {
     const double s = clamp_factor(a.pos, a.tris, a.inc, b0, b1, pi, f, a.eta);
     if (a.dbg_scale) a.dbg_scale[i] = s;
     const double2 np = make_double2(dadd(pi.x, dmul(s, f.x)), dadd(pi.y, dmul(s, f.y)));
-    if (a.npeer) {
+    if (a.send) {
+        reinterpret_cast<double2 *>(a.send)[idx] = np;
+    } else if (a.npeer) {
         for (int r = 0; r < a.npeer; ++r) reinterpret_cast<double2 *>(a.peer_out[r])[i] = np;
         __threadfence_system();  // visible to the peers once the step is over
     } else {
@@ -1277,7 +1283,9 @@ __global__ void __launch_bounds__(128) local_group_kernel(LocalArgs a) {
     if (!live || !lead) return;
     if (a.dbg_scale) a.dbg_scale[i] = s;
     const double2 np = make_double2(dadd(pi.x, dmul(s, f.x)), dadd(pi.y, dmul(s, f.y)));
-    if (a.npeer) {
+    if (a.send) {
+        reinterpret_cast<double2 *>(a.send)[idx] = np;
+    } else if (a.npeer) {
         for (int r = 0; r < a.npeer; ++r) reinterpret_cast<double2 *>(a.peer_out[r])[i] = np;
         __threadfence_system();
     } else {
@@ -1286,6 +1294,21 @@ __global__ void __launch_bounds__(128) local_group_kernel(LocalArgs a) {
 }
 
 __global__ void incr_kernel(int32_t *ctr) { ctr[0] += 1; }
+
+// All-gather exchange, receive side: recv holds every rank's packed slice
+// (rank r at r * chunk, n*r/w .. n*(r+1)/w in leaf order); scatter them to
+// vertex order through the step's tree permutation.
+__global__ void gather_scatter_kernel(int64_t n, int world, int64_t chunk, const int32_t *perm,
+                                      const double *recv, double *pos) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // leaf-order index
+    if (k >= n) return;
+    // owner rank of leaf slot k: the largest r with n*r/w <= k
+    int r = (int)((k * world) / n);
+    while (r + 1 < world && n * (r + 1) / world <= k) ++r;
+    while (r > 0 && n * r / world > k) --r;
+    const int64_t idx = k - n * r / world;
+    reinterpret_cast<double2 *>(pos)[perm[k]] = reinterpret_cast<const double2 *>(recv)[r * chunk + idx];
+}
 
 }  // namespace mdc
 
@@ -1309,6 +1332,10 @@ struct MdcLayoutPlan {
     // peer-memory exchange (mdc_layout_set_peers)
     int npeer = 0;
     double *peers[2][MDC_MAX_PEERS] = {};
+    // all-gather exchange (mdc_layout_set_gather): packed send buffer, and the
+    // leaf permutation of the last enqueued step (fixed pointer per plan)
+    double *gather_send = nullptr;
+    const int32_t *last_perm = nullptr;
     bool timing = false;
     unsigned long long *count = nullptr;  // non-null: instrumented BH launch
     void mark(cudaStream_t s) {
@@ -1467,10 +1494,14 @@ static int enqueue_step(MdcLayoutPlan *p, const double *pin, double *pout, const
     la.k0 = 0;
     la.k1 = n;
     la.npeer = 0;
+    la.send = nullptr;
+    p->last_perm = perm;
     if (p->a.part_world > 1 && perm) {
         part_range(p, la.k0, la.k1);
         la.perm = perm;
-        if (p->npeer) {
+        if (p->gather_send) {
+            la.send = p->gather_send;  // every slot of pos_out is rewritten by the scatter
+        } else if (p->npeer) {
             const int par_out = pout == p->a.pos ? 0 : 1;  // which parity buffer the step writes
             la.npeer = p->npeer;
             for (int r = 0; r < p->npeer; ++r) la.peer_out[r] = p->peers[par_out][r];
@@ -1725,6 +1756,27 @@ extern "C" int mdc_layout_step_parity(MdcLayoutPlan *p, int32_t parity, const do
     }
     MDC_REQUIRE(p->graph_temps == temps, "temps pointer changed after graph capture");
     MDC_CHECK_CUDA(cudaGraphLaunch(p->graph[parity], s));
+    return MDC_OK;
+}
+
+extern "C" int mdc_layout_set_gather(MdcLayoutPlan *p, double *send) {
+    MDC_REQUIRE(p, "null pointer");
+    MDC_REQUIRE(p->a.part_world > 1, "the all-gather exchange needs a partitioned plan (part_world > 1)");
+    MDC_REQUIRE(!p->graph[0] && !p->graph[1], "set the gather buffer before the first captured step");
+    p->gather_send = send;
+    return MDC_OK;
+}
+
+extern "C" int mdc_layout_scatter(MdcLayoutPlan *p, const double *recv, int64_t chunk, void *stream) {
+    MDC_REQUIRE(p && recv, "null pointer");
+    MDC_REQUIRE(p->gather_send && p->last_perm, "no partitioned all-gather step has been enqueued");
+    const int64_t n = p->shape.n;
+    const int w = p->a.part_world;
+    MDC_REQUIRE(chunk >= (n + w - 1) / w, "chunk must hold the largest slice, ceil(n / world)");
+    if (n == 0) return MDC_OK;
+    gather_scatter_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(n, w, chunk, p->last_perm,
+                                                                                         recv, p->a.pos);
+    MDC_CHECK_LAUNCH();
     return MDC_OK;
 }
 

@@ -303,15 +303,23 @@ def _wrap_device(ptr: int, shape, dtype) -> torch.Tensor:
     return torch.as_tensor(_View(), device=torch.device("cuda", torch.cuda.current_device()))
 
 
-def layout_run_partitioned(mesh, params: LayoutParams, group=None, exchange: str = "allreduce") -> LayoutState:
+def layout_run_partitioned(mesh, params: LayoutParams, group=None, exchange: str = "allgather") -> LayoutState:
     """layout_run with the vertices partitioned over the ranks of ``group``
     (SURVEY.md §8e, config 4): every rank rebuilds the kd-tree from the full
     snapshot and updates its leaf-order slice of the vertices; the slices are
-    reassembled each iteration either by one SUM all-reduce (``allreduce``:
-    non-owned entries are exactly 0.0) or by the step kernel itself storing
-    its slice into every rank's next position buffer over NVLink (``p2p``:
-    cudaIpc-mapped peer buffers, one host barrier per step).  Both are
-    bit-identical to the single-GPU trajectory."""
+    reassembled each iteration by
+
+    * ``allgather`` (default, the north_star's exchange): the step packs the
+      owned slice in leaf order, one all_gather_into_tensor (NCCL over
+      NVLink on the GPU box) collects every slice, ``mdc_layout_scatter``
+      writes them back in vertex order -- n x 16 bytes received per rank;
+    * ``allreduce``: non-owned entries are exactly 0.0 and one SUM
+      all-reduce adds the slices (about twice the bytes);
+    * ``p2p``: the step kernel stores its slice into every rank's next
+      position buffer over NVLink (cudaIpc-mapped peer buffers, one host
+      barrier per step).
+
+    All three are bit-identical to the single-GPU trajectory."""
     import torch.distributed as dist
 
     world = dist.get_world_size(group) if dist.is_initialized() else 1
@@ -319,11 +327,17 @@ def layout_run_partitioned(mesh, params: LayoutParams, group=None, exchange: str
     state = initial_state(mesh, params)
     k = params.iterations
     temps = temperature_schedule(state.temperature, params.decay_lambda, k + 1)
+    if exchange not in ("allgather", "allreduce", "p2p"):
+        raise ValueError(f"exchange must be 'allgather', 'allreduce' or 'p2p', got {exchange!r}")
     if exchange == "p2p" and world > 1:
         pos = _run_p2p(mesh, params, temps[:k], world, rank, group)
+    elif exchange == "allgather" and world > 1:
+        ag = GatherLayout(mesh, params, group)
+        ag.eng.set_positions(mesh.current_pos)
+        for it in range(k):
+            ag.step(temps[it:it + 1])
+        pos = ag.eng.pos.cpu().numpy()
     else:
-        if exchange not in ("allreduce", "p2p"):
-            raise ValueError(f"exchange must be 'allreduce' or 'p2p', got {exchange!r}")
         eng = LayoutEngine(mesh, params, part=(rank, world))
         eng.set_positions(mesh.current_pos)
         for it in range(k):
@@ -334,6 +348,33 @@ def layout_run_partitioned(mesh, params: LayoutParams, group=None, exchange: str
     mesh.current_pos = pos
     return LayoutState(mesh=mesh, iteration=k, temperature=float(temps[k]) if k else params.initial_temp,
                        relaxed_pos=mesh.current_pos.copy())
+
+
+class GatherLayout:
+    """Vertex-partitioned layout with the all-gather exchange: per step, the
+    captured step graph (tree + BH + local update of this rank's leaf-order
+    slice, packed into ``send``), one ``all_gather_into_tensor`` and one
+    scatter kernel back to vertex order (``mdc_layout_scatter``)."""
+
+    def __init__(self, mesh, params: LayoutParams, group=None):
+        import torch.distributed as dist
+
+        self.dist, self.group = dist, group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.eng = LayoutEngine(mesh, params, part=(self.rank, self.world))
+        n = self.eng.n
+        self.chunk = -(-n // self.world)
+        dev = self.eng.device
+        self.send = torch.zeros((self.chunk, 2), dtype=torch.float64, device=dev)
+        self.recv = torch.empty((self.world * self.chunk, 2), dtype=torch.float64, device=dev)
+        _lib.check(self.eng.lib.mdc_layout_set_gather(self.eng.plan(), _lib.ptr(self.send)), "mdc_layout_set_gather")
+
+    def step(self, temps) -> None:
+        self.eng.run(temps, use_graph=True)
+        self.dist.all_gather_into_tensor(self.recv, self.send, group=self.group)
+        _lib.check(self.eng.lib.mdc_layout_scatter(self.eng.plan(), _lib.ptr(self.recv), self.chunk,
+                                                   _lib.stream_ptr()), "mdc_layout_scatter")
 
 
 class P2PLayout:

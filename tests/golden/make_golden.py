@@ -87,7 +87,32 @@ def params_dict(p):
     )
 
 
+TRAJ_PAIRS = (0, 1, 2, 3, 4, 49, 99, 199, 299, 399, 498)
+
+
+def make_traj():
+    """g10k_traj.npz: the reference's own 500-step layout_run at config 2
+    (10000 x 16, seed 2 -- the g10k scene, same mesh), keeping the state pairs
+    (k, k+1) for k in TRAJ_PAIRS (SURVEY.md §8c(i) teacher-forced parity)."""
+    R = load_reference()
+    X = gmm(10000, 16, 2)
+    keep = set(TRAJ_PAIRS) | {k + 1 for k in TRAJ_PAIRS}
+    ds, model, cloud, mesh, params, state, states, temps = scene(R, X, 0, 500, keep)
+    g10k = np.load(os.path.join(HERE, "g10k.npz"))
+    for k, v in mesh_arrays(mesh).items():
+        assert np.array_equal(g10k[k], v), f"mesh differs from g10k.npz: {k}"
+    iters = np.array(sorted(keep))
+    out = dict(state_iters=iters, states=np.stack([states[k] for k in iters]),
+               temps=np.array([temps[k] for k in iters]), pairs=np.array(TRAJ_PAIRS),
+               final=state.relaxed_pos, final_temp=np.float64(state.temperature))
+    path = os.path.join(HERE, "g10k_traj.npz")
+    np.savez_compressed(path, **out)
+    print(f"wrote {path} ({os.path.getsize(path) / 1024:.0f} KiB)")
+
+
 def main():
+    if "--traj" in sys.argv:
+        return make_traj()
     R = load_reference()
     F, Rn, L, B, C = R["field"], R["render"], R["layout"], R["bhtree"], R["cli"]
     out = {}

@@ -249,3 +249,45 @@ def test_teacher_forced_at_bench_scale():
         got = eng.pos.cpu().numpy()
         ref = O.layout_step(states[k], mesh.csr_offsets, mesh.csr_targets, mesh.triangles, p, float(temps[k]))
         assert normwise(got, ref) <= TF_TOL, (k, normwise(got, ref))
+
+
+@pytest.fixture(scope="module")
+def g10k_traj():
+    from conftest import load_golden
+
+    return load_golden("g10k_traj")
+
+
+def test_teacher_forced_500_step_reference_trajectory(g10k, g10k_traj):
+    """SURVEY.md §8c(i) at config 2: the reference's own 500-step layout_run
+    (layout.py:298-302, tests/golden/make_golden.py --traj) -- the GPU step
+    applied to reference state k matches reference state k+1 (<= 1e-12
+    normwise) for k in {0..4, 49, 99, 199, 299, 399, 498}, with the exact
+    temperature; and the 500-step temperature is lambda^500 t_i."""
+    m = golden_mesh(g10k)
+    p = _params(g10k, iterations=500)
+    its = list(g10k_traj["state_iters"])
+    st, T = g10k_traj["states"], g10k_traj["temps"]
+    worst = {}
+    for k in g10k_traj["pairs"]:
+        a, b = its.index(k), its.index(k + 1)
+        m.current_pos = st[a].copy()
+        nxt = L.layout_step(L.LayoutState(m, int(k), float(T[a]), st[a]), p)
+        worst[int(k)] = normwise(nxt.relaxed_pos, st[b])
+        assert nxt.temperature == T[b]
+    print("teacher-forced 500-step trajectory:", worst)
+    assert max(worst.values()) <= TF_TOL, worst
+    temps = L.temperature_schedule(p.initial_temp, p.decay_lambda, 500)
+    assert float(temps[-1]) * p.decay_lambda == pytest.approx(float(g10k_traj["final_temp"]), rel=1e-12)
+
+
+def test_free_running_5_steps_config2(g10k, g10k_traj):
+    """SURVEY.md §8c(ii) at config 2 (10k): 5 free-running GPU steps from the
+    reference's state 0 against the reference's state 5, <= 1e-9 normwise."""
+    m = golden_mesh(g10k)
+    p = _params(g10k, iterations=5)
+    its = list(g10k_traj["state_iters"])
+    state = L.layout_run(m, p)
+    err = normwise(state.relaxed_pos, g10k_traj["states"][its.index(5)])
+    print("free-running 5 steps at 10k:", err)
+    assert err <= FREE_TOL

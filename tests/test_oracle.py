@@ -97,3 +97,19 @@ def test_oracle_bh_vs_exact_within_5_percent(g2k):
     ex = g2k["bh_exact_0"]
     rel = np.linalg.norm(bh - ex, axis=1) / np.linalg.norm(ex, axis=1)
     assert rel.max() < 0.05
+
+
+def test_oracle_pinned_to_500_step_reference_trajectory(g10k):
+    """The oracle's step against the reference's own 500-step config-2
+    trajectory (tests/golden/g10k_traj.npz) at an early, a middle and the last
+    stored pair (the GPU test checks every stored pair)."""
+    from conftest import load_golden
+
+    t = load_golden("g10k_traj")
+    p = layout_params(g10k)
+    its = list(t["state_iters"])
+    for k in (0, 249 if 249 in its else 199, 498):
+        a, b = its.index(k), its.index(k + 1)
+        nxt = O.layout_step(t["states"][a], g10k["csr_offsets"], g10k["csr_targets"], g10k["triangles"], p,
+                            t["temps"][a])
+        assert normwise(nxt, t["states"][b]) <= 1e-13, k
