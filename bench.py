@@ -50,7 +50,7 @@ def gmm(n, d, seed):
 
 def workload_name(cfg):
     return (f"config{cfg['id']}: affine MLS alpha=1.5 fp32, {cfg['n']} points x {cfg['d']} dims, "
-            f"{cfg['W']}x{cfg['H']}; layout {cfg['iters']} iterations")
+            f"{cfg['W']}x{cfg['H']}, fused bands + RGBA8 band shading + snap; layout {cfg['iters']} iterations")
 
 
 # ---------------------------------------------------------------------------
@@ -196,6 +196,25 @@ def laid_out_positions(cfg, mesh):
     except (OSError, KeyError):
         pass
     return {0: mesh.original_pos}, mesh.original_pos
+
+
+def build_scene(cfg, device_pca=True):
+    from paper_1408_0677_b200 import dataset as D
+    from paper_1408_0677_b200 import mesh as M
+    from paper_1408_0677_b200 import projection as P
+
+    X = gmm(cfg["n"], cfg["d"], cfg["seed"])
+    ds = D.normalize(D.Dataset(names=[f"d{i}" for i in range(cfg["d"])], data=X))
+    if device_pca:
+        model, cloud = P.pca_project(ds)
+        positions = cloud.positions
+    else:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import oracle as O
+        positions = O.pca_project(ds.data)[3]
+    mesh = M.delaunay(positions, seed=0)
+    raw = np.column_stack([ds.raw_column(nm) for nm in ds.names])
+    return ds, mesh, raw
 
 
 def run_reference(args, cfg, rank):
@@ -456,9 +475,14 @@ def main():
     rows = r1 - r0
     out = torch.empty((d, rows, W), dtype=torch.float32, device=dev)
     bands = torch.empty((d, rows, W), dtype=torch.int32, device=dev)
+    # north_star (3): band shading fused into the MLS epilogue (RGBA8 per pixel-channel)
+    from paper_1408_0677_b200.render import DEFAULT_COLORMAP
+
+    rgba = torch.empty((d, rows, W), dtype=torch.int32, device=dev)
+    pal_t = torch.as_tensor(F.palette_rgba8(DEFAULT_COLORMAP).view(np.int32)).to(dev)
     sp_t = torch.as_tensor(spacing).to(dev)
     nonfinite = torch.zeros((), dtype=torch.int32, device=dev)
-    a = prob.args(out, (rows * W, W, 1), r0, r1, bands, (rows * W, W), sp_t, nonfinite)
+    a = prob.args(out, (rows * W, W, 1), r0, r1, bands, (rows * W, W), sp_t, nonfinite, rgba=rgba, palette=pal_t)
     snap_ws = F._snap_workspace(int(lib.mdc_snap_workspace_bytes(W, rows)), dev)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
     ctrl = [prob.pc_t, prob.q_t, prob.pos_t, prob.tvals_t]
@@ -540,14 +564,14 @@ def main():
     achieved = 2 * fma_instr / sec / 1e12          # FP32-pipe FLOP-equivalents (FMA-pipe op = 2)
     peak = peaks["fp32"] / 1e12
     tf32_peak = 0.5 * _measured_bf16_tflops()       # dense tf32 = 1/2 bf16 (measured bf16, MEASURED_PEAKS.json)
-    traffic, alg_bytes = _kernel_traffic(cfg, W, H, d, use_tc), pairs // cfg["n"] * d * 8 + cfg["n"] * (16 + 4 * d)
+    traffic, alg_bytes = _kernel_traffic(cfg, W, H, d, use_tc), pairs // cfg["n"] * d * 12 + cfg["n"] * (16 + 4 * d)
     roofline = {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak, "traffic": traffic,
                 "traffic_def": "dram__bytes_read.sum + dram__bytes_write.sum of one launch from the committed "
                                "ncu --set full capture of this workload (profiles/r01_mls_tc_kernel_traffic.json)",
                 "algorithmic_bytes": alg_bytes,
-                "algorithmic_bytes_def": "fp32 field + int32 bands per pixel-channel, + controls (16 B) and "
-                                         "fp32 targets per control",
+                "algorithmic_bytes_def": "fp32 field + int32 bands + RGBA8 band shading per pixel-channel, + "
+                                         "controls (16 B) and fp32 targets per control",
                 "kernel": kname, "kernel_ms": kernel_ms,
                 "achieved_def": "FP32-pipe lane-ops executed x 2 (one FMA-pipe lane-op = one FFMA = 2 FLOP) / kernel time",
                 "peak_source": "measured FFMA microbenchmark (mdc_peak_ffma), this run",
@@ -649,6 +673,9 @@ def run_e2e(args, positions, raw, spacing, W, H, d, r0, r1, dev, world):
     pin_pos = torch.from_numpy(np.ascontiguousarray(positions)).pin_memory()
     pin_raw = torch.from_numpy(np.ascontiguousarray(raw)).pin_memory()
     host_out = torch.empty((d, rows, W), dtype=torch.float32).pin_memory()
+    host_rgba = torch.empty((d, rows, W, 4), dtype=torch.uint8).pin_memory()
+    from paper_1408_0677_b200.render import DEFAULT_COLORMAP
+
     mp = F.MlsParams("affine")
     ne = max(1, min(args.steps, 3))
     h2d = [0]
@@ -657,7 +684,8 @@ def run_e2e(args, positions, raw, spacing, W, H, d, r0, r1, dev, world):
         # public API with host buffers in and out: the frame's row bands are
         # copied back while the next band computes (compute_fields_to_host)
         h2d[0] = F.compute_fields_to_host(pin_pos, pin_raw, mp, W, H, host_out,
-                                          row_range=(r0, r1), dtype="f32", band_spacing=spacing)
+                                          row_range=(r0, r1), dtype="f32", band_spacing=spacing,
+                                          rgba_out=host_rgba, colormap=DEFAULT_COLORMAP)
 
     e2e_step()
     torch.cuda.synchronize()
@@ -671,7 +699,7 @@ def run_e2e(args, positions, raw, spacing, W, H, d, r0, r1, dev, world):
     if world > 1:
         dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
     return {"value": W * H * d / (e_ms.item() * 1e-3) / 1e6, "unit": UNIT,
-            "h2d_bytes_per_step": int(h2d[0]), "d2h_bytes_per_step": int(host_out.numel() * 4),
+            "h2d_bytes_per_step": int(h2d[0]), "d2h_bytes_per_step": int(host_out.numel() * 4 + host_rgba.numel()),
             "ms_per_step": e_ms.item(), "timing": "wall clock, synchronized, max over ranks"}
 
 

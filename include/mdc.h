@@ -104,6 +104,13 @@ typedef struct MdcMlsArgs {
     int32_t flags;
     void *workspace;
     size_t workspace_bytes;
+    /* Fused band shading (render.py:142-148 render_discrete of channel k's
+     * single-dimension field): optional uint32 RGBA8 (little-endian R,G,B,A
+     * bytes) per pixel-channel with the bands' strides,
+     * rgba = palette[floor(f / spacing[k]) mod palette_n]; needs spacing. */
+    uint32_t *rgba;
+    const uint32_t *palette;
+    int32_t palette_n;
 } MdcMlsArgs;
 
 #define MDC_FLAG_NO_TC 1

@@ -46,6 +46,7 @@ class MdcMlsArgs(ctypes.Structure):
         ("flags", _c_i32),
         ("workspace", _vp),
         ("workspace_bytes", ctypes.c_size_t),
+        ("rgba", _vp), ("palette", _vp), ("palette_n", _c_i32),
     ]
 
 
@@ -192,3 +193,28 @@ def stream_ptr(stream=None) -> int:
 
 def ptr(t) -> int | None:
     return None if t is None else int(t.data_ptr())
+
+
+class nvtx:
+    """NVTX range around a host-side stage (SURVEY.md §5 tracing): shows up
+    in nsys / ncu --nvtx timelines; a no-op where NVTX is unavailable."""
+
+    def __init__(self, name: str):
+        self.name = name
+
+    def __enter__(self):
+        try:
+            import torch
+
+            torch.cuda.nvtx.range_push(self.name)
+            self.pushed = True
+        except Exception:
+            self.pushed = False
+        return self
+
+    def __exit__(self, *exc):
+        if self.pushed:
+            import torch
+
+            torch.cuda.nvtx.range_pop()
+        return False

@@ -289,9 +289,7 @@ __global__ void __launch_bounds__(NT, MDC_MLS_MINB) mls_kernel(KArgs a) {
                     T f = to_t<T>((tacc[r][k] + (double)acc[r][k]) + a.qm[ch]);
                     reinterpret_cast<T *>(a.out)[ch * a.out_cs + lr * a.out_rs + col * a.out_ps] = f;
                     if (!isfinite((double)f)) bad[r] = true;
-                    if (a.bands)
-                        a.bands[ch * a.band_cs + lr * a.band_rs + col] =
-                            (int32_t)floor((double)f / a.spacing[ch]);
+                    store_band(a, ch, lr, col, (double)f);
                 }
             }
         }
@@ -384,9 +382,7 @@ __global__ void __launch_bounds__(NT, MDC_MLS_MINB) mls_kernel(KArgs a) {
                     T f = to_t<T>((v + (tacc[r][k] + (double)acc[r][k]) / (tsw[r] + (double)sw[r])) + a.qm[ch]);
                     reinterpret_cast<T *>(a.out)[ch * a.out_cs + lr * a.out_rs + col * a.out_ps] = f;
                     if (!isfinite((double)f)) bad[r] = true;
-                    if (a.bands)
-                        a.bands[ch * a.band_cs + lr * a.band_rs + col] =
-                            (int32_t)floor((double)f / a.spacing[ch]);
+                    store_band(a, ch, lr, col, (double)f);
                 }
             }
         }
@@ -507,10 +503,8 @@ __global__ void __launch_bounds__(NT, MDC_MLS_MINB) mls_kernel(KArgs a) {
             T *o = reinterpret_cast<T *>(a.out);
             o[lr * a.out_rs + col * a.out_ps] = f0;
             o[a.out_cs + lr * a.out_rs + col * a.out_ps] = f1;
-            if (a.bands) {
-                a.bands[lr * a.band_rs + col] = (int32_t)floor((double)f0 / a.spacing[0]);
-                a.bands[a.band_cs + lr * a.band_rs + col] = (int32_t)floor((double)f1 / a.spacing[1]);
-            }
+            store_band(a, 0, lr, col, (double)f0);
+            store_band(a, 1, lr, col, (double)f1);
             if (!isfinite((double)f0) || !isfinite((double)f1)) ++cnt_bad;
         }
         if (a.nonfinite && cnt_bad) atomicAdd(a.nonfinite, cnt_bad);
@@ -591,6 +585,9 @@ struct SnapArgs {
     int64_t band_cs, band_rs;
     const double *spacing;
     int32_t *nonfinite;
+    uint32_t *rgba;
+    const uint32_t *palette;
+    int32_t palette_n;
     unsigned long long *best_d2;
     unsigned *best_idx;
 };
@@ -639,7 +636,7 @@ __global__ void snap_kernel(SnapArgs a) {
                         if (!isfinite(o[off])) was_bad = true;
                         o[off] = v;
                     }
-                    if (a.bands) a.bands[k * a.band_cs + lr * a.band_rs + xx] = (int32_t)floor(v / a.spacing[k]);
+                    store_band(a, k, lr, xx, v);
                 }
                 if (was_bad && a.nonfinite) atomicSub(a.nonfinite, 1);
             } else {
@@ -690,6 +687,8 @@ extern "C" int mdc_mls_field(const MdcMlsArgs *a, void *stream) {
     MDC_REQUIRE(a->variant != MDC_MEAN || a->axis != nullptr, "mean variant needs axis[]");
     MDC_REQUIRE(a->pc && a->q && a->qm && a->out, "null device pointer");
     MDC_REQUIRE(a->bands == nullptr || a->spacing != nullptr, "bands need spacing[]");
+    MDC_REQUIRE(a->rgba == nullptr || (a->spacing != nullptr && a->palette != nullptr && a->palette_n > 0),
+                "rgba shading needs spacing[] and a non-empty palette");
     size_t es = a->dtype == MDC_F32 ? 4 : 8;
     int chunk = required_chunk(a->dtype, a->d, a->variant);
     int64_t need = ((a->d + chunk - 1) / chunk) * chunk;
@@ -730,6 +729,9 @@ extern "C" int mdc_mls_field(const MdcMlsArgs *a, void *stream) {
     k.band_rs = a->band_rs;
     k.spacing = a->spacing;
     k.nonfinite = a->nonfinite;
+    k.rgba = a->rgba;
+    k.palette = a->palette;
+    k.palette_n = a->palette_n;
     if (k.npix == 0) return MDC_OK;
     cudaStream_t s = (cudaStream_t)stream;
     if (tc_eligible(a) && a->workspace && a->workspace_bytes >= tc_ws_bytes(a) && ((uintptr_t)a->workspace % 16) == 0)
@@ -756,6 +758,8 @@ extern "C" int mdc_mls_snap(const MdcMlsArgs *a, const double *pos, const double
                             void *workspace, void *stream) {
     MDC_REQUIRE(a && pos && tvals && workspace, "null pointer");
     MDC_REQUIRE(eps > 0, "eps must be positive");
+    MDC_REQUIRE(a->rgba == nullptr || (a->spacing != nullptr && a->palette != nullptr && a->palette_n > 0),
+                "rgba shading needs spacing[] and a non-empty palette");
     MDC_REQUIRE(0 <= a->row0 && a->row0 <= a->row1 && a->row1 <= a->height, "bad row band");
     SnapArgs s;
     s.width = a->width;
@@ -784,6 +788,9 @@ extern "C" int mdc_mls_snap(const MdcMlsArgs *a, const double *pos, const double
     s.band_rs = a->band_rs;
     s.spacing = a->spacing;
     s.nonfinite = a->nonfinite;
+    s.rgba = a->rgba;
+    s.palette = a->palette;
+    s.palette_n = a->palette_n;
     int64_t npix = (int64_t)(a->row1 - a->row0) * a->width;
     s.best_d2 = reinterpret_cast<unsigned long long *>(workspace);
     s.best_idx = reinterpret_cast<unsigned *>(s.best_d2 + npix);

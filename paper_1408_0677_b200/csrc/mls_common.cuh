@@ -144,7 +144,26 @@ struct KArgs {
     int64_t band_cs, band_rs;
     const double *spacing;
     int32_t *nonfinite;
+    uint32_t *rgba;
+    const uint32_t *palette;
+    int32_t palette_n;
 };
+
+// Band epilogue (render.py:135-139) fused with the discrete shading
+// (render.py:142-148): band = floor(f / s_k) and, when requested, the RGBA8
+// colour palette[band mod n] (non-negative modulo, as np.mod).
+template <typename A>
+__device__ __forceinline__ void store_band(const A &a, int ch, int64_t lr, int64_t col, double f) {
+    if (!a.bands && !a.rgba) return;
+    const int32_t b = (int32_t)floor(f / a.spacing[ch]);
+    const int64_t off = ch * a.band_cs + lr * a.band_rs + col;
+    if (a.bands) a.bands[off] = b;
+    if (a.rgba) {
+        int m = b % a.palette_n;
+        if (m < 0) m += a.palette_n;
+        a.rgba[off] = a.palette[m];
+    }
+}
 
 // Pixel centre (global linear pixel index p) in the globally-centred frame,
 // bit-identical to `xs.ravel() - pm[0]` / `ys.ravel() - pm[1]` of

@@ -63,6 +63,13 @@ constexpr int P1U = MDC_TC_P1STATIC > 0 ? MDC_TC_P1STATIC : 1;
 constexpr int A_SBO = (KT / 4) * 128;  // bytes between 8-row core-matrix groups of a Q tile
 static_assert(KT % 8 == 0 && XYR % KT == 0, "K tiles are whole tf32 K steps and tile a staging round");
 constexpr int NC_MAX = 32;             // channels per pass-2 chunk (fp64 totals in shared memory)
+#ifndef MDC_TC_WIDE
+#define MDC_TC_WIDE 64  // d > 32: 64-channel chunks at 2 CTAs per SM (0: 32-channel chunks, 4 CTAs per SM)
+#endif
+// CTAs per SM the register allocation targets: 64-channel chunks need 64 KB
+// of fp64 totals per CTA, so two CTAs share an SM.
+template <int NC>
+constexpr int minb() { return NC > NC_MAX ? 2 : MDC_TC_MINB; }
 
 // ---------------------------------------------------------------------------
 // Q -> tiled core-matrix image, hi/lo split.  img[(chunk * ntiles + t)][hi|lo]
@@ -104,7 +111,7 @@ __device__ __forceinline__ void compute_bar_sync() {  // named barrier over the 
 }
 
 template <int AM, int NC>
-__global__ void __launch_bounds__(THREADS, MDC_TC_MINB) mls_tc_kernel(KArgs a, const float *qimg, int64_t ntiles, int nchunk) {
+__global__ void __launch_bounds__(THREADS, minb<NC>()) mls_tc_kernel(KArgs a, const float *qimg, int64_t ntiles, int nchunk) {
     constexpr int B_HALF = NC * KT * 4;
     constexpr int B_STAGE = 2 * B_HALF;
     // TMEM columns: accumulators (NC) then the G ring ({hi, lo} x KT per stage)
@@ -393,8 +400,7 @@ __global__ void __launch_bounds__(THREADS, MDC_TC_MINB) mls_tc_kernel(KArgs a, c
                         float f = (float)(tot[c * TPB + tid] + a.qm[ch]);
                         reinterpret_cast<float *>(a.out)[ch * a.out_cs + lr * a.out_rs + col * a.out_ps] = f;
                         if (!isfinite(f)) bad = true;
-                        if (a.bands)
-                            a.bands[ch * a.band_cs + lr * a.band_rs + col] = (int32_t)floor((double)f / a.spacing[ch]);
+                        store_band(a, ch, lr, col, (double)f);
                     }
                 }
             }
@@ -671,8 +677,7 @@ __global__ void __launch_bounds__(THREADS, 2) mls_tc1_kernel(KArgs a, const floa
                         float f = (float)(F + a.qm[ch]);
                         reinterpret_cast<float *>(a.out)[ch * a.out_cs + lr * a.out_rs + col * a.out_ps] = f;
                         if (!isfinite(f)) bad = true;
-                        if (a.bands)
-                            a.bands[ch * a.band_cs + lr * a.band_rs + col] = (int32_t)floor((double)f / a.spacing[ch]);
+                        store_band(a, ch, lr, col, (double)f);
                     }
                 }
             }
@@ -696,7 +701,7 @@ static size_t tc_smem_bytes() {
            2 * XYR * sizeof(float2) + 2 * STAGES * sizeof(uint64_t) + 16;
 }
 
-static int pick_nc(int d) { return d <= 16 ? 16 : NC_MAX; }
+static int pick_nc(int d) { return d <= 16 ? 16 : (d <= NC_MAX || !MDC_TC_WIDE ? NC_MAX : MDC_TC_WIDE); }
 
 }  // namespace tc
 
@@ -735,6 +740,9 @@ template <int AM>
 static int launch_tc_am(const KArgs &k, void *ws, cudaStream_t s) {
     switch (tc::pick_nc(k.d)) {
         case 16: return launch_tc_nc<AM, 16>(k, ws, s);
+#if MDC_TC_WIDE
+        case MDC_TC_WIDE: return launch_tc_nc<AM, MDC_TC_WIDE>(k, ws, s);
+#endif
         default: return launch_tc_nc<AM, tc::NC_MAX>(k, ws, s);
     }
 }

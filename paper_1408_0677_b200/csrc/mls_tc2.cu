@@ -531,8 +531,7 @@ __global__ void __launch_bounds__(THREADS, 1) mls_tc2_kernel(KArgs a, const floa
                         const float f = (float)(F + a.qm[ch]);
                         reinterpret_cast<float *>(a.out)[ch * a.out_cs + lr * a.out_rs + col * a.out_ps] = f;
                         if (!isfinite(f)) bad = true;
-                        if (a.bands)
-                            a.bands[ch * a.band_cs + lr * a.band_rs + col] = (int32_t)floor((double)f / a.spacing[ch]);
+                        store_band(a, ch, lr, col, (double)f);
                     }
                 }
             }

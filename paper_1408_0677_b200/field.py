@@ -384,6 +384,7 @@ class FieldBlock:
     row1: int
     nonfinite: torch.Tensor         # () int32 device counter
     h2d_bytes: int = 0              # host->device bytes this call uploaded
+    rgba: torch.Tensor | None = None  # (d, rows, W, 4) uint8: discrete band shading per channel
 
     def check_finite(self) -> None:
         if int(self.nonfinite.item()) != 0:
@@ -469,10 +470,11 @@ class MlsProblem:
         self.qm_t = torch.empty(d, dtype=torch.float64, device=dev)
         wsb = int(lib.mdc_mls_prepare_workspace_bytes(d))
         ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
-        _lib.check(lib.mdc_mls_prepare(n, d, _lib.ptr(self.pos_t), _lib.ptr(self.tvals_t), self.vcode, self.dcode,
-                                       _lib.ptr(self.axis_t), ldq, _lib.ptr(self.pc_t), _lib.ptr(self.q_t),
-                                       _lib.ptr(pm_t), _lib.ptr(self.qm_t), _lib.ptr(ws), wsb, _lib.stream_ptr()),
-                   "mdc_mls_prepare")
+        with _lib.nvtx("mls.prepare"):
+            _lib.check(lib.mdc_mls_prepare(n, d, _lib.ptr(self.pos_t), _lib.ptr(self.tvals_t), self.vcode,
+                                           self.dcode, _lib.ptr(self.axis_t), ldq, _lib.ptr(self.pc_t),
+                                           _lib.ptr(self.q_t), _lib.ptr(pm_t), _lib.ptr(self.qm_t), _lib.ptr(ws), wsb,
+                                           _lib.stream_ptr()), "mdc_mls_prepare")
         self.pm = pm_t.cpu().numpy()  # the kernels take the frame centre by value
         self.h2d_bytes = sum(t.numel() * t.element_size() for t in (self.pos_t, self.tvals_t, self.axis_t))
         self.ldq = ldq
@@ -480,7 +482,7 @@ class MlsProblem:
         self._ws = None
 
     def args(self, out, out_strides, row0, row1, bands=None, band_strides=(0, 0), spacing=None,
-             nonfinite=None) -> _lib.MdcMlsArgs:
+             nonfinite=None, rgba=None, palette=None) -> _lib.MdcMlsArgs:
         t = self.transform
         sx, sy = t.units_per_px
         a = _lib.MdcMlsArgs()
@@ -497,6 +499,9 @@ class MlsProblem:
         a.band_cs, a.band_rs = (int(s) for s in band_strides)
         a.spacing = _lib.ptr(spacing)
         a.nonfinite = _lib.ptr(nonfinite)
+        a.rgba = _lib.ptr(rgba)
+        a.palette = _lib.ptr(palette)
+        a.palette_n = 0 if palette is None else int(palette.numel())
         a.flags = self.flags
         need = int(self.lib.mdc_mls_workspace_bytes(ctypes.byref(a)))
         if need:
@@ -507,26 +512,40 @@ class MlsProblem:
 
     def run(self, a: _lib.MdcMlsArgs, snap: bool = True) -> None:
         stream = _lib.stream_ptr()
-        _lib.check(self.lib.mdc_mls_field(ctypes.byref(a), stream), "mdc_mls_field")
+        with _lib.nvtx(f"mls.field rows {a.row0}-{a.row1}"):
+            _lib.check(self.lib.mdc_mls_field(ctypes.byref(a), stream), "mdc_mls_field")
         if snap:
             rows = a.row1 - a.row0
-            with _ws_lock("snap", self.device):
+            with _lib.nvtx("mls.snap"), _ws_lock("snap", self.device):
                 ws = _snap_workspace(int(self.lib.mdc_snap_workspace_bytes(self.width, rows)), self.device)
                 _lib.check(self.lib.mdc_mls_snap(ctypes.byref(a), _lib.ptr(self.pos_t), _lib.ptr(self.tvals_t),
                                                  ctypes.c_double(self.eps), _lib.ptr(ws), stream),
                            "mdc_mls_snap")
 
 
+def palette_rgba8(colormap) -> np.ndarray:
+    """render.py:142-148's colour table as packed RGBA8 words (the bytes
+    render_discrete writes: clip(rint(255 * rgba)))."""
+    from .render import _rgba
+
+    tab = np.array([_rgba(c) for c in colormap], dtype=np.float64)
+    px = np.clip(np.rint(tab * 255.0), 0, 255).astype(np.uint8)
+    return px.reshape(-1, 4).copy().view(np.uint32).reshape(-1)
+
+
 def compute_fields(positions, targets, params: MlsParams, width: int, height: int,
                    row_range=None, dtype="f32", band_spacing=None, axis=None,
-                   problem: MlsProblem | None = None, tensor_cores: bool = True) -> FieldBlock:
+                   problem: MlsProblem | None = None, tensor_cores: bool = True, colormap=None) -> FieldBlock:
     """Fused d-channel MLS: every column of ``targets`` (n, d) is one field.
 
     Channel k equals channel 0 of the reference's ``compute_field`` for the
     single-dimension target (targets[:, k], 0) -- exactly what the reference
     CLI renders once per dimension (cli.py:143-165) -- for mean and affine;
     rigid takes d == 2 and matches the reference's two channels.
-    ``band_spacing`` (scalar or (d,)) fuses render._band_indices.
+    ``band_spacing`` (scalar or (d,)) fuses render._band_indices; with
+    ``colormap`` (a list of colours, e.g. render.DEFAULT_COLORMAP) the same
+    epilogue also writes each channel's discrete band shading as RGBA8
+    (render.py:142-148 for that channel's single-dimension field).
     Returns a FieldBlock of device tensors (rows [row0, row1) only).
     """
     if params.variant == "linear":
@@ -544,12 +563,20 @@ def compute_fields(positions, targets, params: MlsParams, width: int, height: in
         sp = np.broadcast_to(np.asarray(band_spacing, dtype=np.float64), (prob.d,)).copy()
         spacing_t = _h2d(sp, dev)
         bands = torch.empty((prob.d, rows, width), dtype=torch.int32, device=dev)
+    rgba = pal_t = None
+    if colormap is not None:
+        if spacing_t is None:
+            raise ValueError("colormap shading needs band_spacing")
+        pal_t = _h2d(palette_rgba8(colormap).view(np.int32), dev)
+        rgba = torch.empty((prob.d, rows, width), dtype=torch.int32, device=dev)
     nonfinite = torch.zeros((), dtype=torch.int32, device=dev)
-    a = prob.args(out, (rows * width, width, 1), r0, r1, bands, (rows * width, width), spacing_t, nonfinite)
+    a = prob.args(out, (rows * width, width, 1), r0, r1, bands, (rows * width, width), spacing_t, nonfinite,
+                  rgba=rgba, palette=pal_t)
     prob.run(a)
     h2d = 0 if problem is not None else prob.h2d_bytes + (spacing_t.numel() * 8 if spacing_t is not None else 0)
     return FieldBlock(values=out, bands=bands, transform=prob.transform, row0=r0, row1=r1,
-                      nonfinite=nonfinite, h2d_bytes=h2d)
+                      nonfinite=nonfinite, h2d_bytes=h2d,
+                      rgba=None if rgba is None else rgba.view(torch.uint8).view(prob.d, rows, width, 4))
 
 
 def plan_row_bands(r0: int, r1: int, nbands: int = 4) -> list[tuple[int, int]]:
@@ -568,9 +595,12 @@ def plan_row_bands(r0: int, r1: int, nbands: int = 4) -> list[tuple[int, int]]:
 
 def compute_fields_to_host(positions, targets, params: MlsParams, width: int, height: int,
                            out: torch.Tensor, bands_out: torch.Tensor | None = None, row_range=None,
-                           dtype="f32", band_spacing=None, nbands: int = 4, tensor_cores: bool = True) -> int:
+                           dtype="f32", band_spacing=None, nbands: int = 4, tensor_cores: bool = True,
+                           rgba_out: torch.Tensor | None = None, colormap=None) -> int:
     """``compute_fields`` with the result delivered into HOST memory: ``out``
-    (d, rows, W) pinned float tensor (and optional int32 ``bands_out``).
+    (d, rows, W) pinned float tensor (and optional int32 ``bands_out``, and
+    with ``colormap`` the fused band shading into ``rgba_out``: (d, rows, W,
+    4) uint8).
 
     The frame is evaluated in row bands (``plan_row_bands``); each band's
     device->host copy runs on a side stream while the next band computes (two
@@ -592,6 +622,11 @@ def compute_fields_to_host(positions, targets, params: MlsParams, width: int, he
     if bands_out is not None and (tuple(bands_out.shape) != (d, rows, width) or bands_out.is_cuda
                                   or bands_out.dtype != torch.int32 or not bands_out.is_contiguous()):
         raise ValueError(f"bands_out must be a contiguous host int32 tensor of shape {(d, rows, width)}")
+    if (rgba_out is None) != (colormap is None):
+        raise ValueError("rgba_out and colormap go together")
+    if rgba_out is not None and (tuple(rgba_out.shape) != (d, rows, width, 4) or rgba_out.is_cuda
+                                 or rgba_out.dtype != torch.uint8 or not rgba_out.is_contiguous()):
+        raise ValueError(f"rgba_out must be a contiguous host uint8 tensor of shape {(d, rows, width, 4)}")
     dev = prob.device
     plan = plan_row_bands(r0, r1, nbands)
     step = max(b1 - b0 for b0, b1 in plan)
@@ -599,10 +634,16 @@ def compute_fields_to_host(positions, targets, params: MlsParams, width: int, he
     if band_spacing is not None:
         sp = np.broadcast_to(np.asarray(band_spacing, dtype=np.float64), (d,)).copy()
         spacing_t = _h2d(sp, dev)
+    if colormap is not None and spacing_t is None:
+        raise ValueError("colormap shading needs band_spacing")
+    pal_t = _h2d(palette_rgba8(colormap).view(np.int32), dev) if colormap is not None else None
+    rgba_host = rgba_out.view(torch.int32).view(d, rows, width) if rgba_out is not None else None
     nonfinite = torch.zeros((), dtype=torch.int32, device=dev)
     vbuf = [torch.empty((d, step, width), dtype=prob.tdtype, device=dev) for _ in range(2)]
     bbuf = [torch.empty((d, step, width), dtype=torch.int32, device=dev) for _ in range(2)] \
         if bands_out is not None else [None, None]
+    cbuf = [torch.empty((d, step, width), dtype=torch.int32, device=dev) for _ in range(2)] \
+        if rgba_out is not None else [None, None]
     compute = torch.cuda.current_stream(dev)
     copy = torch.cuda.Stream(device=dev)
     done = [None, None]  # copy-finished events per buffer
@@ -613,13 +654,16 @@ def compute_fields_to_host(positions, targets, params: MlsParams, width: int, he
             compute.wait_event(done[k])
         v = vbuf[k][:, :n_rows]
         bt = bbuf[k][:, :n_rows] if bbuf[k] is not None else None
-        a = prob.args(v, (step * width, width, 1), b0, b1, bt, (step * width, width), spacing_t, nonfinite)
+        ct = cbuf[k][:, :n_rows] if cbuf[k] is not None else None
+        # the shading shares the band strides
+        a = prob.args(v, (step * width, width, 1), b0, b1, bt, (step * width, width), spacing_t, nonfinite,
+                      rgba=ct, palette=pal_t)
         prob.run(a)
         ready = torch.cuda.Event()
         ready.record(compute)
         copy.wait_event(ready)
         # one strided async copy per plane set: d rows of (n_rows x W) elements
-        for src, dst in ((v, out), (bt, bands_out)):
+        for src, dst in ((v, out), (bt, bands_out), (ct, rgba_host)):
             if src is None:
                 continue
             es = src.element_size()
@@ -631,8 +675,9 @@ def compute_fields_to_host(positions, targets, params: MlsParams, width: int, he
         ev.record(copy)
         done[k] = ev
         vbuf[k].record_stream(copy)
-        if bbuf[k] is not None:
-            bbuf[k].record_stream(copy)
+        for buf in (bbuf[k], cbuf[k]):
+            if buf is not None:
+                buf.record_stream(copy)
     copy.synchronize()
     if int(nonfinite.item()) != 0:
         raise FieldError("field evaluation produced non-finite coordinates")

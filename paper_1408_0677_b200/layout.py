@@ -167,8 +167,9 @@ class LayoutEngine:
         else:
             self.temps[:k].copy_(torch.as_tensor(np.asarray(temps, dtype=np.float64)))
         h = self.plan(debug)
-        _lib.check(self.lib.mdc_layout_steps(h, k, _lib.ptr(self.temps), int(use_graph and not debug),
-                                             _lib.stream_ptr()), "mdc_layout_steps")
+        with _lib.nvtx(f"layout.steps x{k}"):
+            _lib.check(self.lib.mdc_layout_steps(h, k, _lib.ptr(self.temps), int(use_graph and not debug),
+                                                 _lib.stream_ptr()), "mdc_layout_steps")
 
     PHASES = ("sorts", "tree", "bh_traversal", "bh_combine", "local")
 
@@ -372,7 +373,8 @@ class GatherLayout:
 
     def step(self, temps) -> None:
         self.eng.run(temps, use_graph=True)
-        self.dist.all_gather_into_tensor(self.recv, self.send, group=self.group)
+        with _lib.nvtx("layout.allgather"):
+            self.dist.all_gather_into_tensor(self.recv, self.send, group=self.group)
         _lib.check(self.eng.lib.mdc_layout_scatter(self.eng.plan(), _lib.ptr(self.recv), self.chunk,
                                                    _lib.stream_ptr()), "mdc_layout_scatter")
 

@@ -64,9 +64,10 @@ def pca_device(x: torch.Tensor):
     axes = torch.empty((2, d), dtype=torch.float64, device=dev)
     pos = torch.empty((n, 2), dtype=torch.float64, device=dev)
     ws = torch.empty(int(lib.mdc_pca_workspace_bytes(n, d)), dtype=torch.uint8, device=dev)
-    _lib.check(lib.mdc_pca(ctypes.c_int64(n), ctypes.c_int32(d), _lib.ptr(x), _lib.ptr(mean),
-                           _lib.ptr(cov), _lib.ptr(ev), _lib.ptr(axes), _lib.ptr(pos),
-                           _lib.ptr(ws), _lib.stream_ptr()), "mdc_pca")
+    with _lib.nvtx("pca"):
+        _lib.check(lib.mdc_pca(ctypes.c_int64(n), ctypes.c_int32(d), _lib.ptr(x), _lib.ptr(mean),
+                               _lib.ptr(cov), _lib.ptr(ev), _lib.ptr(axes), _lib.ptr(pos),
+                               _lib.ptr(ws), _lib.stream_ptr()), "mdc_pca")
     return mean, cov, ev, axes, pos
 
 

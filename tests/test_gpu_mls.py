@@ -239,12 +239,18 @@ def test_compute_fields_to_host_matches_device_block(c1):
     W, H = (int(v) for v in c1["field_wh"])
     raw = np.tile(c1["raw"], (1, 4))
     sp = np.linspace(0.5, 2.0, raw.shape[1])
-    blk = F.compute_fields(pos, raw, F.MlsParams("affine"), W, H, dtype="f32", band_spacing=sp)
+    from paper_1408_0677_b200.render import DEFAULT_COLORMAP
+
+    blk = F.compute_fields(pos, raw, F.MlsParams("affine"), W, H, dtype="f32", band_spacing=sp,
+                           colormap=DEFAULT_COLORMAP)
     for nb in (1, 3, 8):
         out = torch.empty((raw.shape[1], H, W), dtype=torch.float32).pin_memory()
         bands = torch.empty((raw.shape[1], H, W), dtype=torch.int32).pin_memory()
+        rgba = torch.empty((raw.shape[1], H, W, 4), dtype=torch.uint8).pin_memory()
         h2d = F.compute_fields_to_host(pos, raw, F.MlsParams("affine"), W, H, out, bands_out=bands,
-                                       dtype="f32", band_spacing=sp, nbands=nb)
+                                       dtype="f32", band_spacing=sp, nbands=nb, rgba_out=rgba,
+                                       colormap=DEFAULT_COLORMAP)
         assert h2d > 0
         assert torch.equal(out, blk.values.cpu()), nb
         assert torch.equal(bands, blk.bands.cpu()), nb
+        assert torch.equal(rgba, blk.rgba.cpu()), nb

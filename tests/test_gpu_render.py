@@ -82,3 +82,30 @@ def test_overlay_points_matches_reference_order(c1):
     ref = O.overlay_points(base.pixels, fld.transform.to_pixels(pos), 2.5)
     diff = np.abs(got.astype(int) - ref.astype(int))
     assert diff.max() <= 1 and (diff > 0).mean() <= 1e-3
+
+
+@pytest.mark.parametrize("dtype,eps", [("f64", 1e-9), ("f32", 1e-4)])
+def test_fused_band_shading_matches_reference_render_discrete(c1, dtype, eps):
+    """North-star (3): band shading fused into the MLS epilogue.  Each
+    channel's RGBA8 from compute_fields(..., colormap=...) equals the
+    reference's render_discrete of that single-dimension field
+    (render.py:142-148: table[mod(floor(u / s), 11)] -> clip(rint(255 x))),
+    built here from the reference's own golden band indices; exact except
+    within eps of a band boundary (the snap pass restamps snapped pixels)."""
+    pos = c1["field_positions"]
+    W, H = (int(v) for v in c1["field_wh"])
+    names = [f"affine_dim{k}" for k in range(4)]
+    tv = np.column_stack([c1[f"targets_{nm}"][:, 0] for nm in names])
+    sp = np.array([float(c1[f"spacing_{nm}"]) for nm in names])
+    blk = F.compute_fields(pos, tv, F.MlsParams("affine"), W, H, dtype=dtype, band_spacing=sp,
+                           colormap=R.DEFAULT_COLORMAP)
+    got = blk.rgba.cpu().numpy()
+    table = F.palette_rgba8(R.DEFAULT_COLORMAP).view(np.uint8).reshape(-1, 4)
+    for k, nm in enumerate(names):
+        ref_bands = c1[f"bands_{nm}"]
+        want = table[np.mod(ref_bands, len(table))]
+        u = c1[f"field_{nm}"][..., 0] / sp[k]
+        ok = np.abs(u - np.rint(u)) >= eps
+        assert np.array_equal(got[k][ok], want[ok]), nm
+        # and the fused bands agree with the fused colours everywhere
+        assert np.array_equal(got[k], table[np.mod(blk.bands[k].cpu().numpy(), len(table))])
