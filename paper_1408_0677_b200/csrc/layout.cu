@@ -1319,6 +1319,7 @@ struct MdcLayoutPlan {
     TreeShape shape;
     Buffers b;
     cudaGraphExec_t graph[2] = {nullptr, nullptr};
+    cudaGraphExec_t graph_multi = nullptr;  // MDC_LAYOUT_MULTI consecutive steps in one graph
     cudaStream_t cap_stream = nullptr;
     const double *graph_temps = nullptr;
     int build_blocks = 0;
@@ -1636,10 +1637,16 @@ extern "C" int mdc_layout_plan_destroy(MdcLayoutPlan *p) {
     if (!p) return MDC_OK;
     for (auto &g : p->graph)
         if (g) cudaGraphExecDestroy(g);
+    if (p->graph_multi) cudaGraphExecDestroy(p->graph_multi);
     if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
     delete p;
     return MDC_OK;
 }
+
+#ifndef MDC_LAYOUT_MULTI
+#define MDC_LAYOUT_MULTI 32  // steps per multi-step graph (even: the buffer parity returns to 0)
+#endif
+static_assert(MDC_LAYOUT_MULTI % 2 == 0, "a multi-step graph must span an even number of steps");
 
 extern "C" int mdc_layout_steps(MdcLayoutPlan *p, int32_t k, const double *temps, int32_t use_graph,
                                 void *stream) {
@@ -1666,7 +1673,28 @@ extern "C" int mdc_layout_steps(MdcLayoutPlan *p, int32_t k, const double *temps
             p->graph_temps = temps;
         }
         MDC_REQUIRE(p->graph_temps == temps, "temps pointer changed after graph capture");
-        for (int it = 0; it < k; ++it) MDC_CHECK_CUDA(cudaGraphLaunch(p->graph[it & 1], s));
+        int it = 0;
+        if (MDC_LAYOUT_MULTI > 1 && k >= MDC_LAYOUT_MULTI) {
+            // runs of MDC_LAYOUT_MULTI (even) steps as ONE graph launch: no
+            // per-step launch gap, which dominates small meshes (config 1:
+            // ~10 tiny kernels per step)
+            if (!p->graph_multi) {
+                MDC_CHECK_CUDA(cudaStreamBeginCapture(p->cap_stream, cudaStreamCaptureModeThreadLocal));
+                int rc = 0;
+                for (int j = 0; j < MDC_LAYOUT_MULTI && !rc; ++j)
+                    rc = enqueue_step(p, bufs[j & 1], bufs[(j & 1) ^ 1], temps, p->cap_stream);
+                cudaGraph_t g;
+                cudaError_t e = cudaStreamEndCapture(p->cap_stream, &g);
+                if (rc) return rc;
+                MDC_CHECK_CUDA(e);
+                e = cudaGraphInstantiate(&p->graph_multi, g, 0);
+                cudaGraphDestroy(g);
+                MDC_CHECK_CUDA(e);
+            }
+            for (; it + MDC_LAYOUT_MULTI <= k; it += MDC_LAYOUT_MULTI)
+                MDC_CHECK_CUDA(cudaGraphLaunch(p->graph_multi, s));
+        }
+        for (; it < k; ++it) MDC_CHECK_CUDA(cudaGraphLaunch(p->graph[it & 1], s));
     } else {
         for (int it = 0; it < k; ++it) {
             int rc = enqueue_step(p, bufs[it & 1], bufs[(it & 1) ^ 1], temps, s);
@@ -1762,7 +1790,8 @@ extern "C" int mdc_layout_step_parity(MdcLayoutPlan *p, int32_t parity, const do
 extern "C" int mdc_layout_set_gather(MdcLayoutPlan *p, double *send) {
     MDC_REQUIRE(p, "null pointer");
     MDC_REQUIRE(p->a.part_world > 1, "the all-gather exchange needs a partitioned plan (part_world > 1)");
-    MDC_REQUIRE(!p->graph[0] && !p->graph[1], "set the gather buffer before the first captured step");
+    MDC_REQUIRE(!p->graph[0] && !p->graph[1] && !p->graph_multi,
+                "set the gather buffer before the first captured step");
     p->gather_send = send;
     return MDC_OK;
 }

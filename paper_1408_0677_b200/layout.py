@@ -120,6 +120,7 @@ class LayoutEngine:
         self.part = (int(part[0]), int(part[1]))
         self._plans = {}
         self.temps = None
+        self.gather_send = None  # all-gather exchange: packed owned-slice buffer (GatherLayout)
 
     def _args(self, dbg=None) -> _lib.MdcLayoutArgs:
         p = self.params
@@ -149,6 +150,8 @@ class LayoutEngine:
             h = ctypes.c_void_p()
             _lib.check(self.lib.mdc_layout_plan_create(ctypes.byref(a), ctypes.byref(h), _lib.stream_ptr()),
                        "mdc_layout_plan_create")
+            if self.gather_send is not None:  # before any step is captured into a graph
+                _lib.check(self.lib.mdc_layout_set_gather(h, _lib.ptr(self.gather_send)), "mdc_layout_set_gather")
             self._plans[key] = h
         return self._plans[key]
 
@@ -369,7 +372,7 @@ class GatherLayout:
         dev = self.eng.device
         self.send = torch.zeros((self.chunk, 2), dtype=torch.float64, device=dev)
         self.recv = torch.empty((self.world * self.chunk, 2), dtype=torch.float64, device=dev)
-        _lib.check(self.eng.lib.mdc_layout_set_gather(self.eng.plan(), _lib.ptr(self.send)), "mdc_layout_set_gather")
+        self.eng.gather_send = self.send  # applied to every plan the engine creates
 
     def step(self, temps) -> None:
         self.eng.run(temps, use_graph=True)

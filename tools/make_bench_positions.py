@@ -4,6 +4,7 @@ scene, same CUDA-graph steps).  The CPU arm times the reference's MLS at the
 laid-out positions and the reference's layout step from iterations 0 and 250
 from these; bench.py's GPU arm checks its own final positions
 equal the file.  Run on the GPU box: python tools/make_bench_positions.py"""
+import hashlib
 import os
 import sys
 
@@ -34,8 +35,10 @@ def main(ids):
         eng2.run(temps)
         assert np.array_equal(eng2.pos.cpu().numpy(), pfin), "the split run must equal bench.py's one-call run"
         path = os.path.join(ROOT, "bench_data", f"config{cid}_positions.npz")
+        tri = np.ascontiguousarray(mesh.triangles.astype(np.int64))
         np.savez_compressed(path, iters=np.int64(cfg["iters"]), original_pos=mesh.original_pos,
-                            triangles=mesh.triangles, pos_250=p250, pos_final=pfin)
+                            triangles_sha256=np.array(hashlib.sha256(tri.tobytes()).hexdigest()),
+                            pos_250=p250, pos_final=pfin)
         print("wrote", path, os.path.getsize(path))
 
 
