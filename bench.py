@@ -427,7 +427,9 @@ def main():
                 eng.run(temps[:k])
 
         reset()
-        layout_pass(min(5, cfg["iters"]))  # warm-up + graph capture
+        # warm-up: one full pass captures every graph the timed pass replays
+        # (single-step and 32-step graphs)
+        layout_pass(cfg["iters"])
         reset()
         torch.cuda.synchronize()
         if world > 1:

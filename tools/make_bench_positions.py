@@ -24,7 +24,7 @@ def main(ids):
         temps = L.temperature_schedule(params.initial_temp, params.decay_lambda, cfg["iters"])
         eng = L.LayoutEngine(mesh, params)
         eng.set_positions(mesh.original_pos)
-        eng.run(temps[:5])  # bench.py's warm-up + capture
+        eng.run(temps)  # bench.py's warm-up + capture
         eng.set_positions(mesh.original_pos)
         eng.run(temps[:250])
         p250 = eng.pos.cpu().numpy()
