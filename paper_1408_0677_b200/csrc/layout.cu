@@ -503,7 +503,7 @@ __device__ __forceinline__ void node_centroids(const BuildArgs &a, int64_t gw, i
 // __syncthreads), one thread-block cluster (barrier.cluster), or the whole
 // cooperative grid (grid.sync); the code is otherwise identical.
 template <int NTH, int MODE>
-__global__ void __launch_bounds__(NTH) build_levels_kernel(BuildArgs a) {
+__device__ __forceinline__ void build_levels_body(const BuildArgs &a) {
     constexpr int BUILD_THREADS = NTH;
     typedef cub::BlockReduce<int, BUILD_THREADS> BR;
     typedef cub::BlockScan<int, BUILD_THREADS> BS;
@@ -634,6 +634,11 @@ __global__ void __launch_bounds__(NTH) build_levels_kernel(BuildArgs a) {
     }
     grid.sync();
     node_centroids(a, gw, nw);
+}
+
+template <int NTH, int MODE>
+__global__ void __launch_bounds__(NTH) build_levels_kernel(BuildArgs a) {
+    build_levels_body<NTH, MODE>(a);
 }
 
 // Deep levels of the large-n walk: once every frontier segment is small,
@@ -830,17 +835,15 @@ __device__ __forceinline__ void monopole(const double4 g1, double xi, double yi,
 // are combined in task order by the consumer.
 // COUNT (profiling only, mdc_layout_profile): also tally leaf-pair and
 // monopole interactions and node opening tests into cnt[0..2].
+// One warp's work item: point-warp `pw` (32 leaf-order points from k0) x task.
+// s_node / s_mask / s_leaf: this warp's BH_STACK / BH_STACK / 32 entries.
 template <bool COUNT>
-__global__ void __launch_bounds__(BH_WARPS * 32) bh_kernel(int64_t n, int64_t k0, int64_t k1, DevTree t,
-                                                           double c, double eta, double theta,
-                                                           unsigned long long *cnt) {
+__device__ __forceinline__ void bh_body(int64_t n, int64_t k0, int64_t k1, const DevTree &t, double c, double eta,
+                                        double theta, unsigned long long *cnt, int64_t pw, int task, int *s_node_w,
+                                        unsigned *s_mask_w, double2 *s_leaf_w) {
     unsigned long long n_leaf = 0, n_mono = 0, n_test = 0, n_slot = 0;
-    __shared__ int s_node[BH_WARPS][BH_STACK];
-    __shared__ unsigned s_mask[BH_WARPS][BH_STACK];
-    __shared__ double2 s_leaf[BH_WARPS][32];  // the leaf being summed
-    const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int task = blockIdx.y;
-    const int64_t k = k0 + ((int64_t)blockIdx.x * BH_WARPS + wib) * 32 + lane;
+    const int lane = threadIdx.x & 31;
+    const int64_t k = k0 + pw * 32 + lane;
     const bool valid = k < k1;
     double xi = 0.0, yi = 0.0;
     if (valid) {
@@ -865,16 +868,16 @@ __global__ void __launch_bounds__(BH_WARPS * 32) bh_kernel(int64_t n, int64_t k0
     unsigned m0 = __ballot_sync(0xffffffffu, act);
     if (m0) {
         if (lane == 0) {
-            s_node[wib][0] = t.task_node[task];
-            s_mask[wib][0] = m0;
+            s_node_w[0] = t.task_node[task];
+            s_mask_w[0] = m0;
         }
         int sp = 1;
         __syncwarp();
         const double2 *sp2 = reinterpret_cast<const double2 *>(t.spts);
         while (sp > 0) {
             --sp;
-            int node = s_node[wib][sp];
-            unsigned mask = s_mask[wib][sp];
+            int node = s_node_w[sp];
+            unsigned mask = s_mask_w[sp];
             __syncwarp();
             bool on = (mask >> lane) & 1u;
             int4 tp = t.topo[node];
@@ -895,11 +898,11 @@ __global__ void __launch_bounds__(BH_WARPS * 32) bh_kernel(int64_t n, int64_t k0
                 if (COUNT && on) n_leaf += (unsigned long long)(tp.y - tp.x);
                 for (int base = tp.x; base < tp.y; base += 32) {
                     const int cnt = min(32, tp.y - base);
-                    if (lane < cnt) s_leaf[wib][lane] = __ldg(sp2 + base + lane);
+                    if (lane < cnt) s_leaf_w[lane] = __ldg(sp2 + base + lane);
                     __syncwarp();
                     if (on) {
                         auto pair = [&](int q, double &ax, double &ay) {
-                            const double2 pj = s_leaf[wib][q];
+                            const double2 pj = s_leaf_w[q];
                             double dx = xi - pj.x, dy = yi - pj.y;
                             double r2 = fma(dx, dx, fma(dy, dy, 1e-300));
                             double y = rsqrt_nr(r2);
@@ -935,10 +938,10 @@ __global__ void __launch_bounds__(BH_WARPS * 32) bh_kernel(int64_t n, int64_t k0
             unsigned om = __ballot_sync(0xffffffffu, open);
             if (om) {
                 if (lane == 0) {
-                    s_node[wib][sp] = tp.z;
-                    s_mask[wib][sp] = om;
-                    s_node[wib][sp + 1] = tp.w;
-                    s_mask[wib][sp + 1] = om;
+                    s_node_w[sp] = tp.z;
+                    s_mask_w[sp] = om;
+                    s_node_w[sp + 1] = tp.w;
+                    s_mask_w[sp + 1] = om;
                 }
                 sp += 2;
                 __syncwarp();
@@ -952,6 +955,18 @@ __global__ void __launch_bounds__(BH_WARPS * 32) bh_kernel(int64_t n, int64_t k0
         atomicAdd(cnt + 2, n_test);
         if (lane == 0) atomicAdd(cnt + 3, n_slot);
     }
+}
+
+template <bool COUNT>
+__global__ void __launch_bounds__(BH_WARPS * 32) bh_kernel(int64_t n, int64_t k0, int64_t k1, DevTree t,
+                                                           double c, double eta, double theta,
+                                                           unsigned long long *cnt) {
+    __shared__ int s_node[BH_WARPS][BH_STACK];
+    __shared__ unsigned s_mask[BH_WARPS][BH_STACK];
+    __shared__ double2 s_leaf[BH_WARPS][32];  // the leaf being summed
+    const int wib = threadIdx.x >> 5;
+    bh_body<COUNT>(n, k0, k1, t, c, eta, theta, cnt, (int64_t)blockIdx.x * BH_WARPS + wib, blockIdx.y, s_node[wib],
+                   s_mask[wib], s_leaf[wib]);
 }
 
 // Combine the task partials (task order) into out[i] by point id.
@@ -1149,11 +1164,13 @@ __global__ void local_kernel(LocalArgs a) {
 #endif
 constexpr int LOCAL_SL = 4;  // terms per lane per gather round
 
+// gthread: this thread's global index over the n x LG lanes (all 32 lanes of
+// a warp must call together: the group reductions are warp collectives).
 template <int LG>
-__global__ void __launch_bounds__(128) local_group_kernel(LocalArgs a) {
+__device__ __forceinline__ void local_group_body(const LocalArgs &a, int64_t gthread) {
     const unsigned FULL = 0xffffffffu;
     const int sub = threadIdx.x & (LG - 1);
-    const int64_t idx = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LG;
+    const int64_t idx = gthread / LG;
     bool live;
     int64_t i;
     if (a.perm) {
@@ -1293,7 +1310,85 @@ __global__ void __launch_bounds__(128) local_group_kernel(LocalArgs a) {
     }
 }
 
+template <int LG>
+__global__ void __launch_bounds__(128) local_group_kernel(LocalArgs a) {
+    local_group_body<LG>(a, (int64_t)blockIdx.x * blockDim.x + threadIdx.x);
+}
+
 __global__ void incr_kernel(int32_t *ctr) { ctr[0] += 1; }
+
+// ---------------------------------------------------------------------------
+// Small meshes (n <= MDC_LAYOUT_SMALL_MAX, one GPU): the whole step -- exact
+// (coord, id) ranks on both axes, the one-CTA level walk, Barnes-Hut over
+// (point-warp, task) items, the task-ordered combine and the local update --
+// in ONE persistent CTA, for all k steps of the call, with block barriers
+// between phases instead of ~9 kernel launches per step (config 1: 150
+// points, where launch latency, not work, set the step time).  Same device
+// code and summation orders as the multi-kernel step: bit-identical.
+#ifndef MDC_LAYOUT_SMALL_MAX
+#define MDC_LAYOUT_SMALL_MAX 2048
+#endif
+constexpr int SMALL_THREADS = 512;
+
+struct SmallArgs {
+    BuildArgs ba;  // ba.pts is set per step
+    LocalArgs la;  // pos / pos_out / ctr are set per step
+    double *bufs[2];
+    int k;
+    double c, eta, theta;
+    int32_t *ctr;
+};
+
+__global__ void __launch_bounds__(SMALL_THREADS, 1) layout_small_kernel(SmallArgs sa) {
+    constexpr int W = SMALL_THREADS / 32;
+    __shared__ int s_node[W][BH_STACK];
+    __shared__ unsigned s_mask[W][BH_STACK];
+    __shared__ double2 s_leaf[W][32];
+    __shared__ int32_t s_step;
+    const int tid = threadIdx.x, wib = tid >> 5;
+    const int64_t n = sa.ba.n;
+    const DevTree &t = sa.ba.t;
+    const int32_t *perm = (sa.ba.max_depth & 1) ? sa.ba.xs1 : sa.ba.xs0;  // leaf order after the walk
+    for (int step = 0; step < sa.k; ++step) {
+        const double *pin = sa.bufs[step & 1];
+        double *pout = sa.bufs[(step & 1) ^ 1];
+        // exact ranks -> ids in (coord, id) order, x run then y run (the
+        // order the radix sort + equal-key fixup produces)
+        for (int64_t e = tid; e < 2 * n; e += SMALL_THREADS) {
+            const int axis = e >= n;
+            const int64_t i = e - axis * n;
+            const unsigned long long ki = order_key(pin[2 * i + axis]);
+            int r = 0;
+            for (int64_t j = 0; j < n; ++j) {
+                const unsigned long long kj = order_key(pin[2 * j + axis]);
+                r += (kj < ki) || (kj == ki && j < i);
+            }
+            sa.ba.xs0[axis * n + r] = (int32_t)i;
+        }
+        __syncthreads();
+        BuildArgs ba = sa.ba;
+        ba.pts = pin;
+        build_levels_body<SMALL_THREADS, BUILD_ONE_CTA>(ba);
+        __syncthreads();
+        const int64_t npw = (n + 31) / 32;
+        for (int64_t it = wib; it < npw * t.ntask; it += W)
+            bh_body<false>(n, 0, n, t, sa.c, sa.eta, sa.theta, nullptr, it % npw, (int)(it / npw), s_node[wib],
+                           s_mask[wib], s_leaf[wib]);
+        __syncthreads();
+        for (int64_t k = tid; k < n; k += SMALL_THREADS)
+            reinterpret_cast<double2 *>(const_cast<double *>(sa.la.bh))[perm[k]] = bh_total(t, n, k);
+        if (tid == 0) s_step = step;
+        __syncthreads();
+        LocalArgs la = sa.la;
+        la.pos = pin;
+        la.pos_out = pout;
+        la.ctr = &s_step;
+        for (int64_t base = 0; base < n * MDC_LOCAL_LG; base += SMALL_THREADS)
+            local_group_body<MDC_LOCAL_LG>(la, base + tid);
+        __syncthreads();
+    }
+    if (tid == 0) *sa.ctr = sa.k;
+}
 
 // All-gather exchange, receive side: recv holds every rank's packed slice
 // (rank r at r * chunk, n*r/w .. n*(r+1)/w in leaf order); scatter them to
@@ -1657,6 +1752,55 @@ extern "C" int mdc_layout_steps(MdcLayoutPlan *p, int32_t k, const double *temps
     MDC_CHECK_CUDA(cudaMemsetAsync(p->b.ctr, 0, sizeof(int32_t), s));
     double *bufs[2] = {p->a.pos, p->b.pos_b};
     bool dbg = p->a.dbg_bh || p->a.dbg_force || p->a.dbg_scale;
+    const int64_t n = p->shape.n;
+    if (use_graph && !dbg && MDC_LOCAL_LG && n >= 2 && n <= MDC_LAYOUT_SMALL_MAX && n <= BUILD_SINGLE_MAX &&
+        p->a.part_world <= 1) {
+        // small mesh: every step of the call in one persistent CTA
+        SmallArgs sa;
+        BuildArgs &ba = sa.ba;
+        ba.pts = nullptr;
+        ba.n = n;
+        ba.t = p->b.t;
+        ba.max_depth = p->shape.max_depth;
+        ba.nnodes = (int)p->shape.lo.size();
+        ba.xs0 = p->b.xs[0];
+        ba.xs1 = p->b.xs[1];
+        ba.ys0 = p->b.ys[0];
+        ba.ys1 = p->b.ys[1];
+        ba.flag = p->b.flag;
+        ba.oflag = reinterpret_cast<int32_t *>(p->b.kx_out);
+        ba.prefix = reinterpret_cast<int32_t *>(p->b.kx);
+        ba.blocksum = p->b.blocksum;
+        LocalArgs &la = sa.la;
+        la = LocalArgs{};
+        la.n = n;
+        la.bh = p->b.bh;
+        la.csr_off = p->a.csr_off;
+        la.csr_tgt = p->a.csr_tgt;
+        la.tris = p->a.tris;
+        la.inc_off = p->a.inc_off;
+        la.inc = p->a.inc;
+        la.spring = p->a.spring;
+        la.dlen = p->a.dlen;
+        la.eta = p->a.eta;
+        la.c = p->a.c;
+        la.temps = temps;
+        la.k0 = 0;
+        la.k1 = n;
+        sa.bufs[0] = bufs[0];
+        sa.bufs[1] = bufs[1];
+        sa.k = k;
+        sa.c = p->a.c;
+        sa.eta = p->a.eta;
+        sa.theta = p->a.theta;
+        sa.ctr = p->b.ctr;
+        layout_small_kernel<<<1, SMALL_THREADS, 0, s>>>(sa);
+        MDC_CHECK_LAUNCH();
+        if (k & 1)
+            MDC_CHECK_CUDA(cudaMemcpyAsync(p->a.pos, p->b.pos_b, sizeof(double) * 2 * (size_t)n,
+                                           cudaMemcpyDeviceToDevice, s));
+        return MDC_OK;
+    }
     if (use_graph && !dbg) {
         for (int par = 0; par < 2; ++par) {
             if (p->graph[par]) continue;

@@ -291,3 +291,27 @@ def test_free_running_5_steps_config2(g10k, g10k_traj):
     err = normwise(state.relaxed_pos, g10k_traj["states"][its.index(5)])
     print("free-running 5 steps at 10k:", err)
     assert err <= FREE_TOL
+
+
+@pytest.mark.parametrize("scene", ["c1", "g2k"])
+def test_small_mesh_persistent_step_bit_identical(scene, request):
+    """n <= 2048 runs every step of a call in one persistent CTA
+    (layout_small_kernel: exact ranks, one-CTA walk, BH, combine, local
+    update between block barriers).  It must equal the multi-kernel step
+    (use_graph=False: the launch-per-phase path) bit for bit over 12 steps."""
+    g = request.getfixturevalue(scene)
+    m = golden_mesh(g)
+    p = _params(g, iterations=12)
+    temps = L.temperature_schedule(p.initial_temp, p.decay_lambda, 12)
+    fused, multi = L.LayoutEngine(m, p), L.LayoutEngine(m, p)
+    fused.set_positions(m.original_pos)
+    multi.set_positions(m.original_pos)
+    fused.run(temps, use_graph=True)
+    multi.run(temps, use_graph=False)
+    assert np.array_equal(fused.pos.cpu().numpy(), multi.pos.cpu().numpy())
+    one = L.LayoutEngine(m, p)  # odd step counts end in the other buffer
+    one.set_positions(m.original_pos)
+    one.run(temps[:5], use_graph=True)
+    multi.set_positions(m.original_pos)
+    multi.run(temps[:5], use_graph=False)
+    assert np.array_equal(one.pos.cpu().numpy(), multi.pos.cpu().numpy())
