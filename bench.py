@@ -316,7 +316,7 @@ def _kernel_traffic(cfg, W, H, d, use_tc):
     """DRAM bytes per launch of the dominant kernel from the committed ncu
     capture, when this run is the captured workload (else None)."""
     try:
-        t = json.load(open(os.path.join(ROOT, "profiles", "r01_mls_tc_kernel_traffic.json")))
+        t = json.load(open(os.path.join(ROOT, "profiles", "r02_mls_tc_kernel_traffic.json")))
     except (OSError, ValueError):
         return None
     if use_tc and t.get("frame") == [W, H] and t.get("n") == cfg["n"] and t.get("d") == d:
@@ -572,7 +572,7 @@ def main():
     roofline = {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak, "traffic": traffic,
                 "traffic_def": "dram__bytes_read.sum + dram__bytes_write.sum of one launch from the committed "
-                               "ncu --set full capture of this workload (profiles/r01_mls_tc_kernel_traffic.json)",
+                               "ncu --set full capture of this workload (profiles/r02_mls_tc_kernel_traffic.json)",
                 "algorithmic_bytes": alg_bytes,
                 "algorithmic_bytes_def": "fp32 field + int32 bands + RGBA8 band shading per pixel-channel, + "
                                          "controls (16 B) and fp32 targets per control",

@@ -786,17 +786,28 @@ constexpr int BH_STACK = 64;
 // rounding).  The reference's IEEE division/sqrt agree to ~1e-16, far inside
 // the 1e-12 per-step contract.  The opening criterion keeps the IEEE sqrt so
 // every far/near decision matches the reference bit for bit.
+#ifndef MDC_BH_NEWTON
+#define MDC_BH_NEWTON 2  // order of the correction after the MUFU rcp/rsqrt approximations
+#endif
 __device__ __forceinline__ double rcp_nr(double x) {
     double r;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
     double e = fma(-x, r, 1.0);      // r = (1 - e)/x
+#if MDC_BH_NEWTON == 1
+    return fma(r, e, r);             // r (1 + e): relative error ~ e^2
+#else
     return fma(r, fma(e, e, e), r);  // r (1 + e + e^2)
+#endif
 }
 __device__ __forceinline__ double rsqrt_nr(double x) {
     double y;
     asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
     double e = fma(-x * y, y, 1.0);                 // y = (1 - e)^(1/2) / sqrt(x)
+#if MDC_BH_NEWTON == 1
+    return fma(y, 0.5 * e, y);                      // y (1 + e/2): relative error ~ 3e^2/8
+#else
     return fma(y * e, fma(0.375, e, 0.5), y);       // y (1 + e/2 + 3e^2/8)
+#endif
 }
 
 __device__ __forceinline__ bool far_node(const double4 g0, double size, double xi, double yi, double theta) {
