@@ -1360,6 +1360,12 @@ __global__ void __launch_bounds__(SMALL_THREADS, 1) layout_small_kernel(SmallArg
     const int64_t n = sa.ba.n;
     const DevTree &t = sa.ba.t;
     const int32_t *perm = (sa.ba.max_depth & 1) ? sa.ba.xs1 : sa.ba.xs0;  // leaf order after the walk
+#if MDC_SMALL_PROF  // experiments: per-phase clock totals, printed once
+    long long ph[6] = {0, 0, 0, 0, 0, 0}, t0 = clock64();
+#define MDC_PH(i) do { if (tid == 0) { long long t1 = clock64(); ph[i] += t1 - t0; t0 = t1; } } while (0)
+#else
+#define MDC_PH(i) do {} while (0)
+#endif
     for (int step = 0; step < sa.k; ++step) {
         const double *pin = sa.bufs[step & 1];
         double *pout = sa.bufs[(step & 1) ^ 1];
@@ -1377,19 +1383,23 @@ __global__ void __launch_bounds__(SMALL_THREADS, 1) layout_small_kernel(SmallArg
             sa.ba.xs0[axis * n + r] = (int32_t)i;
         }
         __syncthreads();
+        MDC_PH(0);
         BuildArgs ba = sa.ba;
         ba.pts = pin;
         build_levels_body<SMALL_THREADS, BUILD_ONE_CTA>(ba);
         __syncthreads();
+        MDC_PH(1);
         const int64_t npw = (n + 31) / 32;
         for (int64_t it = wib; it < npw * t.ntask; it += W)
             bh_body<false>(n, 0, n, t, sa.c, sa.eta, sa.theta, nullptr, it % npw, (int)(it / npw), s_node[wib],
                            s_mask[wib], s_leaf[wib]);
         __syncthreads();
+        MDC_PH(2);
         for (int64_t k = tid; k < n; k += SMALL_THREADS)
             reinterpret_cast<double2 *>(const_cast<double *>(sa.la.bh))[perm[k]] = bh_total(t, n, k);
         if (tid == 0) s_step = step;
         __syncthreads();
+        MDC_PH(3);
         LocalArgs la = sa.la;
         la.pos = pin;
         la.pos_out = pout;
@@ -1397,7 +1407,14 @@ __global__ void __launch_bounds__(SMALL_THREADS, 1) layout_small_kernel(SmallArg
         for (int64_t base = 0; base < n * MDC_LOCAL_LG; base += SMALL_THREADS)
             local_group_body<MDC_LOCAL_LG>(la, base + tid);
         __syncthreads();
+        MDC_PH(4);
     }
+#if MDC_SMALL_PROF
+    if (tid == 0)
+        printf("small-step cycles/step: ranks %lld build %lld bh %lld combine %lld local %lld (n=%lld k=%d)\n",
+               ph[0] / sa.k, ph[1] / sa.k, ph[2] / sa.k, ph[3] / sa.k, ph[4] / sa.k, (long long)n, sa.k);
+#endif
+#undef MDC_PH
     if (tid == 0) *sa.ctr = sa.k;
 }
 
