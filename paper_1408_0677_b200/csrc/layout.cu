@@ -1337,7 +1337,7 @@ __global__ void incr_kernel(int32_t *ctr) { ctr[0] += 1; }
 // points, where launch latency, not work, set the step time).  Same device
 // code and summation orders as the multi-kernel step: bit-identical.
 #ifndef MDC_LAYOUT_SMALL_MAX
-#define MDC_LAYOUT_SMALL_MAX 2048
+#define MDC_LAYOUT_SMALL_MAX 512  // one CTA only pays off for tiny meshes (n = 2000: 1.9 ms vs ~0.1 ms per step)
 #endif
 constexpr int SMALL_THREADS = 512;
 
@@ -1356,6 +1356,7 @@ __global__ void __launch_bounds__(SMALL_THREADS, 1) layout_small_kernel(SmallArg
     __shared__ unsigned s_mask[W][BH_STACK];
     __shared__ double2 s_leaf[W][32];
     __shared__ int32_t s_step;
+    __shared__ unsigned long long s_key[2 * MDC_LAYOUT_SMALL_MAX];
     const int tid = threadIdx.x, wib = tid >> 5;
     const int64_t n = sa.ba.n;
     const DevTree &t = sa.ba.t;
@@ -1371,13 +1372,19 @@ __global__ void __launch_bounds__(SMALL_THREADS, 1) layout_small_kernel(SmallArg
         double *pout = sa.bufs[(step & 1) ^ 1];
         // exact ranks -> ids in (coord, id) order, x run then y run (the
         // order the radix sort + equal-key fixup produces)
+        for (int64_t e = tid; e < 2 * n; e += SMALL_THREADS) {  // sortable keys staged in shared memory
+            const int axis = e >= n;
+            s_key[e] = order_key(pin[2 * (e - axis * n) + axis]);
+        }
+        __syncthreads();
         for (int64_t e = tid; e < 2 * n; e += SMALL_THREADS) {
             const int axis = e >= n;
             const int64_t i = e - axis * n;
-            const unsigned long long ki = order_key(pin[2 * i + axis]);
+            const unsigned long long ki = s_key[e];
+            const unsigned long long *kk = s_key + axis * n;
             int r = 0;
             for (int64_t j = 0; j < n; ++j) {
-                const unsigned long long kj = order_key(pin[2 * j + axis]);
+                const unsigned long long kj = kk[j];
                 r += (kj < ki) || (kj == ki && j < i);
             }
             sa.ba.xs0[axis * n + r] = (int32_t)i;
