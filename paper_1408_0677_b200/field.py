@@ -579,15 +579,20 @@ def compute_fields(positions, targets, params: MlsParams, width: int, height: in
                       rgba=None if rgba is None else rgba.view(torch.uint8).view(prob.d, rows, width, 4))
 
 
-def plan_row_bands(r0: int, r1: int, nbands: int = 4) -> list[tuple[int, int]]:
+SMALL_FRAME_PIXELS = 1 << 20  # below this the band split's extra launches cost more than the copy it hides
+
+
+def plan_row_bands(r0: int, r1: int, nbands: int = 4, width: int | None = None) -> list[tuple[int, int]]:
     """Row bands for ``compute_fields_to_host``: a large band, then a tail of
     ~rows / (2 nbands) rows whose compute hides the large band's device->host
     copy and whose own (exposed) copy is small.  Each band is one kernel
     launch with its own ramp-up/ramp-down (~1.2 ms at 4K, measured), so two
     bands beat many: 4K config 3 e2e 905 -> 893 ms/frame vs 7 whole-wave
-    bands or 4 equal ones."""
+    bands or 4 equal ones.  Frames under SMALL_FRAME_PIXELS (given ``width``)
+    take one band: there the second band's launches cost more than the copy
+    they would hide (config 1, 256x256)."""
     rows = r1 - r0
-    if rows < 2:
+    if rows < 2 or (width is not None and rows * width < SMALL_FRAME_PIXELS):
         return [(r0, r1)]
     tail = max(1, rows // (2 * max(1, int(nbands))))
     return [(r0, r1 - tail), (r1 - tail, r1)]
@@ -628,7 +633,7 @@ def compute_fields_to_host(positions, targets, params: MlsParams, width: int, he
                                  or rgba_out.dtype != torch.uint8 or not rgba_out.is_contiguous()):
         raise ValueError(f"rgba_out must be a contiguous host uint8 tensor of shape {(d, rows, width, 4)}")
     dev = prob.device
-    plan = plan_row_bands(r0, r1, nbands)
+    plan = plan_row_bands(r0, r1, nbands, width)
     step = max(b1 - b0 for b0, b1 in plan)
     spacing_t = None
     if band_spacing is not None:

@@ -161,6 +161,8 @@ def test_row_band_plan():
         if r1 - r0 >= 2:
             assert len(plan) == 2 and plan[1][1] - plan[1][0] <= plan[0][1] - plan[0][0]
     assert plan_row_bands(0, 2160, 4) == [(0, 1890), (1890, 2160)]
+    assert plan_row_bands(0, 2160, 4, width=3840) == [(0, 1890), (1890, 2160)]
+    assert plan_row_bands(0, 256, 4, width=256) == [(0, 256)]  # small frames: one band
 
 
 def test_delaunay_degenerate_inputs():
