@@ -63,13 +63,16 @@ constexpr int P1U = MDC_TC_P1STATIC > 0 ? MDC_TC_P1STATIC : 1;
 constexpr int A_SBO = (KT / 4) * 128;  // bytes between 8-row core-matrix groups of a Q tile
 static_assert(KT % 8 == 0 && XYR % KT == 0, "K tiles are whole tf32 K steps and tile a staging round");
 constexpr int NC_MAX = 32;             // channels per pass-2 chunk (fp64 totals in shared memory)
+#ifndef MDC_TC_SPLIT
+#define MDC_TC_SPLIT 1  // compute threads per pixel (2: each half takes half of every round / K tile)
+#endif
 #ifndef MDC_TC_WIDE
 #define MDC_TC_WIDE 64  // d > 32: 64-channel chunks at 2 CTAs per SM (0: 32-channel chunks, 4 CTAs per SM)
 #endif
 // CTAs per SM the register allocation targets: 64-channel chunks need 64 KB
 // of fp64 totals per CTA, so two CTAs share an SM.
 template <int NC>
-constexpr int minb() { return NC > NC_MAX ? 2 : MDC_TC_MINB; }
+constexpr int minb() { return NC > NC_MAX ? 2 : (MDC_TC_SPLIT > 1 ? 3 : MDC_TC_MINB); }
 
 // ---------------------------------------------------------------------------
 // Q -> tiled core-matrix image, hi/lo split.  img[(chunk * ntiles + t)][hi|lo]
@@ -103,11 +106,14 @@ __global__ void q_image_kernel(const float *q, int64_t n, int ldq, int d, int nc
 // them to the stage's "empty" barrier.  No block-wide barrier per K tile;
 // compute warps only wait when the ring wraps onto a stage whose MMAs are
 // still in flight, and at each fp64 flush.
-constexpr int CWARPS = TPB / 32;        // compute warps
-constexpr int THREADS = TPB + 32;       // + one issuer warp
+constexpr int SP = MDC_TC_SPLIT;
+constexpr int CT = SP * TPB;             // compute threads
+constexpr int CWARPS = CT / 32;          // compute warps
+constexpr int THREADS = CT + 32;         // + one issuer warp
+static_assert((XYR / 2) % SP == 0 && KT % (2 * SP) == 0, "halves take whole control pairs");
 
 __device__ __forceinline__ void compute_bar_sync() {  // named barrier over the compute threads
-    asm volatile("bar.sync 1, %0;" ::"n"(TPB) : "memory");
+    asm volatile("bar.sync 1, %0;" ::"n"(CT) : "memory");
 }
 
 template <int AM, int NC>
@@ -118,12 +124,16 @@ __global__ void __launch_bounds__(THREADS, minb<NC>()) mls_tc_kernel(KArgs a, co
     constexpr int ACOL = NC;
     constexpr int COLS = ACOL + STAGES * 2 * KT;
     constexpr int TMEM_COLS = COLS <= 32 ? 32 : (COLS <= 64 ? 64 : (COLS <= 128 ? 128 : (COLS <= 256 ? 256 : 512)));
-    constexpr int PER = XYR / TPB;  // staged controls per thread per round
+    constexpr int NPAIR = XYR / 2;                     // staged control pairs per round
+    constexpr int PPT = (NPAIR + CT - 1) / CT;         // pairs staged per thread
     extern __shared__ __align__(128) unsigned char smem[];
     unsigned char *sB = smem;                                          // STAGES x B_STAGE
     double *tot = reinterpret_cast<double *>(sB + STAGES * B_STAGE);   // NC x TPB fp64 totals
     float2 *sxy = reinterpret_cast<float2 *>(tot + NC * TPB);         // 2 x XYR controls
-    uint64_t *full = reinterpret_cast<uint64_t *>(sxy + 2 * XYR);     // STAGES: G + Q ready
+    double *red = reinterpret_cast<double *>(sxy + 2 * XYR);          // SP > 1: 6 x TPB moment totals
+    float *cbuf = reinterpret_cast<float *>(red + (SP > 1 ? 6 * TPB : 0));  // SP > 1: 3 x TPB
+    unsigned char *sbad = reinterpret_cast<unsigned char *>(cbuf + (SP > 1 ? 3 * TPB : 0));  // SP > 1: TPB
+    uint64_t *full = reinterpret_cast<uint64_t *>(sbad + (SP > 1 ? TPB : 0));               // STAGES: G + Q ready
     uint64_t *empty = full + STAGES;                                   // STAGES: MMAs retired
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(empty + STAGES);
 
@@ -188,7 +198,8 @@ __global__ void __launch_bounds__(THREADS, minb<NC>()) mls_tc_kernel(KArgs a, co
             if (mid >= a.p_total) mid = a.p_total - 1;
             pixel_xy(a, mid, ox, oy);
         }
-        int64_t p = tile_base + tid;
+        const int pix = SP > 1 ? tid % TPB : tid, hh = SP > 1 ? tid / TPB : 0;  // pixel (TMEM lane), control half
+        int64_t p = tile_base + pix;
         const bool active = p >= a.p_begin && p < a.p_end;
         if (!active) p = p < a.p_begin ? a.p_begin : a.p_end - 1;
         double vxg, vyg;
@@ -196,7 +207,7 @@ __global__ void __launch_bounds__(THREADS, minb<NC>()) mls_tc_kernel(KArgs a, co
         const float vx = (float)(vxg - ox), vy = (float)(vyg - oy);
         const int64_t n = a.n;
         const int64_t nxy = (n + XYR - 1) / XYR;
-        const uint32_t lane_addr = (uint32_t)(warp * 32) << 16;  // this warp's TMEM lanes
+        const uint32_t lane_addr = (uint32_t)((warp & 3) * 32) << 16;  // this warp's TMEM lanes
 
         // Control positions stream through a double-buffered staging area,
         // one named barrier per round.  Controls past n are parked far away
@@ -205,23 +216,24 @@ __global__ void __launch_bounds__(THREADS, minb<NC>()) mls_tc_kernel(KArgs a, co
         // Staging layout: one float4 per control PAIR, {x0, x1, y0, y1}, so
         // a 128-bit load yields packed (x0, x1) / (y0, y1) operands for the
         // f32x2 arithmetic below.  Each thread stages whole pairs.
-        static_assert(PER % 2 == 0, "controls are staged in pairs");
-        double2 pre[PER];
+        double2 pre[2 * PPT];
         auto fetch = [&](int64_t r) {
 #pragma unroll
-            for (int e = 0; e < PER / 2; ++e) {
+            for (int e = 0; e < PPT; ++e) {
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
-                    int64_t j = r * XYR + 2 * (e * TPB + tid) + h;
-                    pre[2 * e + h] = (r < nxy && j < n) ? reinterpret_cast<const double2 *>(a.pc)[j]
-                                                        : make_double2(1e300, 1e300);
+                    const int pi = e * CT + tid;
+                    int64_t j = r * XYR + 2 * pi + h;
+                    pre[2 * e + h] = (pi < NPAIR && r < nxy && j < n) ? reinterpret_cast<const double2 *>(a.pc)[j]
+                                                                     : make_double2(1e300, 1e300);
                 }
             }
         };
         auto store = [&](int64_t r) {
             float4 *buf = reinterpret_cast<float4 *>(sxy + (r & 1) * XYR);
 #pragma unroll
-            for (int e = 0; e < PER / 2; ++e) {
+            for (int e = 0; e < PPT; ++e) {
+                if (e * CT + tid >= NPAIR) break;
                 float x[2], y[2];
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
@@ -229,7 +241,7 @@ __global__ void __launch_bounds__(THREADS, minb<NC>()) mls_tc_kernel(KArgs a, co
                     x[h] = v.x == 1e300 ? 1e18f : (float)(v.x - ox);
                     y[h] = v.x == 1e300 ? 1e18f : (float)(v.y - oy);
                 }
-                buf[e * TPB + tid] = make_float4(x[0], x[1], y[0], y[1]);
+                buf[e * CT + tid] = make_float4(x[0], x[1], y[0], y[1]);
             }
         };
         auto xy_init = [&]() {
@@ -271,16 +283,19 @@ __global__ void __launch_bounds__(THREADS, minb<NC>()) mls_tc_kernel(KArgs a, co
                 sxy2 = __ffma2_rn(wdx, dy, sxy2);
                 syy2 = __ffma2_rn(wdy, dy, syy2);
             };
+            constexpr int HP = NPAIR / SP;  // pairs per half
+            const int jlo = hh * HP;
 #if MDC_TC_P1STATIC
             if (cnt == XYR) {  // full round: static trip count
 #pragma unroll (P1U)
-                for (int j2 = 0; j2 < XYR / 2; ++j2) acc(s4[j2], false);
+                for (int j2 = 0; j2 < HP; ++j2) acc(s4[jlo + j2], false);
             } else
 #endif
             {
+                const int jhi = min(jlo + HP, cnt >> 1);
 #pragma unroll 4
-                for (int j2 = 0; j2 < (cnt >> 1); ++j2) acc(s4[j2], false);
-                if (cnt & 1) acc(s4[cnt >> 1], true);
+                for (int j2 = jlo; j2 < jhi; ++j2) acc(s4[j2], false);
+                if ((cnt & 1) && (cnt >> 1) >= jlo && (cnt >> 1) < jlo + HP) acc(s4[cnt >> 1], true);
             }
             tw += (double)sw2.x + (double)sw2.y;
             tmx += (double)mx2.x + (double)mx2.y;
@@ -289,8 +304,19 @@ __global__ void __launch_bounds__(THREADS, minb<NC>()) mls_tc_kernel(KArgs a, co
             txy += (double)sxy2.x + (double)sxy2.y;
             tyy += (double)syy2.x + (double)syy2.y;
         }
-        float c0, c1, c2;
-        {
+        float c0 = 0.f, c1 = 0.f, c2 = 0.f;
+        if (SP > 1) {  // halves' moment totals -> half 0 (fixed order: half 0 + half 1)
+            if (hh == 1) {
+                red[0 * TPB + pix] = tw, red[1 * TPB + pix] = tmx, red[2 * TPB + pix] = tmy;
+                red[3 * TPB + pix] = txx, red[4 * TPB + pix] = txy, red[5 * TPB + pix] = tyy;
+            }
+            compute_bar_sync();
+            if (hh == 0) {
+                tw += red[0 * TPB + pix], tmx += red[1 * TPB + pix], tmy += red[2 * TPB + pix];
+                txx += red[3 * TPB + pix], txy += red[4 * TPB + pix], tyy += red[5 * TPB + pix];
+            }
+        }
+        if (hh == 0) {
             double s = tw, m0 = tmx, m1 = tmy;
             double a00 = txx - m0 * m0 / s;
             double a01 = txy - m0 * m1 / s;
@@ -304,6 +330,11 @@ __global__ void __launch_bounds__(THREADS, minb<NC>()) mls_tc_kernel(KArgs a, co
             c0 = (float)(1.0 / s + (m0 * u0 + m1 * u1) / (s * s));
             c1 = (float)(-u0 / s);
             c2 = (float)(-u1 / s);
+            if (SP > 1) cbuf[pix] = c0, cbuf[TPB + pix] = c1, cbuf[2 * TPB + pix] = c2;
+        }
+        if (SP > 1) {
+            compute_bar_sync();
+            c0 = cbuf[pix], c1 = cbuf[TPB + pix], c2 = cbuf[2 * TPB + pix];
         }
 
         // ---------------- pass 2: G tiles -> TMEM ring -> tcgen05 ----------------
@@ -319,7 +350,7 @@ __global__ void __launch_bounds__(THREADS, minb<NC>()) mls_tc_kernel(KArgs a, co
         auto flush = [&](bool init) {
             asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll
-            for (int c8 = 0; c8 < NC / 8; ++c8) {
+            for (int c8 = hh * (NC / 8 / SP); c8 < (hh + 1) * (NC / 8 / SP); ++c8) {  // this half's columns
                 uint32_t v[8];
                 asm volatile(
                     "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
@@ -328,7 +359,7 @@ __global__ void __launch_bounds__(THREADS, minb<NC>()) mls_tc_kernel(KArgs a, co
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
                 for (int e = 0; e < 8; ++e) {
-                    double &t = tot[(c8 * 8 + e) * TPB + tid];
+                    double &t = tot[(c8 * 8 + e) * TPB + pix];
                     t = (init ? 0.0 : t) + (double)__uint_as_float(v[e]);
                 }
             }
@@ -356,10 +387,11 @@ __global__ void __launch_bounds__(THREADS, minb<NC>()) mls_tc_kernel(KArgs a, co
                     mbar_arrive_tx(&full[s], B_STAGE);
                     bulk_g2s(sB + s * B_STAGE, qchunk + (size_t)t * B_STAGE, B_STAGE, &full[s]);
                 }
-                const float4 *buf = reinterpret_cast<const float4 *>(sxy + (round & 1) * XYR + tin * KT);
-                uint32_t ghi[KT], glo[KT];
+                constexpr int KH = KT / SP;  // controls of the K tile this thread evaluates
+                const float4 *buf = reinterpret_cast<const float4 *>(sxy + (round & 1) * XYR + tin * KT) + hh * (KH / 2);
+                uint32_t ghi[KH], glo[KH];
 #pragma unroll
-                for (int h = 0; h < KT / 2; ++h) {
+                for (int h = 0; h < KH / 2; ++h) {
                     const float4 pp = buf[h];
                     const float2 dx = __fadd2_rn(make_float2(pp.x, pp.y), nvx);
                     const float2 dy = __fadd2_rn(make_float2(pp.z, pp.w), nvy);
@@ -379,9 +411,9 @@ __global__ void __launch_bounds__(THREADS, minb<NC>()) mls_tc_kernel(KArgs a, co
                     glo[2 * h + 1] = __float_as_uint(gl.y);
                 }
                 // this warp's 32 rows (TMEM lanes) of the stage's G tile
-                const uint32_t ta = tmem + lane_addr + ACOL + s * 2 * KT;
-                tmem_st<KT>(ta, ghi);
-                tmem_st<KT>(ta + KT, glo);
+                const uint32_t ta = tmem + lane_addr + ACOL + s * 2 * KT + hh * KH;
+                tmem_st<KH>(ta, ghi);
+                tmem_st<KH>(ta + KT, glo);
                 asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
                 asm volatile("tcgen05.fence::before_thread_sync;");
                 __syncwarp();
@@ -394,10 +426,10 @@ __global__ void __launch_bounds__(THREADS, minb<NC>()) mls_tc_kernel(KArgs a, co
             }
             if (active) {
 #pragma unroll 4
-                for (int c = 0; c < NC; ++c) {
+                for (int c = hh * (NC / SP); c < (hh + 1) * (NC / SP); ++c) {
                     const int ch = chunk * NC + c;
                     if (ch < a.d) {
-                        float f = (float)(tot[c * TPB + tid] + a.qm[ch]);
+                        float f = (float)(tot[c * TPB + pix] + a.qm[ch]);
                         reinterpret_cast<float *>(a.out)[ch * a.out_cs + lr * a.out_rs + col * a.out_ps] = f;
                         if (!isfinite(f)) bad = true;
                         store_band(a, ch, lr, col, (double)f);
@@ -405,7 +437,12 @@ __global__ void __launch_bounds__(THREADS, minb<NC>()) mls_tc_kernel(KArgs a, co
                 }
             }
         }
-        if (a.nonfinite && active && bad) atomicAdd(a.nonfinite, 1);
+        if (SP > 1 && a.nonfinite) {  // one count per pixel (the snap pass decrements per pixel)
+            if (hh == 1) sbad[pix] = bad;
+            compute_bar_sync();
+            if (hh == 0) bad = bad || sbad[pix];
+        }
+        if (a.nonfinite && active && bad && hh == 0) atomicAdd(a.nonfinite, 1);
     }
     __syncthreads();
     if (issuer) {
@@ -698,7 +735,8 @@ constexpr int TOT_SETS = 1;
 template <int NC>
 static size_t tc_smem_bytes() {
     return STAGES * (size_t)(2 * NC * KT * 4) + (size_t)TOT_SETS * NC * TPB * sizeof(double) +
-           2 * XYR * sizeof(float2) + 2 * STAGES * sizeof(uint64_t) + 16;
+           2 * XYR * sizeof(float2) + (SP > 1 ? TPB * (6 * sizeof(double) + 3 * sizeof(float) + 1) : 0) +
+           2 * STAGES * sizeof(uint64_t) + 16;
 }
 
 static int pick_nc(int d) { return d <= 16 ? 16 : (d <= NC_MAX || !MDC_TC_WIDE ? NC_MAX : MDC_TC_WIDE); }
