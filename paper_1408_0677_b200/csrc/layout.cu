@@ -969,7 +969,10 @@ __device__ __forceinline__ void bh_body(int64_t n, int64_t k0, int64_t k1, const
 }
 
 template <bool COUNT>
-__global__ void __launch_bounds__(BH_WARPS * 32) bh_kernel(int64_t n, int64_t k0, int64_t k1, DevTree t,
+#ifndef MDC_BH_MINB
+#define MDC_BH_MINB 0  // 0: no occupancy target (the register count caps BH at 8 CTAs = 50 % occupancy)
+#endif
+__global__ void __launch_bounds__(BH_WARPS * 32, MDC_BH_MINB) bh_kernel(int64_t n, int64_t k0, int64_t k1, DevTree t,
                                                            double c, double eta, double theta,
                                                            unsigned long long *cnt) {
     __shared__ int s_node[BH_WARPS][BH_STACK];
@@ -1340,6 +1343,10 @@ __global__ void incr_kernel(int32_t *ctr) { ctr[0] += 1; }
 #define MDC_LAYOUT_SMALL_MAX 512  // one CTA only pays off for tiny meshes (n = 2000: 1.9 ms vs ~0.1 ms per step)
 #endif
 constexpr int SMALL_THREADS = 512;
+#ifndef MDC_SMALL_LG
+#define MDC_SMALL_LG MDC_LOCAL_LG  // lanes per vertex in the persistent step's local update
+#endif
+constexpr int SMALL_LG = MDC_SMALL_LG;
 
 struct SmallArgs {
     BuildArgs ba;  // ba.pts is set per step
@@ -1411,8 +1418,8 @@ __global__ void __launch_bounds__(SMALL_THREADS, 1) layout_small_kernel(SmallArg
         la.pos = pin;
         la.pos_out = pout;
         la.ctr = &s_step;
-        for (int64_t base = 0; base < n * MDC_LOCAL_LG; base += SMALL_THREADS)
-            local_group_body<MDC_LOCAL_LG>(la, base + tid);
+        for (int64_t base = 0; base < n * SMALL_LG; base += SMALL_THREADS)
+            local_group_body<SMALL_LG>(la, base + tid);
         __syncthreads();
         MDC_PH(4);
     }

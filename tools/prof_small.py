@@ -22,10 +22,13 @@ for name in ("c1", "g2k"):
     eng.set_positions(m.original_pos)
     eng.run(temps)
     torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    eng.set_positions(m.original_pos)
-    e0.record()
-    eng.run(temps)
-    e1.record()
-    e1.synchronize()
-    print(name, m.node_count, "us/step", e0.elapsed_time(e1) * 1e3 / 50, flush=True)
+    best = 1e30
+    for _ in range(7):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        eng.set_positions(m.original_pos)
+        e0.record()
+        eng.run(temps)
+        e1.record()
+        e1.synchronize()
+        best = min(best, e0.elapsed_time(e1) * 1e3 / 50)
+    print(name, m.node_count, "us/step (best of 7)", best, flush=True)
