@@ -489,7 +489,7 @@ def main():
     a = prob.args(out, (rows * W, W, 1), r0, r1, bands, (rows * W, W), sp_t, nonfinite, rgba=rgba, palette=pal_t)
     snap_ws = F._snap_workspace(int(lib.mdc_snap_workspace_bytes(W, rows)), dev)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
-    ctrl = [prob.pc_t, prob.q_t, prob.pos_t, prob.tvals_t]
+    ctrl = [prob.pc_t, prob.q_t, prob.pm_t, prob.qm_t, prob.pos_t, prob.tvals_t]
     stream = torch.cuda.current_stream()
     sptr = stream.cuda_stream
     kev = []

@@ -111,6 +111,10 @@ typedef struct MdcMlsArgs {
     uint32_t *rgba;
     const uint32_t *palette;
     int32_t palette_n;
+    /* optional: the frame centre pm (2 fp64, device, e.g. mdc_mls_prepare's
+     * output); when set the kernels read it there instead of pmx / pmy, so
+     * the caller need not copy it back to the host (no stream sync). */
+    const double *pm;
 } MdcMlsArgs;
 
 #define MDC_FLAG_NO_TC 1

@@ -47,6 +47,7 @@ class MdcMlsArgs(ctypes.Structure):
         ("workspace", _vp),
         ("workspace_bytes", ctypes.c_size_t),
         ("rgba", _vp), ("palette", _vp), ("palette_n", _c_i32),
+        ("pm", _vp),
     ]
 
 

@@ -711,6 +711,7 @@ extern "C" int mdc_mls_field(const MdcMlsArgs *a, void *stream) {
     k.sy = a->sy;
     k.pmx = a->pmx;
     k.pmy = a->pmy;
+    k.pm_dev = a->pm;
     k.n = a->n;
     k.d = a->d;
     k.ldq = a->ldq;

@@ -147,6 +147,7 @@ struct KArgs {
     uint32_t *rgba;
     const uint32_t *palette;
     int32_t palette_n;
+    const double *pm_dev;  // non-null: pm is read here (device) instead of pmx / pmy
 };
 
 // Band epilogue (render.py:135-139) fused with the discrete shading
@@ -173,8 +174,9 @@ __device__ __forceinline__ void pixel_xy(const KArgs &a, int64_t p, double &vx, 
     int col = (int)(p - row * a.width);
     double xs = dadd(a.x0, dmul((double)col + 0.5, a.sx));
     double ys = dsub(a.y1, dmul((double)row + 0.5, a.sy));
-    vx = dsub(xs, a.pmx);
-    vy = dsub(ys, a.pmy);
+    const double pmx = a.pm_dev ? __ldg(a.pm_dev) : a.pmx, pmy = a.pm_dev ? __ldg(a.pm_dev + 1) : a.pmy;
+    vx = dsub(xs, pmx);
+    vy = dsub(ys, pmy);
 }
 
 // Stage tile `t` of the control positions (fp64, re-centred on o) into sxy,

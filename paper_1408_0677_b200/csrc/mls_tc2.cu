@@ -175,8 +175,9 @@ __global__ void q2_image_kernel(const float *q, int64_t n, int ldq, int d, int n
 __device__ __forceinline__ void pixel_xy_rc(const KArgs &a, int64_t row, int64_t col, double &vx, double &vy) {
     double xs = dadd(a.x0, dmul((double)col + 0.5, a.sx));
     double ys = dsub(a.y1, dmul((double)row + 0.5, a.sy));
-    vx = dsub(xs, a.pmx);
-    vy = dsub(ys, a.pmy);
+    const double pmx = a.pm_dev ? __ldg(a.pm_dev) : a.pmx, pmy = a.pm_dev ? __ldg(a.pm_dev + 1) : a.pmy;
+    vx = dsub(xs, pmx);
+    vy = dsub(ys, pmy);
 }
 
 struct Args2 {
@@ -209,8 +210,9 @@ __global__ void __launch_bounds__(THREADS, 1) mls_tc2_kernel(KArgs a, const floa
     const int nchunk = g2.nchunk;
     constexpr int QROUND = NC * QSTRIDE;  // floats per staged round
     // tile frame origin (fp64): the tile's centre
-    const double cx = dsub(dadd(a.x0, dmul((double)(tx * TW + TW / 2), a.sx)), a.pmx);
-    const double cy = dsub(dsub(a.y1, dmul((double)(ty * TH + TH / 2), a.sy)), a.pmy);
+    const double pmx = a.pm_dev ? __ldg(a.pm_dev) : a.pmx, pmy = a.pm_dev ? __ldg(a.pm_dev + 1) : a.pmy;
+    const double cx = dsub(dadd(a.x0, dmul((double)(tx * TW + TW / 2), a.sx)), pmx);
+    const double cy = dsub(dsub(a.y1, dmul((double)(ty * TH + TH / 2), a.sy)), pmy);
 
     if (tid == 0) {
         for (int s = 0; s < STAGES; ++s) {

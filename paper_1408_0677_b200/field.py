@@ -475,7 +475,7 @@ class MlsProblem:
                                            self.dcode, _lib.ptr(self.axis_t), ldq, _lib.ptr(self.pc_t),
                                            _lib.ptr(self.q_t), _lib.ptr(pm_t), _lib.ptr(self.qm_t), _lib.ptr(ws), wsb,
                                            _lib.stream_ptr()), "mdc_mls_prepare")
-        self.pm = pm_t.cpu().numpy()  # the kernels take the frame centre by value
+        self.pm_t = pm_t  # the kernels read the frame centre on the device (no host round trip)
         self.h2d_bytes = sum(t.numel() * t.element_size() for t in (self.pos_t, self.tvals_t, self.axis_t))
         self.ldq = ldq
         self.flags = 0 if tensor_cores else _lib.MDC_FLAG_NO_TC
@@ -490,7 +490,8 @@ class MlsProblem:
         a.width, a.height, a.row0, a.row1 = self.width, self.height, int(row0), int(row1)
         a.n, a.d, a.ldq = self.n, self.d, self.ldq
         a.x0, a.y1, a.sx, a.sy = t.x0, t.y1, sx, sy
-        a.pmx, a.pmy = float(self.pm[0]), float(self.pm[1])
+        a.pmx = a.pmy = 0.0
+        a.pm = _lib.ptr(self.pm_t)
         a.alpha, a.reg_eps = self.alpha, self.reg_eps
         a.pc, a.q, a.qm, a.axis = _lib.ptr(self.pc_t), _lib.ptr(self.q_t), _lib.ptr(self.qm_t), _lib.ptr(self.axis_t)
         a.out = _lib.ptr(out)
@@ -521,6 +522,34 @@ class MlsProblem:
                 _lib.check(self.lib.mdc_mls_snap(ctypes.byref(a), _lib.ptr(self.pos_t), _lib.ptr(self.tvals_t),
                                                  ctypes.c_double(self.eps), _lib.ptr(ws), stream),
                            "mdc_mls_snap")
+
+
+_PALETTES: dict = {}
+_COPY_STREAMS: dict = {}
+_CACHE_GUARD = threading.Lock()
+
+
+def _palette_device(colormap, dev: torch.device) -> torch.Tensor:
+    """The packed palette on ``dev``, uploaded once per (colormap, device)."""
+    key = (tuple(tuple(c) for c in colormap), dev.index if dev.index is not None else torch.cuda.current_device())
+    with _CACHE_GUARD:
+        t = _PALETTES.get(key)
+    if t is None:
+        t = _h2d(palette_rgba8(colormap).view(np.int32), dev)
+        with _CACHE_GUARD:
+            t = _PALETTES.setdefault(key, t)
+    return t
+
+
+def _copy_stream(dev: torch.device) -> torch.cuda.Stream:
+    """One side stream per (device, thread) for the band D2H copies (creating
+    a stream per call costs tens of microseconds on small frames)."""
+    key = (dev.index if dev.index is not None else torch.cuda.current_device(), threading.get_ident())
+    with _CACHE_GUARD:
+        st = _COPY_STREAMS.get(key)
+        if st is None:
+            st = _COPY_STREAMS[key] = torch.cuda.Stream(device=dev)
+    return st
 
 
 def palette_rgba8(colormap) -> np.ndarray:
@@ -567,7 +596,7 @@ def compute_fields(positions, targets, params: MlsParams, width: int, height: in
     if colormap is not None:
         if spacing_t is None:
             raise ValueError("colormap shading needs band_spacing")
-        pal_t = _h2d(palette_rgba8(colormap).view(np.int32), dev)
+        pal_t = _palette_device(colormap, dev)
         rgba = torch.empty((prob.d, rows, width), dtype=torch.int32, device=dev)
     nonfinite = torch.zeros((), dtype=torch.int32, device=dev)
     a = prob.args(out, (rows * width, width, 1), r0, r1, bands, (rows * width, width), spacing_t, nonfinite,
@@ -641,7 +670,7 @@ def compute_fields_to_host(positions, targets, params: MlsParams, width: int, he
         spacing_t = _h2d(sp, dev)
     if colormap is not None and spacing_t is None:
         raise ValueError("colormap shading needs band_spacing")
-    pal_t = _h2d(palette_rgba8(colormap).view(np.int32), dev) if colormap is not None else None
+    pal_t = _palette_device(colormap, dev) if colormap is not None else None
     rgba_host = rgba_out.view(torch.int32).view(d, rows, width) if rgba_out is not None else None
     nonfinite = torch.zeros((), dtype=torch.int32, device=dev)
     vbuf = [torch.empty((d, step, width), dtype=prob.tdtype, device=dev) for _ in range(2)]
@@ -650,7 +679,7 @@ def compute_fields_to_host(positions, targets, params: MlsParams, width: int, he
     cbuf = [torch.empty((d, step, width), dtype=torch.int32, device=dev) for _ in range(2)] \
         if rgba_out is not None else [None, None]
     compute = torch.cuda.current_stream(dev)
-    copy = torch.cuda.Stream(device=dev)
+    copy = _copy_stream(dev)
     done = [None, None]  # copy-finished events per buffer
     for i, (b0, b1) in enumerate(plan):
         n_rows = b1 - b0

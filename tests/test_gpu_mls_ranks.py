@@ -60,7 +60,7 @@ def _worker(rank, world, port, d, out_dir):
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
     pos, raw, spacing = _scene(d)
     prob = MlsProblem(pos, raw, "affine", W, H, dtype="f32")
-    ctrl = [prob.pc_t, prob.q_t, prob.pos_t, prob.tvals_t]
+    ctrl = [prob.pc_t, prob.q_t, prob.pm_t, prob.qm_t, prob.pos_t, prob.tvals_t]
     if rank != 0:  # prove the control block arrives by broadcast, not by recomputation
         for t in ctrl:
             t.zero_()
