@@ -810,6 +810,9 @@ __device__ __forceinline__ double rsqrt_nr(double x) {
 #endif
 }
 
+#ifndef MDC_BH_F32TEST
+#define MDC_BH_F32TEST 1  // fp32 pre-test of the opening criterion (exact fp64 only inside its band)
+#endif
 __device__ __forceinline__ bool far_node(const double4 g0, double size, double xi, double yi, double theta) {
     double gx = g0.x - xi;
     if (gx < 0.0) gx = xi - g0.z;
@@ -817,6 +820,17 @@ __device__ __forceinline__ bool far_node(const double4 g0, double size, double x
     double gy = g0.y - yi;
     if (gy < 0.0) gy = yi - g0.w;
     if (gy < 0.0) gy = 0.0;
+#if MDC_BH_F32TEST
+    {
+        // fp32 pre-test: gx, gy are exact fp64 differences rounded once to
+        // fp32 (relative 2^-24), so d2 and size^2 carry < 1e-6 relative
+        // error; outside a 1e-4 band the fp32 decision equals the fp64 one.
+        const float gxf = (float)gx, gyf = (float)gy, sf = (float)size, tf = (float)theta;
+        const float d2f = __fmaf_rn(gxf, gxf, gyf * gyf), lf = sf * sf, rf = (tf * tf) * d2f;
+        if (lf < rf * (1.0f - 1e-4f)) return true;
+        if (lf > rf * (1.0f + 1e-4f)) return false;
+    }
+#endif
     const double d2 = __dadd_rn(__dmul_rn(gx, gx), __dmul_rn(gy, gy));
     // The reference decides size < theta * sqrt(d2) with both roundings.
     // Squared comparison with a 2^-40 relative guard band settles every case
