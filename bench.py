@@ -549,13 +549,15 @@ def main():
     alg_flops = pairs * (19 + 6 * d)  # SURVEY.md §8d per-pair figure (one-pass formulation)
     use_tc = (not args.no_tc) and d >= 8
     if use_tc:
-        nc = 16 if d <= 16 else 32
+        nc = 16 if d <= 16 else (32 if d <= 32 else (64 if d <= 64 else 128))  # mls_tc.cu pick_nc
         chunks = -(-d // nc)
         # SIMT FP32 lane-ops per pair (FFMA2/FADD2/FMUL2 count 2): pass-1 moments 14,
         # pass-2 G evaluation + tf32 split 10 per channel chunk
         fma_instr = pairs * (14 + 10 * chunks)
-        tc_flops = pairs * chunks * 3 * 2 * nc      # 3xTF32 MMAs
-        kname = f"mls_tc_kernel<alpha=1.5, N={nc}> (tcgen05 kind::tf32 3xTF32 pass 2)"
+        mixed = nc > 32  # wide chunks: tf32 main + 2 bf16 corrections = 2 tf32-equivalent passes
+        tc_flops = pairs * chunks * (2 if mixed else 3) * 2 * nc
+        kname = (f"mls_tc_kernel<alpha=1.5, N={nc}> (tcgen05 pass 2: "
+                 + ("kind::tf32 + kind::f16 bf16 corrections)" if mixed else "kind::tf32 3xTF32)"))
     else:
         dc = 1
         while dc < d and dc < 8:

@@ -24,6 +24,9 @@
 //
 // Tile geometry (A/B-tuned): CTA = 128 pixels (one M = 128 MMA tile) + an
 // issuer warp, K tile = 16 controls, 2-stage ring, 4 CTAs per SM (TMEM).
+#include <cuda_bf16.h>
+#include <type_traits>
+
 #include "mls_common.cuh"
 #include "tcgen05.cuh"
 
@@ -67,18 +70,49 @@ constexpr int NC_MAX = 32;             // channels per pass-2 chunk (fp64 totals
 #define MDC_TC_SPLIT 1  // compute threads per pixel (2: each half takes half of every round / K tile)
 #endif
 #ifndef MDC_TC_WIDE
-#define MDC_TC_WIDE 64  // d > 32: 64-channel chunks at 2 CTAs per SM (0: 32-channel chunks, 4 CTAs per SM)
+#define MDC_TC_WIDE 64  // d > 32: 64-channel chunks (0: 32-channel chunks only)
+#endif
+#ifndef MDC_TC_WIDE2
+#define MDC_TC_WIDE2 128  // d > 64: 128-channel chunks (0: 64-channel chunks)
+#endif
+#ifndef MDC_TC_MIXED
+#define MDC_TC_MIXED 1  // wide chunks: tf32 main product + bf16 correction products (2 instead of 3 tf32 passes)
+#endif
+#ifndef MDC_TC_TOT32
+#define MDC_TC_TOT32 1  // wide chunks keep their run totals in fp32 (RN adds) instead of fp64
 #endif
 // CTAs per SM the register allocation targets: 64-channel chunks need 64 KB
 // of fp64 totals per CTA, so two CTAs share an SM.
+// Run totals: fp64 for chunks of up to 32 channels; wide chunks use fp32
+// totals (round-to-nearest adds of the fp32 runs -- the truncating tensor-core
+// accumulation stays bounded by the run length) so that their shared memory
+// (NC x 128 x 4 B) does not cap the CTAs per SM.
+// Wide chunks are tensor-bound (N = 64/128 at 3 MMAs per K step), so they
+// use the mixed split: G_hi . Q_hi on kind::tf32 plus [G_hi | G_lo] .
+// [Q_lo ; Q_hi] on kind::f16 with bf16 operands (the correction products
+// are 2^-11 of the main one; 8 significant bits carry them).
 template <int NC>
-constexpr int minb() { return NC > NC_MAX ? 2 : (MDC_TC_SPLIT > 1 ? 3 : MDC_TC_MINB); }
+__host__ __device__ constexpr bool mixed() { return MDC_TC_MIXED && NC > NC_MAX; }
+static_assert(!MDC_TC_MIXED || MDC_TC_SPLIT == 1, "the mixed split's bf16 pairs assume one thread per pixel");
+
+template <int NC>
+struct TotOf {
+    using T = typename std::conditional<(NC > NC_MAX && MDC_TC_TOT32), float, double>::type;
+};
+// CTAs per SM the register allocation targets: TMEM (NC + 64 columns, power
+// of two) and the totals' shared memory set the real limit.
+template <int NC>
+__host__ __device__ constexpr int minb() {
+    return NC > 2 * NC_MAX ? 2 : (NC > NC_MAX ? (MDC_TC_TOT32 ? MDC_TC_MINB : 2) : (MDC_TC_SPLIT > 1 ? 3 : MDC_TC_MINB));
+}
 
 // ---------------------------------------------------------------------------
 // Q -> tiled core-matrix image, hi/lo split.  img[(chunk * ntiles + t)][hi|lo]
 // each half = NC rows (channels) x KT controls = NC * KT * 4 bytes.
+// mixed: the tile is [tf32 hi: NC x KT core matrices (8 x 4) | bf16 lo | bf16
+// hi: NC x KT core matrices (8 x 8 bf16)] -- the same NC * KT * 8 bytes.
 __global__ void q_image_kernel(const float *q, int64_t n, int ldq, int d, int nc, int nchunk, int64_t ntiles,
-                               float *img) {
+                               float *img, int mixed_layout) {
     int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int64_t total = (int64_t)nchunk * ntiles * nc * KT;
     if (e >= total) return;
@@ -97,7 +131,14 @@ __global__ void q_image_kernel(const float *q, int64_t n, int ldq, int d, int nc
     char *base = reinterpret_cast<char *>(img) + ((size_t)chunk * ntiles + t) * 2 * tile_bytes;
     uint32_t off = (uint32_t)((ch >> 3) * A_SBO + (k >> 2) * 128 + (ch & 7) * 16 + (k & 3) * 4);
     *reinterpret_cast<float *>(base + off) = hi;
-    *reinterpret_cast<float *>(base + tile_bytes + off) = lo;
+    if (!mixed_layout) {
+        *reinterpret_cast<float *>(base + tile_bytes + off) = lo;
+        return;
+    }
+    const size_t bf_bytes = (size_t)nc * KT * 2;
+    const uint32_t boff = (uint32_t)((ch >> 3) * (KT / 8) * 128 + (k >> 3) * 128 + (ch & 7) * 16 + (k & 7) * 2);
+    *reinterpret_cast<__nv_bfloat16 *>(base + tile_bytes + boff) = __float2bfloat16_rn(lo);
+    *reinterpret_cast<__nv_bfloat16 *>(base + tile_bytes + bf_bytes + boff) = __float2bfloat16_rn(hi);
 }
 
 // Warp roles: warps 0..3 (128 threads, one pixel each) evaluate moments and
@@ -128,7 +169,8 @@ __global__ void __launch_bounds__(THREADS, minb<NC>()) mls_tc_kernel(KArgs a, co
     constexpr int PPT = (NPAIR + CT - 1) / CT;         // pairs staged per thread
     extern __shared__ __align__(128) unsigned char smem[];
     unsigned char *sB = smem;                                          // STAGES x B_STAGE
-    double *tot = reinterpret_cast<double *>(sB + STAGES * B_STAGE);   // NC x TPB fp64 totals
+    using TotT = typename TotOf<NC>::T;
+    TotT *tot = reinterpret_cast<TotT *>(sB + STAGES * B_STAGE);       // NC x TPB run totals
     float2 *sxy = reinterpret_cast<float2 *>(tot + NC * TPB);         // 2 x XYR controls
     double *red = reinterpret_cast<double *>(sxy + 2 * XYR);          // SP > 1: 6 x TPB moment totals
     float *cbuf = reinterpret_cast<float *>(red + (SP > 1 ? 6 * TPB : 0));  // SP > 1: 3 x TPB
@@ -159,6 +201,7 @@ __global__ void __launch_bounds__(THREADS, minb<NC>()) mls_tc_kernel(KArgs a, co
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tmem = *tmem_slot;
     const uint32_t idesc = idesc_tf32(NC);
+    const uint32_t idesc_bf = idesc_bf16(NC);
 
     if (issuer) {
         // ------------------------------ MMA issuer --------------------------
@@ -170,17 +213,30 @@ __global__ void __launch_bounds__(THREADS, minb<NC>()) mls_tc_kernel(KArgs a, co
                     mbar_wait_sleep(&full[s], (ring / STAGES) & 1);
                     asm volatile("tcgen05.fence::after_thread_sync;");
                     const uint32_t b_hi = smem_u32(sB + s * B_STAGE), b_lo = b_hi + B_HALF;
+                    if constexpr (mixed<NC>()) {
+                        // stage A: [G_hi tf32 (KT cols) | G_hi bf16 pairs (KT/2) | G_lo bf16 pairs (KT/2)]
+                        // stage B: [Q_hi tf32 | Q_lo bf16 | Q_hi bf16]
+                        const uint32_t ta = tmem + ACOL + s * 2 * KT;
 #pragma unroll
-                    for (int kk = 0; kk < KT / 8; ++kk) {
-                        const uint32_t koff = kk * 256;
-                        // a fresh fp32 run after every fp64 flush
-                        const uint32_t acc = (t % FLUSH != 0 || kk > 0) ? 1u : 0u;
-                        const uint64_t dbh = umma_desc(b_hi + koff, 128, A_SBO);
-                        const uint64_t dbl = umma_desc(b_lo + koff, 128, A_SBO);
-                        const uint32_t ta = tmem + ACOL + s * 2 * KT + kk * 8;
-                        mma_tf32_ts(tmem, ta, dbh, idesc, acc);
-                        mma_tf32_ts(tmem, ta, dbl, idesc, 1u);
-                        mma_tf32_ts(tmem, ta + KT, dbh, idesc, 1u);
+                        for (int kk = 0; kk < KT / 8; ++kk)
+                            mma_tf32_ts(tmem, ta + kk * 8, umma_desc(b_hi + kk * 256, 128, A_SBO), idesc,
+                                        (t % FLUSH != 0 || kk > 0) ? 1u : 0u);
+                        constexpr uint32_t BF_SBO = (KT / 8) * 128, BF_BYTES = NC * KT * 2;
+                        mma_bf16_ts(tmem, ta + KT, umma_desc(b_lo, 128, BF_SBO), idesc_bf, 1u);
+                        mma_bf16_ts(tmem, ta + KT + KT / 2, umma_desc(b_lo + BF_BYTES, 128, BF_SBO), idesc_bf, 1u);
+                    } else {
+#pragma unroll
+                        for (int kk = 0; kk < KT / 8; ++kk) {
+                            const uint32_t koff = kk * 256;
+                            // a fresh fp32 run after every fp64 flush
+                            const uint32_t acc = (t % FLUSH != 0 || kk > 0) ? 1u : 0u;
+                            const uint64_t dbh = umma_desc(b_hi + koff, 128, A_SBO);
+                            const uint64_t dbl = umma_desc(b_lo + koff, 128, A_SBO);
+                            const uint32_t ta = tmem + ACOL + s * 2 * KT + kk * 8;
+                            mma_tf32_ts(tmem, ta, dbh, idesc, acc);
+                            mma_tf32_ts(tmem, ta, dbl, idesc, 1u);
+                            mma_tf32_ts(tmem, ta + KT, dbh, idesc, 1u);
+                        }
                     }
                     asm volatile(
                         "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -359,8 +415,8 @@ __global__ void __launch_bounds__(THREADS, minb<NC>()) mls_tc_kernel(KArgs a, co
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
                 for (int e = 0; e < 8; ++e) {
-                    double &t = tot[(c8 * 8 + e) * TPB + pix];
-                    t = (init ? 0.0 : t) + (double)__uint_as_float(v[e]);
+                    TotT &t = tot[(c8 * 8 + e) * TPB + pix];
+                    t = (init ? TotT(0) : t) + (TotT)__uint_as_float(v[e]);
                 }
             }
             // the next run's first MMA (accumulate = 0) overwrites these
@@ -407,8 +463,13 @@ __global__ void __launch_bounds__(THREADS, minb<NC>()) mls_tc_kernel(KArgs a, co
                     const float2 gl = __ffma2_rn(gh, make_float2(-1.f, -1.f), g);  // g - hi, exact
                     ghi[2 * h] = __float_as_uint(gh.x);
                     ghi[2 * h + 1] = __float_as_uint(gh.y);
-                    glo[2 * h] = __float_as_uint(gl.x);
-                    glo[2 * h + 1] = __float_as_uint(gl.y);
+                    if constexpr (mixed<NC>()) {  // [hi bf16 pairs | lo bf16 pairs]
+                        glo[h] = pack_bf16(gh.x, gh.y);
+                        glo[KH / 2 + h] = pack_bf16(gl.x, gl.y);
+                    } else {
+                        glo[2 * h] = __float_as_uint(gl.x);
+                        glo[2 * h + 1] = __float_as_uint(gl.y);
+                    }
                 }
                 // this warp's 32 rows (TMEM lanes) of the stage's G tile
                 const uint32_t ta = tmem + lane_addr + ACOL + s * 2 * KT + hh * KH;
@@ -429,7 +490,7 @@ __global__ void __launch_bounds__(THREADS, minb<NC>()) mls_tc_kernel(KArgs a, co
                 for (int c = hh * (NC / SP); c < (hh + 1) * (NC / SP); ++c) {
                     const int ch = chunk * NC + c;
                     if (ch < a.d) {
-                        float f = (float)(tot[c * TPB + pix] + a.qm[ch]);
+                        float f = (float)((double)tot[c * TPB + pix] + a.qm[ch]);
                         reinterpret_cast<float *>(a.out)[ch * a.out_cs + lr * a.out_rs + col * a.out_ps] = f;
                         if (!isfinite(f)) bad = true;
                         store_band(a, ch, lr, col, (double)f);
@@ -734,12 +795,17 @@ constexpr int TOT_SETS = 1;
 
 template <int NC>
 static size_t tc_smem_bytes() {
-    return STAGES * (size_t)(2 * NC * KT * 4) + (size_t)TOT_SETS * NC * TPB * sizeof(double) +
+    return STAGES * (size_t)(2 * NC * KT * 4) + (size_t)TOT_SETS * NC * TPB * sizeof(typename TotOf<NC>::T) +
            2 * XYR * sizeof(float2) + (SP > 1 ? TPB * (6 * sizeof(double) + 3 * sizeof(float) + 1) : 0) +
            2 * STAGES * sizeof(uint64_t) + 16;
 }
 
-static int pick_nc(int d) { return d <= 16 ? 16 : (d <= NC_MAX || !MDC_TC_WIDE ? NC_MAX : MDC_TC_WIDE); }
+static int pick_nc(int d) {
+    if (d <= 16) return 16;
+    if (d <= NC_MAX || !MDC_TC_WIDE) return NC_MAX;
+    if (d <= MDC_TC_WIDE || !MDC_TC_WIDE2) return MDC_TC_WIDE;
+    return MDC_TC_WIDE2;
+}
 
 }  // namespace tc
 
@@ -758,7 +824,8 @@ static int launch_tc_nc(const KArgs &k, void *ws, cudaStream_t s) {
     float *img = reinterpret_cast<float *>(ws);
     int64_t total = (int64_t)nchunk * ntiles * NC * KT;
     q_image_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(reinterpret_cast<const float *>(k.q), k.n,
-                                                                   k.ldq, k.d, NC, nchunk, ntiles, img);
+                                                                   k.ldq, k.d, NC, nchunk, ntiles, img,
+                                                                   mixed<NC>() ? 1 : 0);
 #if MDC_TC_ONEPASS
     auto fn = mls_tc1_kernel<AM, NC>;
 #else
@@ -780,6 +847,9 @@ static int launch_tc_am(const KArgs &k, void *ws, cudaStream_t s) {
         case 16: return launch_tc_nc<AM, 16>(k, ws, s);
 #if MDC_TC_WIDE
         case MDC_TC_WIDE: return launch_tc_nc<AM, MDC_TC_WIDE>(k, ws, s);
+#endif
+#if MDC_TC_WIDE2
+        case MDC_TC_WIDE2: return launch_tc_nc<AM, MDC_TC_WIDE2>(k, ws, s);
 #endif
         default: return launch_tc_nc<AM, tc::NC_MAX>(k, ws, s);
     }

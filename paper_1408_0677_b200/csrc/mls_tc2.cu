@@ -91,20 +91,6 @@ struct Geo {
                                    (2 * STAGES + 6 + 2 * NACC) * sizeof(uint64_t) + 16 + TP;
 };
 
-// Instruction descriptor, kind::f16 with bf16 A/B, D f32, both K-major.
-__host__ __device__ constexpr uint32_t idesc_bf16(int n) {
-    return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-}
-__device__ __forceinline__ void mma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc,
-                                            uint32_t acc) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "setp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
-        "}\n" ::"r"(tmem_d),
-        "r"(tmem_a), "l"(b), "r"(idesc), "r"(acc));
-}
 __device__ __forceinline__ void ring_wait(uint64_t *bar, uint32_t parity) {
 #if MDC_TC2_PARK
     mbar_wait_sleep(bar, parity);
@@ -137,11 +123,6 @@ __device__ __forceinline__ void tmem_ld<16>(uint32_t taddr, uint32_t (&v)[16]) {
         : "r"(taddr));
 }
 
-__device__ __forceinline__ uint32_t pack_bf16(float lo_k, float hi_k) {  // element k in the low half
-    uint32_t r;
-    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi_k), "f"(lo_k));
-    return r;
-}
 __device__ __forceinline__ float trunc_tf32(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
 
 // Byte offsets inside one B stage.  tf32 part: rows n (MMA N) x 16 controls,

@@ -41,7 +41,8 @@ def main():
         ms = e0.elapsed_time(e1)
         pairs = W * H * n
         if d >= 8:
-            chunks = -(-d // (16 if d <= 16 else 32))
+            nc = 16 if d <= 16 else (32 if d <= 32 else (64 if d <= 64 else 128))  # mls_tc.cu pick_nc
+            chunks = -(-d // nc)
             lane_ops, path = 14 + 10 * chunks, "tcgen05"
         else:
             lane_ops, path = 14 + 9 + d, "simt"  # DC = d here (one chunk)
