@@ -78,6 +78,9 @@ constexpr int NC_MAX = 32;             // channels per pass-2 chunk (fp64 totals
 #ifndef MDC_TC_MIXED
 #define MDC_TC_MIXED 1  // wide chunks: tf32 main product + bf16 correction products (2 instead of 3 tf32 passes)
 #endif
+#ifndef MDC_TC_MIXED_MIN
+#define MDC_TC_MIXED_MIN 64  // smallest chunk width using the mixed split
+#endif
 #ifndef MDC_TC_TOT32
 #define MDC_TC_TOT32 1  // wide chunks keep their run totals in fp32 (RN adds) instead of fp64
 #endif
@@ -92,7 +95,7 @@ constexpr int NC_MAX = 32;             // channels per pass-2 chunk (fp64 totals
 // [Q_lo ; Q_hi] on kind::f16 with bf16 operands (the correction products
 // are 2^-11 of the main one; 8 significant bits carry them).
 template <int NC>
-__host__ __device__ constexpr bool mixed() { return MDC_TC_MIXED && NC > NC_MAX; }
+__host__ __device__ constexpr bool mixed() { return MDC_TC_MIXED && NC >= MDC_TC_MIXED_MIN; }
 static_assert(!MDC_TC_MIXED || MDC_TC_SPLIT == 1, "the mixed split's bf16 pairs assume one thread per pixel");
 
 template <int NC>
