@@ -60,7 +60,27 @@ constexpr int TPR = XYR / KT;                 // K tiles per round
 #define MDC_TC2_LAG (MDC_TC2_STAGES + 2)
 #endif
 #ifndef MDC_TC2_EXP
-#define MDC_TC2_EXP 0  // timing experiments only: 1 no B build, 2 no weights, 3 no MMAs
+#define MDC_TC2_EXP 0  // timing experiments only (bit mask): 1 no B build, 2 no weights, 4 no MMAs
+#endif
+#ifndef MDC_TC2_PROF
+#define MDC_TC2_PROF 0  // experiments: per-role cycle breakdown printed by CTA 0
+#endif
+#if MDC_TC2_PROF
+struct Prof {
+    long long c[8];
+};
+#define PDECL Prof P = {}
+#define PBEGIN(v) long long v = clock64()
+#define PEND(i, v) P.c[i] += clock64() - v
+#define PREPORT(name)                                                                                           \
+    if (blockIdx.x == 0 && (threadIdx.x & 31) == 0)                                                             \
+        printf("%s w%d: %lld %lld %lld %lld %lld %lld\n", name, threadIdx.x >> 5, P.c[0], P.c[1], P.c[2], P.c[3], \
+               P.c[4], P.c[5])
+#else
+#define PDECL do {} while (0)
+#define PBEGIN(v) do {} while (0)
+#define PEND(i, v) do {} while (0)
+#define PREPORT(name) do {} while (0)
 #endif
 #ifndef MDC_TC2_PARK
 #define MDC_TC2_PARK 1  // pixel / builder warps park (suspend-hinted try_wait) instead of spinning on the ring
@@ -235,21 +255,27 @@ __global__ void __launch_bounds__(THREADS, 1) mls_tc2_kernel(KArgs a, const floa
             int s = 0;
             uint32_t ph = 0;
             int run = 0;  // global accumulation run
+            PDECL;
+            PBEGIN(tall);
             for (int chunk = 0; chunk < nchunk; ++chunk) {
                 int tr = 0;  // tile within the run
                 for (int t = 0; t < ntiles; ++t) {
                     const uint32_t d = tmem + (uint32_t)((run % NACC) * NCOL);
+                    PBEGIN(t0);
                     if (tr == 0 && run >= NACC) mbar_wait_sleep(&acc_free[run % NACC], (uint32_t)((run / NACC - 1) & 1));
+                    PEND(0, t0);
+                    PBEGIN(t1);
 #if MDC_TC2_ISSUER_SPIN
                     mbar_wait(&full[s], ph);
 #else
                     mbar_wait_sleep(&full[s], ph);
 #endif
+                    PEND(1, t1);
                     asm volatile("tcgen05.fence::after_thread_sync;");
                     const uint32_t bs = sb0 + s * BSTAGE;
                     const uint32_t ta = tmem + GE::ARING + s * ASTAGE;
 #pragma unroll
-                    for (int h = 0; h < 2 * (MDC_TC2_EXP != 3); ++h) {
+                    for (int h = 0; h < 2 * !(MDC_TC2_EXP & 4); ++h) {
                         mma_tf32_ts(d, ta + 16 * h, umma_desc(bs + h * 256, 128, 512), id_tf, (tr | h) ? 1u : 0u);
                         mma_bf16_ts(d, ta + 16 * h + 8, umma_desc(bs + PART + h * 256, 128, 512), id_bf, 1u);
                     }
@@ -262,6 +288,8 @@ __global__ void __launch_bounds__(THREADS, 1) mls_tc2_kernel(KArgs a, const floa
                     }
                 }
             }
+            PEND(5, tall);
+            PREPORT("issuer   accfree full - - - total");
         }
         __syncwarp();
     } else if (warp >= PW) {
@@ -307,6 +335,8 @@ __global__ void __launch_bounds__(THREADS, 1) mls_tc2_kernel(KArgs a, const floa
             __syncwarp();
             if (lane == 0) mbar_arrive(&xy_full[b]);
         };
+        PDECL;
+        PBEGIN(tall);
         stage_round(0);
         int s = 0;
         uint32_t ph = 0;
@@ -318,13 +348,20 @@ __global__ void __launch_bounds__(THREADS, 1) mls_tc2_kernel(KArgs a, const floa
                 const int b = R & 1;
                 {  // stage the next round mid-way through this one (or at its last tile if shorter)
                     const int last = min(TPR, ntiles - (t - tin)) - 1;
+                    PBEGIN(b0);
                     if (tin == min(TPR / 2, last)) stage_round(R + 1);
+                    PEND(0, b0);
                 }
+                PBEGIN(b1);
                 if (tin == 0) {
                     ring_wait(&xy_full[b], (uint32_t)((R >> 1) & 1));
                     ring_wait(&q_full[b], (uint32_t)((R >> 1) & 1));
                 }
+                PEND(1, b1);
+                PBEGIN(b2);
                 if (warm) ring_wait(&empty[s], ph ^ 1);
+                PEND(2, b2);
+                PBEGIN(b3);
                 unsigned char *st = sB + s * BSTAGE;
                 const float4 *xy = sxy + b * (XYR / 2) + tin * (KT / 2) + 4 * kh;
                 float X[8], Y[8];
@@ -349,7 +386,7 @@ __global__ void __launch_bounds__(THREADS, 1) mls_tc2_kernel(KArgs a, const floa
                         make_uint4(pack_bf16(lo[0], lo[1]), pack_bf16(lo[2], lo[3]), pack_bf16(lo[4], lo[5]),
                                    pack_bf16(lo[6], lo[7]));
                 };
-                if (MDC_TC2_EXP == 1) {
+                if (MDC_TC2_EXP & 1) {
                 } else if (role_q) {
                     const float *qrow = sq + b * QROUND + c * QSTRIDE + tin * KT + 8 * kh;
                     const float4 q0 = *reinterpret_cast<const float4 *>(qrow);
@@ -376,14 +413,19 @@ __global__ void __launch_bounds__(THREADS, 1) mls_tc2_kernel(KArgs a, const floa
                     }
                     emit(3 * NC + mm, v);
                 }
+                PEND(3, b3);
+                PBEGIN(b4);
                 fence_async_smem();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&full[s]);
+                PEND(4, b4);
                 if (++s == STAGES) s = 0, ph ^= 1, warm = true;
                 if (++tin == TPR) tin = 0, ++R;
             }
             if (tin != 0) ++R;  // a chunk's short last round
         }
+        PEND(5, tall);
+        PREPORT("builder  stage xyq empty build fence total");
     } else {
         // ------------------------------ pixel warps ------------------------------
         const int q4 = warp & 3, h = warp >> 2;
@@ -437,10 +479,17 @@ __global__ void __launch_bounds__(THREADS, 1) mls_tc2_kernel(KArgs a, const floa
                 for (int i = 0; i < 6; ++i) M6[i] += (double)__uint_as_float(v3[i]);
             };
             int tin = 0;
+            PDECL;
+            PBEGIN(tall);
             for (int t = 0; t < ntiles; ++t) {
                 const int b = R & 1;
+                PBEGIN(p0);
                 if (tin == 0) ring_wait(&xy_full[b], (uint32_t)((R >> 1) & 1));
+                PEND(0, p0);
+                PBEGIN(p1);
                 if (warm) ring_wait(&empty[s], ph ^ 1);
+                PEND(1, p1);
+                PBEGIN(p2);
                 asm volatile("tcgen05.fence::after_thread_sync;");
                 const float4 *xy = sxy + b * (XYR / 2) + tin * (KT / 2) + 4 * h;
                 uint32_t v[16];
@@ -458,10 +507,12 @@ __global__ void __launch_bounds__(THREADS, 1) mls_tc2_kernel(KArgs a, const floa
                     v[8 + p] = pack_bf16(wh.x, wh.y);
                     v[12 + p] = pack_bf16(wl.x, wl.y);
                 }
-                if (MDC_TC2_EXP == 2) {
+                if (MDC_TC2_EXP & 2) {
 #pragma unroll
                     for (int e = 0; e < 16; ++e) v[e] = 0x3f800000u;
                 }
+                PEND(2, p2);
+                PBEGIN(p3);
                 tmem_st<16>(a_base + s * ASTAGE, v);
                 asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
                 asm volatile("tcgen05.fence::before_thread_sync;");
@@ -471,13 +522,18 @@ __global__ void __launch_bounds__(THREADS, 1) mls_tc2_kernel(KArgs a, const floa
                     mbar_arrive(&full[s]);
                     if (round_end) mbar_arrive(&xy_empty[b]);
                 }
+                PEND(3, p3);
                 if (++s == STAGES) s = 0, ph ^= 1, warm = true;
                 if (++tin == TPR) tin = 0, ++R;
+                PBEGIN(p4);
                 if (t == drain_at) {
                     drain(next++);
                     drain_at += FLUSH;
                 }
+                PEND(4, p4);
             }
+            PEND(5, tall);
+            PREPORT("pixel    xy empty math store+arrive drain total");
             if (tin != 0) ++R;
             while (next < nruns) drain(next++);
             run0 += nruns;
