@@ -44,7 +44,11 @@ namespace tc2 {
 using namespace ::mdc::tc;
 
 constexpr int TW = 16, TH = 8, TP = TW * TH;  // pixel tile = MMA M
-constexpr int KT = 16;                        // controls per K tile
+#ifndef MDC_TC2_KQ
+#define MDC_TC2_KQ 1  // K tile = 16 KQ controls (each pixel warp half: 8 KQ per tile)
+#endif
+constexpr int KQ = MDC_TC2_KQ;
+constexpr int KT = 16 * KQ;                   // controls per K tile
 constexpr int XYR = 256;                      // controls per staging round
 constexpr int TPR = XYR / KT;                 // K tiles per round
 #ifndef MDC_TC2_STAGES
@@ -93,14 +97,15 @@ static_assert(LAG < (NACC - 1) * FLUSH, "a region is drained before the tensor c
 constexpr int PW = 8, BW = 3;         // pixel / builder warps (12 warps: 3 per SMSP -> 168 registers)
 constexpr int THREADS = (PW + BW + 1) * 32;
 constexpr int BT = BW * 32;           // builder threads
-constexpr int ASTAGE = 32;            // TMEM columns per A stage
+constexpr int ASTAGE = 32 * KQ;       // TMEM columns per A stage: per half [tf32 8KQ | bf16 hi 4KQ | bf16 lo 4KQ]
+constexpr int GSBO = 512 * KQ;        // bytes per 8-row core-matrix group of one B operand part
 constexpr int QSTRIDE = XYR + 4;      // staged targets: channel-major rows, padded (conflict-free LDS.128)
 
 template <int NC>
 struct Geo {
     static constexpr int NCOL = ((3 * NC + 6) + 15) / 16 * 16;  // MMA N
     static constexpr int G = NCOL / 8;                          // 8-row core-matrix groups
-    static constexpr int PART = G * 512;                        // bytes of one operand part per stage
+    static constexpr int PART = G * GSBO;                       // bytes of one operand part per stage
     static constexpr int BSTAGE = 2 * PART;                     // tf32 part + bf16 part
     static constexpr int ACC = 0;                               // accumulator regions [0, 2 NCOL)
     static constexpr int ARING = NACC * NCOL;
@@ -145,14 +150,18 @@ __device__ __forceinline__ void tmem_ld<16>(uint32_t taddr, uint32_t (&v)[16]) {
 
 __device__ __forceinline__ float trunc_tf32(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
 
-// Byte offsets inside one B stage.  tf32 part: rows n (MMA N) x 16 controls,
-// core matrices of 8 rows x 4 controls; bf16 part: rows n x 32 "k" slots,
-// k-block 2h = B_lo of controls 8h..8h+7, k-block 2h+1 = B_hi of the same.
-__device__ __forceinline__ uint32_t tf_off(int n, int k) { return (n >> 3) * 512 + (k >> 2) * 128 + (n & 7) * 16; }
+// Byte offsets inside one B stage.  tf32 part: rows n (MMA N) x KT controls,
+// core matrices of 8 rows x 4 controls; bf16 part: rows n x 2 KT "k" slots in
+// 8-slot k-blocks, per pixel-warp half h: KQ blocks of B_lo then KQ blocks of
+// B_hi for its 8 KQ controls (lo_block / hi_block below).
+__device__ __forceinline__ uint32_t tf_off(int n, int k) { return (n >> 3) * GSBO + (k >> 2) * 128 + (n & 7) * 16; }
 template <int PART>
 __device__ __forceinline__ uint32_t bf_off(int n, int kb, int kin) {
-    return PART + (n >> 3) * 512 + kb * 128 + (n & 7) * 16 + kin * 2;
+    return PART + (n >> 3) * GSBO + kb * 128 + (n & 7) * 16 + kin * 2;
 }
+// 8-control block kb8 (0 .. 2 KQ - 1) of a K tile: its half and bf16 k-blocks
+__device__ __forceinline__ int lo_block(int kb8) { return 2 * KQ * (kb8 / KQ) + kb8 % KQ; }
+__device__ __forceinline__ int hi_block(int kb8) { return 2 * KQ * (kb8 / KQ) + KQ + kb8 % KQ; }
 
 // Targets, chunk-major, channel-major within a staging round and zero-padded
 // to whole rounds: img[((chunk * nr + r) * nc + c) * QSTRIDE + jl] =
@@ -276,8 +285,15 @@ __global__ void __launch_bounds__(THREADS, 1) mls_tc2_kernel(KArgs a, const floa
                     const uint32_t ta = tmem + GE::ARING + s * ASTAGE;
 #pragma unroll
                     for (int h = 0; h < 2 * !(MDC_TC2_EXP & 4); ++h) {
-                        mma_tf32_ts(d, ta + 16 * h, umma_desc(bs + h * 256, 128, 512), id_tf, (tr | h) ? 1u : 0u);
-                        mma_bf16_ts(d, ta + 16 * h + 8, umma_desc(bs + PART + h * 256, 128, 512), id_bf, 1u);
+#pragma unroll
+                        for (int j = 0; j < KQ; ++j)
+                            mma_tf32_ts(d, ta + (ASTAGE / 2) * h + 8 * j,
+                                        umma_desc(bs + (2 * KQ * h + 2 * j) * 128, 128, GSBO), id_tf,
+                                        (tr | h | j) ? 1u : 0u);
+#pragma unroll
+                        for (int c = 0; c < KQ; ++c)
+                            mma_bf16_ts(d, ta + (ASTAGE / 2) * h + 8 * KQ + 8 * c,
+                                        umma_desc(bs + PART + (2 * KQ * h + 2 * c) * 128, 128, GSBO), id_bf, 1u);
                     }
                     commit(&empty[s]);
                     if (++s == STAGES) s = 0, ph ^= 1;
@@ -297,13 +313,7 @@ __global__ void __launch_bounds__(THREADS, 1) mls_tc2_kernel(KArgs a, const floa
         // Fixed roles: (channel c, control half kh) -> rows c, NC + c, 2 NC + c
         // (q, X q, Y q) of 8 controls; or (moment m, kh) -> row 3 NC + m.
         const int bt = tid - PW * 32;
-        const bool role_q = bt < 2 * NC;
-        const bool role_m = !role_q && bt < 2 * NC + 12;
-        const int c = role_q ? bt % NC : 0;
-        const int mm = role_m ? (bt - 2 * NC) % 6 : 0;
-        const int kh = role_q ? bt / NC : (role_m ? (bt - 2 * NC) / 6 : 0);
-        const bool uX = mm == 1 || mm == 3 || mm == 4, uY = mm == 2 || mm == 5;
-        const bool wX = mm == 3, wY = mm == 4 || mm == 5;
+        constexpr int NB8 = 2 * KQ;  // 8-control blocks per K tile
         const int total_rounds = nchunk * nr;
         auto stage_round = [&](int R) {  // global round R -> buffer R & 1
             if (R >= total_rounds) return;
@@ -363,55 +373,69 @@ __global__ void __launch_bounds__(THREADS, 1) mls_tc2_kernel(KArgs a, const floa
                 PEND(2, b2);
                 PBEGIN(b3);
                 unsigned char *st = sB + s * BSTAGE;
-                const float4 *xy = sxy + b * (XYR / 2) + tin * (KT / 2) + 4 * kh;
-                float X[8], Y[8];
+                // items: (channel c, 8-control block kb8) -> rows c, NC + c, 2 NC + c; then
+                // (moment m, kb8) -> row 3 NC + m
+                constexpr int NQI = NC * NB8, NITEM = NQI + 6 * NB8;
+#pragma unroll 1
+                for (int it = bt; it < NITEM; it += BT) {
+                    const bool role_q = it < NQI;
+                    const int c = role_q ? it % NC : 0;
+                    const int mm = role_q ? 0 : (it - NQI) % 6;
+                    const int kb8 = role_q ? it / NC : (it - NQI) / 6;
+                    const float4 *xy = sxy + b * (XYR / 2) + tin * (KT / 2) + 4 * kb8;
+                    float X[8], Y[8];
 #pragma unroll
-                for (int p = 0; p < 4; ++p) {
-                    const float4 pp = xy[p];
-                    X[2 * p] = pp.x, X[2 * p + 1] = pp.y, Y[2 * p] = pp.z, Y[2 * p + 1] = pp.w;
-                }
-                auto emit = [&](int nrw, const float (&v)[8]) {
-                    float hi[8], lo[8];
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) {
-                        hi[e] = trunc_tf32(v[e]);
-                        lo[e] = v[e] - hi[e];
+                    for (int p = 0; p < 4; ++p) {
+                        const float4 pp = xy[p];
+                        X[2 * p] = pp.x, X[2 * p + 1] = pp.y, Y[2 * p] = pp.z, Y[2 * p + 1] = pp.w;
                     }
-                    *reinterpret_cast<float4 *>(st + tf_off(nrw, 8 * kh)) = make_float4(hi[0], hi[1], hi[2], hi[3]);
-                    *reinterpret_cast<float4 *>(st + tf_off(nrw, 8 * kh + 4)) = make_float4(hi[4], hi[5], hi[6], hi[7]);
-                    *reinterpret_cast<uint4 *>(st + bf_off<PART>(nrw, 2 * kh + 1, 0)) =
-                        make_uint4(pack_bf16(hi[0], hi[1]), pack_bf16(hi[2], hi[3]), pack_bf16(hi[4], hi[5]),
-                                   pack_bf16(hi[6], hi[7]));
-                    *reinterpret_cast<uint4 *>(st + bf_off<PART>(nrw, 2 * kh, 0)) =
-                        make_uint4(pack_bf16(lo[0], lo[1]), pack_bf16(lo[2], lo[3]), pack_bf16(lo[4], lo[5]),
-                                   pack_bf16(lo[6], lo[7]));
-                };
-                if (MDC_TC2_EXP & 1) {
-                } else if (role_q) {
-                    const float *qrow = sq + b * QROUND + c * QSTRIDE + tin * KT + 8 * kh;
-                    const float4 q0 = *reinterpret_cast<const float4 *>(qrow);
-                    const float4 q1 = *reinterpret_cast<const float4 *>(qrow + 4);
-                    const float q[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};  // zero past n
-                    float v[8];
+                    const int hb = hi_block(kb8), lb = lo_block(kb8);
+                    auto emit = [&](int nrw, const float (&v)[8]) {
+                        float hi[8], lo[8];
 #pragma unroll
-                    for (int e = 0; e < 8; ++e) v[e] = q[e];
-                    emit(c, v);
+                        for (int e = 0; e < 8; ++e) {
+                            hi[e] = trunc_tf32(v[e]);
+                            lo[e] = v[e] - hi[e];
+                        }
+                        *reinterpret_cast<float4 *>(st + tf_off(nrw, 8 * kb8)) = make_float4(hi[0], hi[1], hi[2], hi[3]);
+                        *reinterpret_cast<float4 *>(st + tf_off(nrw, 8 * kb8 + 4)) =
+                            make_float4(hi[4], hi[5], hi[6], hi[7]);
+                        *reinterpret_cast<uint4 *>(st + bf_off<PART>(nrw, hb, 0)) =
+                            make_uint4(pack_bf16(hi[0], hi[1]), pack_bf16(hi[2], hi[3]), pack_bf16(hi[4], hi[5]),
+                                       pack_bf16(hi[6], hi[7]));
+                        *reinterpret_cast<uint4 *>(st + bf_off<PART>(nrw, lb, 0)) =
+                            make_uint4(pack_bf16(lo[0], lo[1]), pack_bf16(lo[2], lo[3]), pack_bf16(lo[4], lo[5]),
+                                       pack_bf16(lo[6], lo[7]));
+                    };
+                    if (MDC_TC2_EXP & 1) {
+                    } else if (role_q) {
+                        const float *qrow = sq + b * QROUND + c * QSTRIDE + tin * KT + 8 * kb8;
+                        const float4 q0 = *reinterpret_cast<const float4 *>(qrow);
+                        const float4 q1 = *reinterpret_cast<const float4 *>(qrow + 4);
+                        const float q[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};  // zero past n
+                        float v[8];
 #pragma unroll
-                    for (int e = 0; e < 8; ++e) v[e] = X[e] * q[e];
-                    emit(NC + c, v);
+                        for (int e = 0; e < 8; ++e) v[e] = q[e];
+                        emit(c, v);
 #pragma unroll
-                    for (int e = 0; e < 8; ++e) v[e] = Y[e] * q[e];
-                    emit(2 * NC + c, v);
-                } else if (role_m) {
-                    const bool tail = (int64_t)(t + 1) * KT > n;
-                    float v[8];
+                        for (int e = 0; e < 8; ++e) v[e] = X[e] * q[e];
+                        emit(NC + c, v);
 #pragma unroll
-                    for (int e = 0; e < 8; ++e) {
-                        const float u = uX ? X[e] : (uY ? Y[e] : 1.f);
-                        const float w = wX ? X[e] : (wY ? Y[e] : 1.f);
-                        v[e] = (tail && (int64_t)t * KT + 8 * kh + e >= n) ? 0.f : u * w;
+                        for (int e = 0; e < 8; ++e) v[e] = Y[e] * q[e];
+                        emit(2 * NC + c, v);
+                    } else {
+                        const bool uX = mm == 1 || mm == 3 || mm == 4, uY = mm == 2 || mm == 5;
+                        const bool wX = mm == 3, wY = mm == 4 || mm == 5;
+                        const bool tail = (int64_t)(t + 1) * KT > n;
+                        float v[8];
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) {
+                            const float u = uX ? X[e] : (uY ? Y[e] : 1.f);
+                            const float w = wX ? X[e] : (wY ? Y[e] : 1.f);
+                            v[e] = (tail && (int64_t)t * KT + 8 * kb8 + e >= n) ? 0.f : u * w;
+                        }
+                        emit(3 * NC + mm, v);
                     }
-                    emit(3 * NC + mm, v);
                 }
                 PEND(3, b3);
                 PBEGIN(b4);
@@ -439,7 +463,7 @@ __global__ void __launch_bounds__(THREADS, 1) mls_tc2_kernel(KArgs a, const floa
         const float2 nax = make_float2(-ax, -ax), nby = make_float2(-by, -by);
         const float neg_alpha = (float)(-a.alpha);
         const uint32_t lane_addr = (uint32_t)(q4 * 32) << 16;
-        const uint32_t a_base = tmem + lane_addr + GE::ARING + 16 * h;
+        const uint32_t a_base = tmem + lane_addr + GE::ARING + (ASTAGE / 2) * h;
         double T0[NH], TX[NH], TY[NH], M6[6];
         bool bad = false;
         int s = 0;
@@ -491,10 +515,10 @@ __global__ void __launch_bounds__(THREADS, 1) mls_tc2_kernel(KArgs a, const floa
                 PEND(1, p1);
                 PBEGIN(p2);
                 asm volatile("tcgen05.fence::after_thread_sync;");
-                const float4 *xy = sxy + b * (XYR / 2) + tin * (KT / 2) + 4 * h;
-                uint32_t v[16];
+                const float4 *xy = sxy + b * (XYR / 2) + tin * (KT / 2) + (KT / 4) * h;
+                uint32_t v[16 * KQ];
 #pragma unroll
-                for (int p = 0; p < 4; ++p) {
+                for (int p = 0; p < 4 * KQ; ++p) {
                     // parked controls (past n) get a tiny finite weight against zero B rows
                     const float4 pp = xy[p];
                     const float2 dx = __fadd2_rn(make_float2(pp.x, pp.y), nax);
@@ -504,16 +528,16 @@ __global__ void __launch_bounds__(THREADS, 1) mls_tc2_kernel(KArgs a, const floa
                     const float2 wl = __ffma2_rn(wh, make_float2(-1.f, -1.f), w);
                     v[2 * p] = __float_as_uint(wh.x);
                     v[2 * p + 1] = __float_as_uint(wh.y);
-                    v[8 + p] = pack_bf16(wh.x, wh.y);
-                    v[12 + p] = pack_bf16(wl.x, wl.y);
+                    v[8 * KQ + p] = pack_bf16(wh.x, wh.y);
+                    v[12 * KQ + p] = pack_bf16(wl.x, wl.y);
                 }
                 if (MDC_TC2_EXP & 2) {
 #pragma unroll
-                    for (int e = 0; e < 16; ++e) v[e] = 0x3f800000u;
+                    for (int e = 0; e < 16 * KQ; ++e) v[e] = 0x3f800000u;
                 }
                 PEND(2, p2);
                 PBEGIN(p3);
-                tmem_st<16>(a_base + s * ASTAGE, v);
+                tmem_st<16 * KQ>(a_base + s * ASTAGE, v);
                 asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
                 asm volatile("tcgen05.fence::before_thread_sync;");
                 __syncwarp();
