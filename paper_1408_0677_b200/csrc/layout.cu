@@ -18,6 +18,7 @@
 // per-warp (node, lane-mask) stack, right child popped first as in the
 // reference, so every lane accumulates its own interactions in the
 // reference's order.
+#include <utility>
 #include <math.h>
 
 #include <cooperative_groups.h>
@@ -259,6 +260,18 @@ static size_t carve(Buffers &b, char *base, const TreeShape &s) {
     return c.off + 256;
 }
 
+#ifndef MDC_LAYOUT_PDL
+#define MDC_LAYOUT_PDL 1  // step kernels launch as programmatic dependents (launch overlaps the predecessor's tail)
+#endif
+// First statement of every step kernel: under programmatic dependent launch
+// the kernel may start before its predecessor finishes and must wait here
+// before touching its outputs (a no-op for ordinary launches).
+__device__ __forceinline__ void pdl_wait() {
+#if MDC_LAYOUT_PDL
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+
 // ---------------------------------------------------------------------------
 // Kernels: tree build.
 
@@ -283,6 +296,7 @@ __device__ __forceinline__ uint32_t order_key32(double x) {
 }
 
 __global__ void keys_kernel(const double *pts, int64_t n, unsigned long long *keys, int32_t *ids) {
+    pdl_wait();
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= 2 * n) return;
     const int axis = i >= n;
@@ -301,6 +315,7 @@ __device__ __forceinline__ bool exact_less(const double *pts, int axis, int32_t 
 // exact order (exact-tie runs stay untouched: they are sorted by id).
 __global__ void run_mark_kernel(int64_t n, const unsigned long long *keys, const int32_t *ids, const double *pts,
                                 int32_t *runflag) {
+    pdl_wait();
     int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x + 1;
     if (k >= 2 * n || keys[k] != keys[k - 1]) return;
     const int axis = (int)(keys[k] >> 31);
@@ -314,6 +329,7 @@ __global__ void run_mark_kernel(int64_t n, const unsigned long long *keys, const
 // distinct doubles sharing one float), then clear its flag.
 __global__ void run_sort_kernel(int64_t n, const unsigned long long *keys, int32_t *ids, const double *pts,
                                 int32_t *runflag) {
+    pdl_wait();
     int64_t s0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (s0 >= 2 * n || !runflag[s0]) return;
     runflag[s0] = 0;
@@ -375,6 +391,7 @@ __device__ __forceinline__ uint32_t axis_key32(const double *pts, int64_t j, int
 
 __global__ void __launch_bounds__(RANK_THREADS) rank_count_kernel(const double *pts, int n, int span,
                                                                   int32_t *rank) {
+    pdl_wait();
     __shared__ uint32_t tile[RANK_TILE];
     const int axis = blockIdx.y;
     const int i = blockIdx.x * RANK_THREADS + threadIdx.x;
@@ -396,6 +413,7 @@ __global__ void __launch_bounds__(RANK_THREADS) rank_count_kernel(const double *
 
 __global__ void rank_scatter_kernel(const double *pts, int64_t n, int32_t *rank, unsigned long long *keys_out,
                                     int32_t *ids_out) {
+    pdl_wait();
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= 2 * n) return;
     const int axis = k >= n;
@@ -638,6 +656,7 @@ __device__ __forceinline__ void build_levels_body(const BuildArgs &a) {
 
 template <int NTH, int MODE>
 __global__ void __launch_bounds__(NTH) build_levels_kernel(BuildArgs a) {
+    pdl_wait();
     build_levels_body<NTH, MODE>(a);
 }
 
@@ -669,6 +688,7 @@ __device__ __forceinline__ int first_node_at_or_after(const DevTree &t, int L, i
 }
 
 __global__ void __launch_bounds__(SUBTREE_THREADS) build_subtree_kernel(BuildArgs a, int L0) {
+    pdl_wait();
     typedef cub::BlockScan<int, SUBTREE_THREADS> BS;
     __shared__ typename BS::TempStorage scan_tmp;
     __shared__ int s_carry;
@@ -769,6 +789,7 @@ __global__ void __launch_bounds__(SUBTREE_THREADS) build_subtree_kernel(BuildArg
 }
 
 __global__ void centroid_kernel(BuildArgs a) {
+    pdl_wait();
     const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     node_centroids(a, gtid >> 5, ((int64_t)gridDim.x * blockDim.x) >> 5);
 }
@@ -989,6 +1010,7 @@ template <bool COUNT>
 __global__ void __launch_bounds__(BH_WARPS * 32, MDC_BH_MINB) bh_kernel(int64_t n, int64_t k0, int64_t k1, DevTree t,
                                                            double c, double eta, double theta,
                                                            unsigned long long *cnt) {
+    pdl_wait();
     __shared__ int s_node[BH_WARPS][BH_STACK];
     __shared__ unsigned s_mask[BH_WARPS][BH_STACK];
     __shared__ double2 s_leaf[BH_WARPS][32];  // the leaf being summed
@@ -1009,6 +1031,7 @@ __device__ __forceinline__ double2 bh_total(const DevTree &t, int64_t n, int64_t
 }
 
 __global__ void bh_combine_kernel(int64_t n, int64_t k0, int64_t k1, DevTree t, const int32_t *perm, double *out) {
+    pdl_wait();
     int64_t k = k0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= k1) return;
     reinterpret_cast<double2 *>(out)[perm[k]] = bh_total(t, n, k);
@@ -1097,6 +1120,7 @@ __global__ void clamp_factors_kernel(int64_t n, const double *pos, const double 
 }
 
 __global__ void local_kernel(LocalArgs a) {
+    pdl_wait();
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t idx = i;
     if (a.perm) {
@@ -1340,10 +1364,14 @@ __device__ __forceinline__ void local_group_body(const LocalArgs &a, int64_t gth
 
 template <int LG>
 __global__ void __launch_bounds__(128) local_group_kernel(LocalArgs a) {
+    pdl_wait();
     local_group_body<LG>(a, (int64_t)blockIdx.x * blockDim.x + threadIdx.x);
 }
 
-__global__ void incr_kernel(int32_t *ctr) { ctr[0] += 1; }
+__global__ void incr_kernel(int32_t *ctr) {
+    pdl_wait();
+    ctr[0] += 1;
+}
 
 // ---------------------------------------------------------------------------
 // Small meshes (n <= MDC_LAYOUT_SMALL_MAX, one GPU): the whole step -- exact
@@ -1497,6 +1525,25 @@ struct MdcLayoutPlan {
 
 namespace mdc {
 
+// Launch as a programmatic dependent of the stream's previous kernel
+// (MDC_LAYOUT_PDL): its CTAs may be scheduled while the predecessor drains;
+// the kernel's pdl_wait() orders its reads.  Captured into the step graph as
+// programmatic edges.
+template <typename... KT, typename... AT>
+static cudaError_t launch_pdl(void (*kern)(KT...), dim3 grid, dim3 block, cudaStream_t s, AT &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = MDC_LAYOUT_PDL ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<AT>(args)...);
+}
+
 // Builds the tree for pts into b.t; returns the final perm (leaf order).
 static int build_tree(MdcLayoutPlan *p, const double *pts, cudaStream_t s, const int32_t **perm_out) {
     const TreeShape &sh = p->shape;
@@ -1513,18 +1560,21 @@ static int build_tree(MdcLayoutPlan *p, const double *pts, cudaStream_t s, const
         chunks = std::max(1, std::min(chunks, (int)((n + RANK_TILE - 1) / RANK_TILE) * 8));
         const int span = (int)((n + chunks - 1) / chunks);
         chunks = (int)((n + span - 1) / span);
-        rank_count_kernel<<<dim3(bx, 2, chunks), RANK_THREADS, 0, s>>>(pts, (int)n, span, b.rank);
-        rank_scatter_kernel<<<nb2, 256, 0, s>>>(pts, n, b.rank, b.kx_out, b.xs[0]);
+        MDC_CHECK_CUDA(launch_pdl(rank_count_kernel, dim3(bx, 2, chunks), dim3(RANK_THREADS), s, pts, (int)n, span,
+                                  b.rank));
+        MDC_CHECK_CUDA(launch_pdl(rank_scatter_kernel, dim3(nb2), dim3(256), s, pts, n, b.rank, b.kx_out, b.xs[0]));
         MDC_CHECK_LAUNCH();
     } else {
-        keys_kernel<<<nb2, 256, 0, s>>>(pts, n, b.kx, b.ids);
+        MDC_CHECK_CUDA(launch_pdl(keys_kernel, dim3(nb2), dim3(256), s, pts, n, b.kx, b.ids));
         MDC_CHECK_LAUNCH();
         size_t bytes = b.cub_bytes;
         MDC_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(b.cub_tmp, bytes, b.kx, b.kx_out, b.ids, b.xs[0],
                                                        (int)(2 * n), 0, 32, s));
     }
-    run_mark_kernel<<<nb2, 256, 0, s>>>(n, b.kx_out, b.xs[0], pts, b.runflag);
-    run_sort_kernel<<<nb2, 256, 0, s>>>(n, b.kx_out, b.xs[0], pts, b.runflag);
+    MDC_CHECK_CUDA(launch_pdl(run_mark_kernel, dim3(nb2), dim3(256), s, n, (const unsigned long long *)b.kx_out,
+                              (const int32_t *)b.xs[0], pts, b.runflag));
+    MDC_CHECK_CUDA(launch_pdl(run_sort_kernel, dim3(nb2), dim3(256), s, n, (const unsigned long long *)b.kx_out,
+                              b.xs[0], pts, b.runflag));
     MDC_CHECK_LAUNCH();
     p->mark(s);  // sorts done
     BuildArgs ba;
@@ -1542,7 +1592,8 @@ static int build_tree(MdcLayoutPlan *p, const double *pts, cudaStream_t s, const
     ba.prefix = reinterpret_cast<int32_t *>(b.kx);
     ba.blocksum = b.blocksum;
     if (n <= BUILD_SINGLE_MAX) {
-        build_levels_kernel<BUILD_SINGLE_THREADS, BUILD_ONE_CTA><<<1, BUILD_SINGLE_THREADS, 0, s>>>(ba);
+        MDC_CHECK_CUDA(launch_pdl(build_levels_kernel<BUILD_SINGLE_THREADS, BUILD_ONE_CTA>, dim3(1),
+                                  dim3(BUILD_SINGLE_THREADS), s, ba));
         MDC_CHECK_LAUNCH();
     } else if (n <= BUILD_CLUSTER_MAX && p->cluster_ok) {
         const bool sub = MDC_BUILD_CLUSTER_SUB && p->subtree_l0 >= 0;
@@ -1560,8 +1611,10 @@ static int build_tree(MdcLayoutPlan *p, const double *pts, cudaStream_t s, const
         cfg.numAttrs = 1;
         MDC_CHECK_CUDA(cudaLaunchKernelEx(&cfg, build_levels_kernel<BUILD_CLUSTER_THREADS, BUILD_ONE_CLUSTER>, ba));
         if (sub) {
-            build_subtree_kernel<<<p->subtree_nseg, SUBTREE_THREADS, 0, s>>>(ba, p->subtree_l0);
-            centroid_kernel<<<(unsigned)(((int64_t)ba.nnodes * 32 + 255) / 256), 256, 0, s>>>(ba);
+            MDC_CHECK_CUDA(launch_pdl(build_subtree_kernel, dim3(p->subtree_nseg), dim3(SUBTREE_THREADS), s, ba,
+                                      p->subtree_l0));
+            MDC_CHECK_CUDA(launch_pdl(centroid_kernel, dim3((unsigned)(((int64_t)ba.nnodes * 32 + 255) / 256)),
+                                      dim3(256), s, ba));
             MDC_CHECK_LAUNCH();
         }
     } else {
@@ -1570,8 +1623,10 @@ static int build_tree(MdcLayoutPlan *p, const double *pts, cudaStream_t s, const
         MDC_CHECK_CUDA(cudaLaunchCooperativeKernel((const void *)build_levels_kernel<BUILD_THREADS, BUILD_GRID>,
                                                    dim3(p->build_blocks), dim3(BUILD_THREADS), kargs, 0, s));
         if (p->subtree_l0 >= 0) {
-            build_subtree_kernel<<<p->subtree_nseg, SUBTREE_THREADS, 0, s>>>(ba, p->subtree_l0);
-            centroid_kernel<<<(unsigned)(((int64_t)ba.nnodes * 32 + 255) / 256), 256, 0, s>>>(ba);
+            MDC_CHECK_CUDA(launch_pdl(build_subtree_kernel, dim3(p->subtree_nseg), dim3(SUBTREE_THREADS), s, ba,
+                                      p->subtree_l0));
+            MDC_CHECK_CUDA(launch_pdl(centroid_kernel, dim3((unsigned)(((int64_t)ba.nnodes * 32 + 255) / 256)),
+                                      dim3(256), s, ba));
             MDC_CHECK_LAUNCH();
         }
     }
@@ -1602,9 +1657,11 @@ static int run_bh(MdcLayoutPlan *p, const double *pts, double *out, cudaStream_t
         if (p->count)
             bh_kernel<true><<<grid, BH_WARPS * 32, 0, s>>>(n, k0, k1, p->b.t, p->a.c, p->a.eta, p->a.theta, p->count);
         else
-            bh_kernel<false><<<grid, BH_WARPS * 32, 0, s>>>(n, k0, k1, p->b.t, p->a.c, p->a.eta, p->a.theta, nullptr);
+            MDC_CHECK_CUDA(launch_pdl(bh_kernel<false>, grid, dim3(BH_WARPS * 32), s, n, k0, k1, p->b.t, p->a.c,
+                                      p->a.eta, p->a.theta, (unsigned long long *)nullptr));
         p->mark(s);  // traversal done
-        bh_combine_kernel<<<(unsigned)((k1 - k0 + 255) / 256), 256, 0, s>>>(n, k0, k1, p->b.t, perm, out);
+        MDC_CHECK_CUDA(launch_pdl(bh_combine_kernel, dim3((unsigned)((k1 - k0 + 255) / 256)), dim3(256), s, n, k0,
+                                  k1, p->b.t, perm, out));
         p->mark(s);  // combine done
     }
     MDC_CHECK_LAUNCH();
@@ -1663,13 +1720,14 @@ static int enqueue_step(MdcLayoutPlan *p, const double *pin, double *pout, const
     }
 #if MDC_LOCAL_LG
     if (la.k1 > la.k0 && la.k1 - la.k0 <= MDC_LOCAL_LG_MAXN)
-        local_group_kernel<MDC_LOCAL_LG>
-            <<<(unsigned)(((la.k1 - la.k0) * MDC_LOCAL_LG + 127) / 128), 128, 0, s>>>(la);
+        MDC_CHECK_CUDA(launch_pdl(local_group_kernel<MDC_LOCAL_LG>,
+                                  dim3((unsigned)(((la.k1 - la.k0) * MDC_LOCAL_LG + 127) / 128)), dim3(128), s, la));
     else
 #endif
-        if (la.k1 > la.k0) local_kernel<<<(unsigned)((la.k1 - la.k0 + 127) / 128), 128, 0, s>>>(la);
+        if (la.k1 > la.k0)
+            MDC_CHECK_CUDA(launch_pdl(local_kernel, dim3((unsigned)((la.k1 - la.k0 + 127) / 128)), dim3(128), s, la));
     p->mark(s);  // local forces + update done
-    incr_kernel<<<1, 1, 0, s>>>(p->b.ctr);
+    MDC_CHECK_CUDA(launch_pdl(incr_kernel, dim3(1), dim3(1), s, p->b.ctr));
     MDC_CHECK_LAUNCH();
     return MDC_OK;
 }

@@ -138,10 +138,12 @@ def test_g2k_field(g2k):
 
 @pytest.mark.parametrize("n,d,W,H,alpha", [(3000, 32, 96, 64, 1.5), (2000, 8, 64, 40, 1.0),
                                            (2500, 16, 70, 48, 1.3), (1800, 40, 64, 64, 1.5),
-                                           (1000, 70, 48, 40, 2.0), (777, 24, 50, 30, 0.5)])
+                                           (1000, 70, 48, 40, 2.0), (777, 24, 50, 30, 0.5),
+                                           (1200, 64, 48, 40, 1.3), (900, 200, 40, 30, 1.5)])
 def test_tensor_core_path_vs_oracle_and_simt(n, d, W, H, alpha):
-    """tcgen05 3xTF32 pass 2 (fp32 affine, d >= 8) against the fp64 oracle at
-    the fp32 contract and against the SIMT kernel."""
+    """tcgen05 pass 2 (fp32 affine, d >= 8: 3xTF32 for 16/32-channel chunks,
+    tf32 + bf16 corrections with fp32 run totals for 64/128-channel chunks)
+    against the fp64 oracle at the fp32 contract and against the SIMT kernel."""
     rng = np.random.default_rng(n * 7 + d)
     pos = rng.normal(0, 3, (n, 2))
     q = rng.normal(0, 1, (n, d)) + np.sin(pos[:, :1] * np.arange(1, d + 1) * 0.3)
