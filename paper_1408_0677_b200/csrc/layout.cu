@@ -29,6 +29,13 @@
 
 #include "common.cuh"
 
+#ifndef MDC_BH_SMALL_N
+#define MDC_BH_SMALL_N 0  // meshes up to this size split BH into 2^MDC_BH_CUT_SMALL tasks
+#endif
+#ifndef MDC_BH_CUT_SMALL
+#define MDC_BH_CUT_SMALL 6
+#endif
+
 namespace mdc {
 
 // ---------------------------------------------------------------------------
@@ -107,7 +114,10 @@ static void make_shape(TreeShape &t, int64_t n, int leaf) {
         int min_leaf_depth = t.max_depth;
         for (int i = 0; i < nn; ++i)
             if (t.left[i] < 0) min_leaf_depth = std::min(min_leaf_depth, t.depth[i]);
-        t.cut = std::min(4, min_leaf_depth);
+        // more, smaller tasks for small meshes: the walk is latency-bound and
+        // ceil(n / 32) point-warps x 16 tasks do not fill the GPU below ~20k points
+        const int want = n <= MDC_BH_SMALL_N ? MDC_BH_CUT_SMALL : 4;
+        t.cut = std::min(want, min_leaf_depth);
         for (int i = 0; i < nn; ++i)
             if (t.depth[i] == t.cut) t.task_node.push_back(i);
         std::sort(t.task_node.begin(), t.task_node.end(), [&](int32_t a, int32_t b) { return t.lo[a] < t.lo[b]; });
