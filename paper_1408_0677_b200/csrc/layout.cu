@@ -30,7 +30,7 @@
 #include "common.cuh"
 
 #ifndef MDC_BH_SMALL_N
-#define MDC_BH_SMALL_N 0  // meshes up to this size split BH into 2^MDC_BH_CUT_SMALL tasks
+#define MDC_BH_SMALL_N 200000  // meshes up to this size split BH into 2^MDC_BH_CUT_SMALL tasks (else 16)
 #endif
 #ifndef MDC_BH_CUT_SMALL
 #define MDC_BH_CUT_SMALL 6
