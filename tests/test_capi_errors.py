@@ -43,6 +43,9 @@ def _mls_args(**kw):
     (dict(ldq=3), "ldq"),
     (dict(ldq=5), "ldq"),
     (dict(q=FAKE + 4), "aligned"),
+    (dict(rgba=FAKE), "palette"),
+    (dict(rgba=FAKE, spacing=FAKE), "palette"),
+    (dict(rgba=FAKE, spacing=FAKE, palette=FAKE, palette_n=0), "palette"),
 ])
 def test_mls_field_rejects_bad_arguments(kw, msg):
     lib = _lib.load()
@@ -58,6 +61,10 @@ def test_other_entry_points_reject_bad_arguments():
     la.n, la.leaf = 0, 32
     h = ctypes.c_void_p()
     assert lib.mdc_layout_plan_create(ctypes.byref(la), ctypes.byref(h), None) == EINVAL and "n out of range" in _err(lib)
+    assert lib.mdc_layout_set_gather(None, FAKE) == EINVAL and "null" in _err(lib)
+    assert lib.mdc_layout_scatter(None, FAKE, 1, None) == EINVAL and "null" in _err(lib)
+    assert lib.mdc_rigid_field_norm(1, FAKE, FAKE, 2, FAKE, FAKE, FAKE, FAKE, 1.0, FAKE, None, None) == EINVAL
+    assert "norm_out" in _err(lib)
     la.n, la.leaf = 10, 0
     assert lib.mdc_layout_plan_create(ctypes.byref(la), ctypes.byref(h), None) == EINVAL and "leaf" in _err(lib)
     la.leaf = 32
