@@ -199,6 +199,12 @@ struct Buffers {
     int32_t *ctr;
     void *cub_tmp;
     size_t cub_bytes;
+    // bucket rank sort (MDC_SORT_BUCKET): 2B+1 bucket counts (all-zero between
+    // steps) and starts, each element's bucket, ids in bucket order, and the
+    // per-axis min/max order keys (reset to {~0, 0} between steps)
+    int64_t nbucket;  // B per axis
+    int32_t *bk_hist, *bk_start, *bk_of, *bk_slot;
+    unsigned long long *bk_mm;
 };
 
 constexpr int SCAN_BLOCK = 1024;
@@ -208,6 +214,21 @@ static size_t cub_sort_bytes(int64_t n) {
     cub::DeviceRadixSort::SortPairs(nullptr, bytes, (unsigned long long *)nullptr,
                                     (unsigned long long *)nullptr, (int32_t *)nullptr,
                                     (int32_t *)nullptr, (int)(2 * n), 0, 32);
+    return bytes;
+}
+
+#ifndef MDC_SORT_BUCKET
+#define MDC_SORT_BUCKET 1  // bucket rank sort (exact (coord, id) order) instead of the radix / count ranks + fixup
+#endif
+#ifndef MDC_SORT_BUCKET_OCC
+#define MDC_SORT_BUCKET_OCC 2  // mean elements per bucket
+#endif
+
+static int64_t sort_buckets(int64_t n) { return std::max<int64_t>(1, n / MDC_SORT_BUCKET_OCC); }
+
+static size_t cub_scan_bytes(int64_t items) {
+    size_t bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, bytes, (int32_t *)nullptr, (int32_t *)nullptr, (int)items);
     return bytes;
 }
 
@@ -265,7 +286,13 @@ static size_t carve(Buffers &b, char *base, const TreeShape &s) {
     b.pos_b = c.take<double>(2 * n);
     b.bh = c.take<double>(2 * n);
     b.ctr = c.take<int32_t>(4);
-    b.cub_bytes = cub_sort_bytes(n);
+    b.nbucket = sort_buckets(n);
+    b.bk_hist = c.take<int32_t>(2 * b.nbucket + 1);
+    b.bk_start = c.take<int32_t>(2 * b.nbucket + 1);
+    b.bk_of = c.take<int32_t>(2 * n);
+    b.bk_slot = c.take<int32_t>(2 * n);
+    b.bk_mm = c.take<unsigned long long>(4);
+    b.cub_bytes = std::max(cub_sort_bytes(n), cub_scan_bytes(2 * b.nbucket + 1));
     b.cub_tmp = c.take<char>(b.cub_bytes);
     return c.off + 256;
 }
@@ -432,6 +459,125 @@ __global__ void rank_scatter_kernel(const double *pts, int64_t n, int32_t *rank,
     keys_out[dst] = axis_key32(pts, i, axis);
     ids_out[dst] = (int32_t)i;
     rank[k] = 0;  // ready for the next step
+}
+
+// Bucket rank sort: the exact (coord, id) order of both axes without radix
+// passes or a float-key fixup.  The bucket of x is floor(B (x - lo)/(hi - lo))
+// -- a composition of correctly rounded monotone operations, so buckets are
+// non-decreasing in x -- and an element's final slot is its bucket's start
+// plus its rank among the bucket's members under the exact key.  With B = n/2
+// buckets over [lo, hi] a bucket holds a few points; the in-bucket rank is a
+// loop over the members (a bucket of m points costs m^2 compares: dense
+// clusters are slower, never wrong).
+__device__ __forceinline__ double key_to_double(unsigned long long k) {
+    return __longlong_as_double((long long)((k & 0x8000000000000000ULL) ? (k & ~0x8000000000000000ULL) : ~k));
+}
+
+__device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = min(v, (unsigned long long)__shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = max(v, (unsigned long long)__shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+constexpr int BK_THREADS = 256;
+
+__global__ void __launch_bounds__(BK_THREADS) bucket_minmax_kernel(const double *pts, int64_t n,
+                                                                   unsigned long long *mm) {
+    pdl_wait();
+    __shared__ unsigned long long s_mm[4];
+    if (threadIdx.x < 4) s_mm[threadIdx.x] = (threadIdx.x & 1) ? 0ULL : ~0ULL;
+    __syncthreads();
+    unsigned long long lo[2] = {~0ULL, ~0ULL}, hi[2] = {0ULL, 0ULL};
+    for (int64_t i = (int64_t)blockIdx.x * BK_THREADS + threadIdx.x; i < n; i += (int64_t)gridDim.x * BK_THREADS) {
+        const double2 p = reinterpret_cast<const double2 *>(pts)[i];
+        const unsigned long long kx = order_key(p.x), ky = order_key(p.y);
+        lo[0] = min(lo[0], kx);
+        hi[0] = max(hi[0], kx);
+        lo[1] = min(lo[1], ky);
+        hi[1] = max(hi[1], ky);
+    }
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+        lo[a] = warp_min_u64(lo[a]);
+        hi[a] = warp_max_u64(hi[a]);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(&s_mm[0], lo[0]);
+        atomicMax(&s_mm[1], hi[0]);
+        atomicMin(&s_mm[2], lo[1]);
+        atomicMax(&s_mm[3], hi[1]);
+    }
+    __syncthreads();
+    if (threadIdx.x < 4) {
+        if (threadIdx.x & 1)
+            atomicMax(&mm[threadIdx.x], s_mm[threadIdx.x]);
+        else
+            atomicMin(&mm[threadIdx.x], s_mm[threadIdx.x]);
+    }
+}
+
+__device__ __forceinline__ int bucket_of(double x, double lo, double hi, int64_t B) {
+    if (!(hi > lo)) return 0;
+    const double t = __dmul_rn(__ddiv_rn(__dsub_rn(x, lo), __dsub_rn(hi, lo)), (double)B);
+    return (int)fmin(fmax(t, 0.0), (double)(B - 1));
+}
+
+__global__ void __launch_bounds__(BK_THREADS) bucket_count_kernel(const double *pts, int64_t n, int64_t B,
+                                                                  const unsigned long long *mm, int32_t *hist,
+                                                                  int32_t *bk_of) {
+    pdl_wait();
+    const int64_t e = (int64_t)blockIdx.x * BK_THREADS + threadIdx.x;
+    if (e >= 2 * n) return;
+    const int axis = e >= n;
+    const double x = pts[2 * (e - axis * n) + axis];
+    const int g = (int)(axis * B) + bucket_of(x, key_to_double(mm[2 * axis]), key_to_double(mm[2 * axis + 1]), B);
+    bk_of[e] = g;
+    atomicAdd(hist + g, 1);
+}
+
+// Place every element in its bucket (any order inside it); the atomic
+// decrements leave the counts at zero for the next step.
+__global__ void __launch_bounds__(BK_THREADS) bucket_scatter_kernel(int64_t n, const int32_t *bk_of,
+                                                                    const int32_t *start, int32_t *hist,
+                                                                    int32_t *slot, unsigned long long *mm) {
+    pdl_wait();
+    const int64_t e = (int64_t)blockIdx.x * BK_THREADS + threadIdx.x;
+    if (e == 0) {
+        mm[0] = mm[2] = ~0ULL;
+        mm[1] = mm[3] = 0ULL;
+    }
+    if (e >= 2 * n) return;
+    const int g = bk_of[e];
+    const int pos = start[g] + atomicSub(hist + g, 1) - 1;
+    slot[pos] = (int32_t)e;  // axis * n + id
+}
+
+// Final slot = bucket start + rank under the exact (coord, id) key among the
+// bucket's members; ids land in xs0 (x run, then y run) as the sort writes them.
+__global__ void __launch_bounds__(BK_THREADS) bucket_rank_kernel(const double *pts, int64_t n,
+                                                                 const int32_t *bk_of, const int32_t *start,
+                                                                 const int32_t *slot, int32_t *xs0) {
+    pdl_wait();
+    const int64_t p = (int64_t)blockIdx.x * BK_THREADS + threadIdx.x;
+    if (p >= 2 * n) return;
+    const int e = slot[p];
+    const int axis = e >= n;
+    const int id = e - axis * (int)n;
+    const int g = bk_of[e];
+    const int s0 = start[g], s1 = start[g + 1];
+    const unsigned long long k = order_key(pts[2 * id + axis]);
+    int r = 0;
+    for (int q = s0; q < s1; ++q) {
+        const int j = slot[q] - axis * (int)n;
+        const unsigned long long kj = order_key(pts[2 * j + axis]);
+        r += (kj < k) || (kj == k && j < id);
+    }
+    xs0[s0 + r] = id;
 }
 
 // ---------------------------------------------------------------------------
@@ -1563,7 +1709,22 @@ static int build_tree(MdcLayoutPlan *p, const double *pts, cudaStream_t s, const
     // runs (a one-CTA 64-bit block sort was tried for small n: 143 us at any n
     // up to 12k vs ~25 us for this path)
     const int nb2 = (int)((2 * n + 255) / 256);
-    if (n <= MDC_RANK_SORT_MAX) {
+    if (MDC_SORT_BUCKET) {
+        const int64_t B = b.nbucket;
+        const int nmm = (int)std::min<int64_t>((n + BK_THREADS - 1) / BK_THREADS, 4 * (int64_t)p->sms);
+        MDC_CHECK_CUDA(launch_pdl(bucket_minmax_kernel, dim3(nmm), dim3(BK_THREADS), s, pts, n, b.bk_mm));
+        MDC_CHECK_CUDA(launch_pdl(bucket_count_kernel, dim3(nb2), dim3(BK_THREADS), s, pts, n, B,
+                                  (const unsigned long long *)b.bk_mm, b.bk_hist, b.bk_of));
+        size_t bytes = b.cub_bytes;
+        MDC_CHECK_CUDA(cub::DeviceScan::ExclusiveSum(b.cub_tmp, bytes, b.bk_hist, b.bk_start, (int)(2 * B + 1), s));
+        MDC_CHECK_CUDA(launch_pdl(bucket_scatter_kernel, dim3(nb2), dim3(BK_THREADS), s, n,
+                                  (const int32_t *)b.bk_of, (const int32_t *)b.bk_start, b.bk_hist, b.bk_slot,
+                                  b.bk_mm));
+        MDC_CHECK_CUDA(launch_pdl(bucket_rank_kernel, dim3(nb2), dim3(BK_THREADS), s, pts, n,
+                                  (const int32_t *)b.bk_of, (const int32_t *)b.bk_start, (const int32_t *)b.bk_slot,
+                                  b.xs[0]));
+        MDC_CHECK_LAUNCH();
+    } else if (n <= MDC_RANK_SORT_MAX) {
         // b.rank (2n) is all-zero between steps: the scatter clears it
         const int bx = (int)((n + RANK_THREADS - 1) / RANK_THREADS);
         int chunks = (4 * p->sms + 2 * bx - 1) / (2 * bx);
@@ -1581,11 +1742,13 @@ static int build_tree(MdcLayoutPlan *p, const double *pts, cudaStream_t s, const
         MDC_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(b.cub_tmp, bytes, b.kx, b.kx_out, b.ids, b.xs[0],
                                                        (int)(2 * n), 0, 32, s));
     }
-    MDC_CHECK_CUDA(launch_pdl(run_mark_kernel, dim3(nb2), dim3(256), s, n, (const unsigned long long *)b.kx_out,
-                              (const int32_t *)b.xs[0], pts, b.runflag));
-    MDC_CHECK_CUDA(launch_pdl(run_sort_kernel, dim3(nb2), dim3(256), s, n, (const unsigned long long *)b.kx_out,
-                              b.xs[0], pts, b.runflag));
-    MDC_CHECK_LAUNCH();
+    if (!MDC_SORT_BUCKET) {
+        MDC_CHECK_CUDA(launch_pdl(run_mark_kernel, dim3(nb2), dim3(256), s, n,
+                                  (const unsigned long long *)b.kx_out, (const int32_t *)b.xs[0], pts, b.runflag));
+        MDC_CHECK_CUDA(launch_pdl(run_sort_kernel, dim3(nb2), dim3(256), s, n,
+                                  (const unsigned long long *)b.kx_out, b.xs[0], pts, b.runflag));
+        MDC_CHECK_LAUNCH();
+    }
     p->mark(s);  // sorts done
     BuildArgs ba;
     ba.pts = pts;
@@ -1838,6 +2001,10 @@ extern "C" int mdc_layout_plan_create(const MdcLayoutArgs *a, MdcLayoutPlan **pl
     }
     cudaMemsetAsync(p->b.runflag, 0, sizeof(int32_t) * 2 * (size_t)p->shape.n, s);
     cudaMemsetAsync(p->b.rank, 0, sizeof(int32_t) * 2 * (size_t)p->shape.n, s);
+    cudaMemsetAsync(p->b.bk_hist, 0, sizeof(int32_t) * (2 * (size_t)p->b.nbucket + 1), s);
+    cudaMemsetAsync(p->b.bk_mm, 0xFF, 4 * sizeof(unsigned long long), s);
+    cudaMemsetAsync(p->b.bk_mm + 1, 0, sizeof(unsigned long long), s);
+    cudaMemsetAsync(p->b.bk_mm + 3, 0, sizeof(unsigned long long), s);
     // host vectors must outlive the async copies
     cudaError_t e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) {

@@ -194,22 +194,34 @@ def test_vertex_partition_reassembles_bit_identically(g2k):
     assert normwise(pos.cpu().numpy(), g2k["states"][5]) <= FREE_TOL
 
 
-@pytest.mark.parametrize("kind", ["float_collisions", "long_run"])
-def test_kdtree_device_sort_exact_order(kind):
-    """n > 12288 takes the device radix sort on 33-bit float keys: runs of
-    distinct doubles that share a float key (and exact ties) must still end
-    up in exact (coord, id) order -- checked through the kd-tree membership
-    against the oracle."""
+@pytest.mark.parametrize("kind,n", [("float_collisions", 20000), ("long_run", 20000), ("float_collisions", 3000),
+                                    ("signed_zero", 5000), ("constant_x", 4000), ("outlier_cluster", 20000)])
+def test_kdtree_device_sort_exact_order(kind, n):
+    """The device sort (bucket ranks, MDC_SORT_BUCKET) must give the exact
+    (coord, id) order whatever the distribution: distinct doubles sharing a
+    float, exact ties, -0.0 vs +0.0, a constant column (one bucket), a far
+    outlier squeezing the rest into a few buckets -- checked through the
+    kd-tree membership against the oracle."""
     rng = np.random.default_rng(7)
-    n = 20000
+    y = rng.normal(0, 3, n)
     if kind == "float_collisions":
         base = rng.normal(0, 3, n // 8)
         x = np.repeat(base, 8) * (1 + rng.integers(-3, 4, n) * 2.0 ** -45)  # same float, distinct doubles
-        y = rng.normal(0, 3, n)
         x[::97] = x[0]  # exact ties as well
-    else:
+    elif kind == "long_run":
         x = 1.0 + rng.integers(0, 4000, n) * 2.0 ** -40  # one float key, a 20000-long run
         y = rng.normal(0, 1, n)
+    elif kind == "signed_zero":
+        x = rng.normal(0, 1, n)
+        x[rng.integers(0, n, n // 4)] = 0.0
+        x[rng.integers(0, n, n // 4)] = -0.0
+        y[::3] = -0.0
+    elif kind == "constant_x":
+        x = np.full(n, 0.75)
+    else:
+        x = rng.normal(0, 1e-3, n)
+        x[123] = 1e6
+        y[77] = -1e9
     pts = np.column_stack([x, y])
     gt = bhtree.KdTree(pts, leaf_size=32)
     ot = O.KdTree(pts, leaf_size=32)
