@@ -48,8 +48,17 @@ __device__ __forceinline__ void run_flush(T &part, double &tot) {
 // ------------------------------------------------------------------------------
 // The fused kernel.  VAR: MDC_MEAN / MDC_AFFINE / MDC_RIGID; DC: channels per
 // pass-2 chunk; R: pixels per thread.
+// fp64 with 32-channel chunks: one pass 2 for d <= 32 (instead of two
+// 16-channel passes, each re-evaluating the weights); 135 KB of staged
+// controls, so one CTA per SM and the whole register file for it.
+#ifndef MDC_F64_DC32
+#define MDC_F64_DC32 2  // pixels per thread for the fp64 32-channel instantiation (0: off; A/B at config 3: 16-ch chunks 41.0, R = 1 49.2, R = 2 56.4 Mpixel*dim/s)
+#endif
+template <typename T, int DC>
+constexpr int mls_minb() { return (sizeof(T) == 8 && DC == 32) ? 1 : MDC_MLS_MINB; }
+
 template <typename T, int VAR, int AM, int DC, int R>
-__global__ void __launch_bounds__(NT, MDC_MLS_MINB) mls_kernel(KArgs a) {
+__global__ void __launch_bounds__(NT, mls_minb<T, DC>()) mls_kernel(KArgs a) {
     using T2 = typename V2<T>::type;
     constexpr int QE = Stager<T, DC>::QV * 16 / (int)sizeof(T);  // padded channels per control
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -546,6 +555,10 @@ static int dispatch_dc(const KArgs &k, cudaStream_t s) {
         // fp32 keeps fp64 run totals per channel in registers: chunks of 8
         return launch_t<T, VAR, AM, 8, R>(k, s);
     } else {
+#if MDC_F64_DC32
+        if (VAR == MDC_AFFINE && d > 16 && k.ldq >= ((d + 31) / 32) * 32)
+            return launch_t<T, VAR, AM, 32, MDC_F64_DC32>(k, s);
+#endif
         return launch_t<T, VAR, AM, 16, R>(k, s);
     }
 }
