@@ -1540,7 +1540,10 @@ __global__ void incr_kernel(int32_t *ctr) {
 #ifndef MDC_LAYOUT_SMALL_MAX
 #define MDC_LAYOUT_SMALL_MAX 512  // one CTA only pays off for tiny meshes (n = 2000: 1.9 ms vs ~0.1 ms per step)
 #endif
-constexpr int SMALL_THREADS = 512;
+#ifndef MDC_SMALL_THREADS
+#define MDC_SMALL_THREADS 512
+#endif
+constexpr int SMALL_THREADS = MDC_SMALL_THREADS;
 #ifndef MDC_SMALL_LG
 #define MDC_SMALL_LG MDC_LOCAL_LG  // lanes per vertex in the persistent step's local update
 #endif
