@@ -123,6 +123,25 @@ def test_fused_vs_oracle_larger(n, d, W, H, alpha):
         assert normwise(vals[k], ref) <= FP32_TOL, k
 
 
+@pytest.mark.parametrize("n,d,W,H,alpha", [(1200, 20, 48, 40, 1.5), (1500, 33, 40, 36, 1.5),
+                                           (1000, 64, 36, 30, 1.5), (900, 48, 40, 24, 1.3)])
+def test_fp64_channel_chunks_vs_oracle(n, d, W, H, alpha):
+    """fp64 parity mode across its channel-chunk paths: 32-channel chunks
+    (d = 20 padded to 32, d = 33 and 64 in two chunks) and 16-channel chunks
+    where the padded stride is not a multiple of 32 (d = 48), all channels,
+    within the 1e-10 contract."""
+    rng = np.random.default_rng(n + d)
+    pos = rng.normal(0, 3, (n, 2))
+    q = rng.normal(0, 1, (n, d)) + pos[:, 1:] * np.linspace(-1, 1, d)
+    blk = F.compute_fields(pos, q, F.MlsParams("affine", alpha=alpha), W, H, dtype="f64")
+    blk.check_finite()
+    vals = blk.values.cpu().numpy()
+    for k in range(d):
+        tv = np.column_stack([q[:, k], np.zeros(n)])
+        ref = O.compute_field(pos, tv, "affine", W, H, alpha=alpha)[..., 0]
+        assert normwise(vals[k], ref) <= FP64_TOL, k
+
+
 def test_rigid_single_channel_rejected(c1):
     tv = F.TargetAssignment(targets=c1["targets_affine_dim0"], mode="dims", dims=("a",))
     with pytest.raises(F.FieldError):
