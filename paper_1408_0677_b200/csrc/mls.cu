@@ -54,6 +54,13 @@ __device__ __forceinline__ void run_flush(T &part, double &tot) {
 #ifndef MDC_F64_DC32
 #define MDC_F64_DC32 2  // pixels per thread for the fp64 32-channel instantiation (0: off; A/B at config 3: 16-ch chunks 41.0, R = 1 49.2, R = 2 56.4 Mpixel*dim/s)
 #endif
+#ifndef MDC_SIMT_P1_UNROLL
+#define MDC_SIMT_P1_UNROLL 8  // control-loop unroll of the scalar (fp64) passes (A/B, fp64 config 3: 2 55.9, 4 56.5, 8 57.6)
+#endif
+#ifndef MDC_SIMT_P2_UNROLL
+#define MDC_SIMT_P2_UNROLL 2
+#endif
+constexpr int SIMT_P1U = MDC_SIMT_P1_UNROLL, SIMT_P2U = MDC_SIMT_P2_UNROLL;
 template <typename T, int DC>
 constexpr int mls_minb() { return (sizeof(T) == 8 && DC == 32) ? 1 : MDC_MLS_MINB; }
 
@@ -167,7 +174,7 @@ __global__ void __launch_bounds__(NT, mls_minb<T, DC>()) mls_kernel(KArgs a) {
                 tsxy[0] += xy2.x; tsxy[1] += xy2.y;
                 tsyy[0] += yy2.x; tsyy[1] += yy2.y;
             } else {
-#pragma unroll 4
+#pragma unroll SIMT_P1U
                 for (int j = 0; j < cnt; ++j) {
                     T2 p = sxy[j];
 #pragma unroll
@@ -262,7 +269,7 @@ __global__ void __launch_bounds__(NT, mls_minb<T, DC>()) mls_kernel(KArgs a) {
                         tacc[1][k] += acc2[k].y;
                     }
                 } else {
-#pragma unroll 2
+#pragma unroll SIMT_P2U
                     for (int j = 0; j < cnt; ++j) {
                         T2 p = sxy[j];
                         T qv[DC];

@@ -20,7 +20,7 @@ X = bench.gmm(cfg["n"], cfg["d"], cfg["seed"])
 ds = D.normalize(D.Dataset(names=[f"d{i}" for i in range(cfg["d"])], data=X))
 _, cloud = P.pca_project(ds)
 raw = np.column_stack([ds.raw_column(nm) for nm in ds.names])
-W, H, rows = cfg["W"], cfg["H"], 16
+W, H, rows = cfg["W"], cfg["H"], int(os.environ.get("MDC_PROF_ROWS", "16"))
 prob = F.MlsProblem(cloud.positions, raw, "affine", W, H, dtype="f64")
 out = torch.empty((cfg["d"], rows, W), dtype=torch.float64, device="cuda")
 a = prob.args(out, (rows * W, W, 1), H // 2, H // 2 + rows)
