@@ -16,5 +16,7 @@ ncu --set full --import-source on --clock-control none -k regex:bh_kernel -s 20 
     python bench.py --steps 1 --warmup 0 --no-cpu --no-e2e --no-fp64 --layout-iters 30 > gpurun_out/ncu_bh.log 2>&1
 ncu --set full --import-source on --clock-control none -k regex:"^local_kernel" -s 3 -c 1 -o gpurun_out/local_full -f \
     python tools/prof_layout.py 3 > gpurun_out/ncu_local.log 2>&1
+MDC_PROF_ROWS=64 ncu --set full --import-source on --clock-control none -k regex:mls_kernel -c 1 -o gpurun_out/mls_f64_full -f \
+    python tools/prof_fp64.py > gpurun_out/ncu_f64.log 2>&1
 python -m pytest tests/test_gpu_parity_report.py tests/test_gpu_bench_parity.py -q -s -m gpu -p no:cacheprovider > gpurun_out/parity.log 2>&1
 ls -la gpurun_out
