@@ -205,6 +205,7 @@ struct Buffers {
     int64_t nbucket;  // B per axis
     int32_t *bk_hist, *bk_start, *bk_of, *bk_slot;
     unsigned long long *bk_mm;
+    unsigned long long *bk_split;  // sorted sample keys, 1024 per axis
 };
 
 constexpr int SCAN_BLOCK = 1024;
@@ -224,7 +225,8 @@ static size_t cub_sort_bytes(int64_t n) {
 #define MDC_SORT_BUCKET_OCC 2  // mean elements per bucket
 #endif
 
-static int64_t sort_buckets(int64_t n) { return std::max<int64_t>(1, n / MDC_SORT_BUCKET_OCC); }
+// 1024 sample intervals x F linear sub-buckets per axis, ~OCC points per bucket
+static int64_t sort_buckets(int64_t n) { return 1024 * std::max<int64_t>(1, n / (1024 * MDC_SORT_BUCKET_OCC)); }
 
 static size_t cub_scan_bytes(int64_t items) {
     size_t bytes = 0;
@@ -292,6 +294,7 @@ static size_t carve(Buffers &b, char *base, const TreeShape &s) {
     b.bk_of = c.take<int32_t>(2 * n);
     b.bk_slot = c.take<int32_t>(2 * n);
     b.bk_mm = c.take<unsigned long long>(4);
+    b.bk_split = c.take<unsigned long long>(2 * 1024);
     b.cub_bytes = std::max(cub_sort_bytes(n), cub_scan_bytes(2 * b.nbucket + 1));
     b.cub_tmp = c.take<char>(b.cub_bytes);
     return c.off + 256;
@@ -462,13 +465,16 @@ __global__ void rank_scatter_kernel(const double *pts, int64_t n, int32_t *rank,
 }
 
 // Bucket rank sort: the exact (coord, id) order of both axes without radix
-// passes or a float-key fixup.  The bucket of x is floor(B (x - lo)/(hi - lo))
-// -- a composition of correctly rounded monotone operations, so buckets are
-// non-decreasing in x -- and an element's final slot is its bucket's start
-// plus its rank among the bucket's members under the exact key.  With B = n/2
-// buckets over [lo, hi] a bucket holds a few points; the in-bucket rank is a
-// loop over the members (a bucket of m points costs m^2 compares: dense
-// clusters are slower, never wrong).
+// passes or a float-key fixup.  Two-level buckets, non-decreasing in x under
+// the exact key: the interval between consecutive keys of a regular sample
+// (S = 1024, sorted per axis), then F ~ n / 2S linear sub-buckets inside it
+// (correctly rounded monotone operations; the end intervals run to the axis
+// min / max).  The sample adapts the coarse level to the data's density, so
+// outliers or clusters do not squeeze the bulk into a few buckets, and the
+// linear level leaves ~2 points per bucket.  An element's final slot is its
+// bucket's start plus its rank among the bucket's members under the exact
+// (coord, id) key (a bucket of m points costs m^2 compares: exact ties
+// concentrate -- slower, never wrong).
 __device__ __forceinline__ double key_to_double(unsigned long long k) {
     return __longlong_as_double((long long)((k & 0x8000000000000000ULL) ? (k & ~0x8000000000000000ULL) : ~k));
 }
@@ -486,14 +492,12 @@ __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v)
 
 constexpr int BK_THREADS = 256;
 
-__global__ void __launch_bounds__(BK_THREADS) bucket_minmax_kernel(const double *pts, int64_t n,
-                                                                   unsigned long long *mm) {
-    pdl_wait();
-    __shared__ unsigned long long s_mm[4];
+__device__ __forceinline__ void bucket_minmax(const double *pts, int64_t n, unsigned long long *mm, int blk,
+                                              int nblk, unsigned long long *s_mm) {
     if (threadIdx.x < 4) s_mm[threadIdx.x] = (threadIdx.x & 1) ? 0ULL : ~0ULL;
     __syncthreads();
     unsigned long long lo[2] = {~0ULL, ~0ULL}, hi[2] = {0ULL, 0ULL};
-    for (int64_t i = (int64_t)blockIdx.x * BK_THREADS + threadIdx.x; i < n; i += (int64_t)gridDim.x * BK_THREADS) {
+    for (int64_t i = (int64_t)blk * blockDim.x + threadIdx.x; i < n; i += (int64_t)nblk * blockDim.x) {
         const double2 p = reinterpret_cast<const double2 *>(pts)[i];
         const unsigned long long kx = order_key(p.x), ky = order_key(p.y);
         lo[0] = min(lo[0], kx);
@@ -521,21 +525,82 @@ __global__ void __launch_bounds__(BK_THREADS) bucket_minmax_kernel(const double 
     }
 }
 
-__device__ __forceinline__ int bucket_of(double x, double lo, double hi, int64_t B) {
-    if (!(hi > lo)) return 0;
-    const double t = __dmul_rn(__ddiv_rn(__dsub_rn(x, lo), __dsub_rn(hi, lo)), (double)B);
-    return (int)fmin(fmax(t, 0.0), (double)(B - 1));
+// Sample splitters (one CTA per axis): S = 1024 order keys at ids s n / S,
+// bitonic-sorted (shared memory for partner distances >= 32, shuffles below).
+constexpr int BK_SAMPLE = 1024;
+__device__ __forceinline__ void bucket_sample(const double *pts, int64_t n, int axis, unsigned long long *spl,
+                                              unsigned long long *sk) {
+    const int q = threadIdx.x;
+    unsigned long long v = order_key(pts[2 * ((int64_t)q * n / BK_SAMPLE) + axis]);
+    for (int k = 2; k <= BK_SAMPLE; k <<= 1)
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            unsigned long long w;
+            if (j >= 32) {
+                sk[q] = v;
+                __syncthreads();
+                w = sk[q ^ j];
+                __syncthreads();
+            } else {
+                w = __shfl_xor_sync(0xffffffffu, v, j);
+            }
+            const bool lower = (q & j) == 0, up = (q & k) == 0;
+            v = (lower == up) ? min(v, w) : max(v, w);
+        }
+    spl[axis * BK_SAMPLE + q] = v;
 }
 
-__global__ void __launch_bounds__(BK_THREADS) bucket_count_kernel(const double *pts, int64_t n, int64_t B,
-                                                                  const unsigned long long *mm, int32_t *hist,
+// One launch for both inputs of the bucket map: CTAs 0, 1 sort the x / y
+// samples, the rest reduce the per-axis min / max order keys.
+// nsample = 0: keep the previous splitters (any sorted splitters give the
+// exact order; they only balance the buckets -- within a captured run of
+// steps the points move little between resamplings).
+__global__ void __launch_bounds__(BK_SAMPLE) bucket_prep_kernel(const double *pts, int64_t n,
+                                                                unsigned long long *mm, unsigned long long *spl,
+                                                                int nsample) {
+    pdl_wait();
+    __shared__ unsigned long long sk[BK_SAMPLE];
+    if ((int)blockIdx.x < nsample) {
+        bucket_sample(pts, n, blockIdx.x, spl, sk);
+        return;
+    }
+    bucket_minmax(pts, n, mm, blockIdx.x - nsample, gridDim.x - nsample, sk);
+}
+
+// Bucket = (sample interval c, linear sub-bucket): c = #{j in [1, S) :
+// splitter_j <= x}; inside [lo_c, hi_c) (the two end intervals reach the
+// axis min / max) F sub-buckets floor(F (x - lo_c)/(hi_c - lo_c)).
+constexpr int BK_COUNT_THREADS = 1024;  // the splitter table (16 KB) is staged once per CTA
+__global__ void __launch_bounds__(BK_COUNT_THREADS) bucket_count_kernel(const double *pts, int64_t n, int F,
+                                                                  const unsigned long long *mm,
+                                                                  const unsigned long long *spl, int32_t *hist,
                                                                   int32_t *bk_of) {
     pdl_wait();
-    const int64_t e = (int64_t)blockIdx.x * BK_THREADS + threadIdx.x;
+    __shared__ unsigned long long s_spl[2 * BK_SAMPLE];
+    for (int q = threadIdx.x; q < 2 * BK_SAMPLE; q += BK_COUNT_THREADS) s_spl[q] = spl[q];
+    __syncthreads();
+    const int64_t e = (int64_t)blockIdx.x * BK_COUNT_THREADS + threadIdx.x;
     if (e >= 2 * n) return;
     const int axis = e >= n;
     const double x = pts[2 * (e - axis * n) + axis];
-    const int g = (int)(axis * B) + bucket_of(x, key_to_double(mm[2 * axis]), key_to_double(mm[2 * axis + 1]), B);
+    const unsigned long long k = order_key(x);
+    const unsigned long long *sp = s_spl + axis * BK_SAMPLE;
+    int lo = 1, hi = BK_SAMPLE;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (sp[mid] <= k)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    const int c = lo - 1;
+    const double a = key_to_double(c == 0 ? mm[2 * axis] : sp[c]);
+    const double b = key_to_double(c == BK_SAMPLE - 1 ? mm[2 * axis + 1] : sp[c + 1]);
+    int fine = 0;
+    if (b > a) {
+        const double t = __dmul_rn(__ddiv_rn(__dsub_rn(x, a), __dsub_rn(b, a)), (double)F);
+        fine = (int)fmin(fmax(t, 0.0), (double)(F - 1));
+    }
+    const int g = (axis * BK_SAMPLE + c) * F + fine;
     bk_of[e] = g;
     atomicAdd(hist + g, 1);
 }
@@ -572,11 +637,22 @@ __global__ void __launch_bounds__(BK_THREADS) bucket_rank_kernel(const double *p
     const int s0 = start[g], s1 = start[g + 1];
     const unsigned long long k = order_key(pts[2 * id + axis]);
     int r = 0;
-    for (int q = s0; q < s1; ++q) {
-        const int j = slot[q] - axis * (int)n;
+    const int off = axis * (int)n;
+    auto less = [&](int j) {
         const unsigned long long kj = order_key(pts[2 * j + axis]);
-        r += (kj < k) || (kj == k && j < id);
+        return (int)((kj < k) || (kj == k && j < id));
+    };
+    int q = s0;
+    // 8 members per round: independent loads in flight (a large bucket is a
+    // long latency chain otherwise)
+    for (; q + 8 <= s1; q += 8) {
+        int j[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) j[u] = slot[q + u] - off;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) r += less(j[u]);
     }
+    for (; q < s1; ++q) r += less(slot[q] - off);
     xs0[s0 + r] = id;
 }
 
@@ -1704,7 +1780,8 @@ static cudaError_t launch_pdl(void (*kern)(KT...), dim3 grid, dim3 block, cudaSt
 }
 
 // Builds the tree for pts into b.t; returns the final perm (leaf order).
-static int build_tree(MdcLayoutPlan *p, const double *pts, cudaStream_t s, const int32_t **perm_out) {
+static int build_tree(MdcLayoutPlan *p, const double *pts, cudaStream_t s, const int32_t **perm_out,
+                      bool sample = true) {
     const TreeShape &sh = p->shape;
     Buffers &b = p->b;
     int64_t n = sh.n;
@@ -1714,10 +1791,14 @@ static int build_tree(MdcLayoutPlan *p, const double *pts, cudaStream_t s, const
     const int nb2 = (int)((2 * n + 255) / 256);
     if (MDC_SORT_BUCKET) {
         const int64_t B = b.nbucket;
-        const int nmm = (int)std::min<int64_t>((n + BK_THREADS - 1) / BK_THREADS, 4 * (int64_t)p->sms);
-        MDC_CHECK_CUDA(launch_pdl(bucket_minmax_kernel, dim3(nmm), dim3(BK_THREADS), s, pts, n, b.bk_mm));
-        MDC_CHECK_CUDA(launch_pdl(bucket_count_kernel, dim3(nb2), dim3(BK_THREADS), s, pts, n, B,
-                                  (const unsigned long long *)b.bk_mm, b.bk_hist, b.bk_of));
+        const int nmm = (int)std::min<int64_t>((n + BK_SAMPLE - 1) / BK_SAMPLE, (int64_t)p->sms);
+        const int nsample = sample ? 2 : 0;
+        MDC_CHECK_CUDA(launch_pdl(bucket_prep_kernel, dim3(nmm + nsample), dim3(BK_SAMPLE), s, pts, n, b.bk_mm,
+                                  b.bk_split, nsample));
+        MDC_CHECK_CUDA(launch_pdl(bucket_count_kernel, dim3((unsigned)((2 * n + BK_COUNT_THREADS - 1) / BK_COUNT_THREADS)),
+                                  dim3(BK_COUNT_THREADS), s, pts, n, (int)(B / BK_SAMPLE),
+                                  (const unsigned long long *)b.bk_mm, (const unsigned long long *)b.bk_split,
+                                  b.bk_hist, b.bk_of));
         size_t bytes = b.cub_bytes;
         MDC_CHECK_CUDA(cub::DeviceScan::ExclusiveSum(b.cub_tmp, bytes, b.bk_hist, b.bk_start, (int)(2 * B + 1), s));
         MDC_CHECK_CUDA(launch_pdl(bucket_scatter_kernel, dim3(nb2), dim3(BK_THREADS), s, n,
@@ -1821,9 +1902,9 @@ static void part_range(const MdcLayoutPlan *p, int64_t &k0, int64_t &k1) {
 }
 
 static int run_bh(MdcLayoutPlan *p, const double *pts, double *out, cudaStream_t s,
-                  const int32_t **perm_out = nullptr) {
+                  const int32_t **perm_out = nullptr, bool sample = true) {
     const int32_t *perm = nullptr;
-    int rc = build_tree(p, pts, s, &perm);
+    int rc = build_tree(p, pts, s, &perm, sample);
     if (rc) return rc;
     int64_t n = p->shape.n, k0, k1;
     part_range(p, k0, k1);
@@ -1846,12 +1927,12 @@ static int run_bh(MdcLayoutPlan *p, const double *pts, double *out, cudaStream_t
 }
 
 static int enqueue_step(MdcLayoutPlan *p, const double *pin, double *pout, const double *temps,
-                        cudaStream_t s) {
+                        cudaStream_t s, bool sample = true) {
     int64_t n = p->shape.n;
     const int32_t *perm = nullptr;
     p->mark(s);  // step start
     if (n >= 2) {
-        int rc = run_bh(p, pin, p->b.bh, s, &perm);
+        int rc = run_bh(p, pin, p->b.bh, s, &perm, sample);
         if (rc) return rc;
     } else {
         MDC_CHECK_CUDA(cudaMemsetAsync(p->b.bh, 0, sizeof(double) * 2 * (size_t)n, s));
@@ -2119,8 +2200,8 @@ extern "C" int mdc_layout_steps(MdcLayoutPlan *p, int32_t k, const double *temps
             if (!p->graph_multi) {
                 MDC_CHECK_CUDA(cudaStreamBeginCapture(p->cap_stream, cudaStreamCaptureModeThreadLocal));
                 int rc = 0;
-                for (int j = 0; j < MDC_LAYOUT_MULTI && !rc; ++j)
-                    rc = enqueue_step(p, bufs[j & 1], bufs[(j & 1) ^ 1], temps, p->cap_stream);
+                for (int j = 0; j < MDC_LAYOUT_MULTI && !rc; ++j)  // sort splitters resampled every 8 steps
+                    rc = enqueue_step(p, bufs[j & 1], bufs[(j & 1) ^ 1], temps, p->cap_stream, j % 8 == 0);
                 cudaGraph_t g;
                 cudaError_t e = cudaStreamEndCapture(p->cap_stream, &g);
                 if (rc) return rc;
