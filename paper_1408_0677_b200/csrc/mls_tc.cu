@@ -69,6 +69,9 @@ constexpr int NC_MAX = 32;             // channels per pass-2 chunk (fp64 totals
 #ifndef MDC_TC_SPLIT
 #define MDC_TC_SPLIT 1  // compute threads per pixel (2: each half takes half of every round / K tile)
 #endif
+#ifndef MDC_TC_P1_TRACE
+#define MDC_TC_P1_TRACE 1  // alpha = 3/2: accumulate sum 1/r instead of sum w dy^2 (13 FP32 lane-ops per pass-1 pair)
+#endif
 #ifndef MDC_TC_WIDE
 #define MDC_TC_WIDE 64  // d > 32: 64-channel chunks (0: 32-channel chunks only)
 #endif
@@ -316,6 +319,7 @@ __global__ void __launch_bounds__(THREADS, minb<NC>()) mls_tc_kernel(KArgs a, co
         };
 
         // ---------------- pass 1: moments (SIMT, packed f32x2) ----------------
+        constexpr bool TRACE = MDC_TC_P1_TRACE && AM == A_THREE_HALVES;
         // Lane 0 of each float2 accumulates the even controls, lane 1 the odd
         // ones.  The fp32 partials cover one staging round (XYR controls) and
         // are then added into fp64 totals, so the rounding error is bounded by
@@ -332,6 +336,22 @@ __global__ void __launch_bounds__(THREADS, minb<NC>()) mls_tc_kernel(KArgs a, co
             auto acc = [&](const float4 pp, bool odd_tail) {
                 const float2 dx = __fadd2_rn(make_float2(pp.x, pp.y), nvx);
                 const float2 dy = __fadd2_rn(make_float2(pp.z, pp.w), nvy);
+                if constexpr (TRACE) {
+                    // alpha = 3/2: w r^2 = 1/r = y, so sum w dy^2 = sum y - sum w dx^2
+                    // (the last moment becomes a plain sum: one FMUL2 less per pair)
+                    const float2 d2 = __ffma2_rn(dy, dy, __fmul2_rn(dx, dx));
+                    float2 y = make_float2(rsqrt_approx(d2.x), rsqrt_approx(d2.y));
+                    float2 w = __fmul2_rn(__fmul2_rn(y, y), y);
+                    if (odd_tail) w.y = y.y = 0.f;
+                    const float2 wdx = __fmul2_rn(w, dx);
+                    sw2 = __fadd2_rn(sw2, w);
+                    mx2 = __fadd2_rn(mx2, wdx);
+                    my2 = __ffma2_rn(w, dy, my2);
+                    sxx2 = __ffma2_rn(wdx, dx, sxx2);
+                    sxy2 = __ffma2_rn(wdx, dy, sxy2);
+                    syy2 = __fadd2_rn(syy2, y);  // sum y (= sum w r^2)
+                    return;
+                }
                 float2 w = weight2<AM>(__ffma2_rn(dy, dy, __fmul2_rn(dx, dx)), neg_alpha);
                 if (odd_tail) w.y = 0.f;  // parked control (alpha < 1 does not underflow)
                 const float2 wdx = __fmul2_rn(w, dx), wdy = __fmul2_rn(w, dy);
@@ -377,6 +397,7 @@ __global__ void __launch_bounds__(THREADS, minb<NC>()) mls_tc_kernel(KArgs a, co
         }
         if (hh == 0) {
             double s = tw, m0 = tmx, m1 = tmy;
+            if (TRACE) tyy -= txx;  // sum w dy^2 = sum w r^2 - sum w dx^2
             double a00 = txx - m0 * m0 / s;
             double a01 = txy - m0 * m1 / s;
             double a11 = tyy - m1 * m1 / s;
