@@ -551,9 +551,10 @@ def main():
     if use_tc:
         nc = 16 if d <= 16 else (32 if d <= 32 else (64 if d <= 64 else 128))  # mls_tc.cu pick_nc
         chunks = -(-d // nc)
-        # SIMT FP32 lane-ops per pair (FFMA2/FADD2/FMUL2 count 2): pass-1 moments 14,
-        # pass-2 G evaluation + tf32 split 10 per channel chunk
-        fma_instr = pairs * (14 + 10 * chunks)
+        # SIMT FP32 lane-ops per pair (FFMA2/FADD2/FMUL2 count 2): pass-1 moments 13
+        # (alpha = 3/2: sum 1/r replaces sum w dy^2), pass-2 G evaluation + tf32
+        # split 10 per channel chunk (ncu SASS count: profiles/r02_mls_tc_kernel_fp32_lane_ops.txt)
+        fma_instr = pairs * (13 + 10 * chunks)
         mixed = nc > 32  # wide chunks: tf32 main + 2 bf16 corrections = 2 tf32-equivalent passes
         tc_flops = pairs * chunks * (2 if mixed else 3) * 2 * nc
         kname = (f"mls_tc_kernel<alpha=1.5, N={nc}> (tcgen05 pass 2: "
