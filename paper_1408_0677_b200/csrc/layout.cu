@@ -1063,6 +1063,20 @@ __device__ __forceinline__ double rsqrt_nr(double x) {
 #endif
 }
 
+// r = sqrt(x) from the same MUFU seed y0 ~ 1/sqrt(x): r = x y0 (1 + e/2 + 3e^2/8)
+// with e = 1 - x y0^2 -- the rsqrt_nr series applied to r0 = x y0 directly,
+// one multiply fewer than x * rsqrt_nr(x).
+#ifndef MDC_BH_SQRT_NR
+#define MDC_BH_SQRT_NR 1
+#endif
+__device__ __forceinline__ double sqrt_nr(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    const double r0 = x * y;
+    const double e = fma(-r0, y, 1.0);
+    return fma(r0, e * fma(0.375, e, 0.5), r0);
+}
+
 #ifndef MDC_BH_F32TEST
 #define MDC_BH_F32TEST 1  // fp32 pre-test of the opening criterion (exact fp64 only inside its band)
 #endif
@@ -1100,8 +1114,12 @@ __device__ __forceinline__ void monopole(const double4 g1, double xi, double yi,
                                          double &fy) {
     double dx = xi - g1.x, dy = yi - g1.y;
     double r2 = dx * dx + dy * dy;
+#if MDC_BH_SQRT_NR
+    double coef = g1.w * rcp_nr(fma(r2, sqrt_nr(r2), eta));
+#else
     double r = r2 * rsqrt_nr(r2);
     double coef = g1.w * rcp_nr(r * r * r + eta);
+#endif
     fx = fma(coef, dx, fx);
     fy = fma(coef, dy, fy);
 }
@@ -1183,8 +1201,12 @@ __device__ __forceinline__ void bh_body(int64_t n, int64_t k0, int64_t k1, const
                             const double2 pj = s_leaf_w[q];
                             double dx = xi - pj.x, dy = yi - pj.y;
                             double r2 = fma(dx, dx, fma(dy, dy, 1e-300));
+#if MDC_BH_SQRT_NR
+                            double w = rcp_nr(fma(r2, sqrt_nr(r2), eta));
+#else
                             double y = rsqrt_nr(r2);
                             double w = rcp_nr(r2 * (r2 * y) + eta);
+#endif
                             ax = fma(w, dx, ax);
                             ay = fma(w, dy, ay);
                         };
