@@ -274,11 +274,11 @@ def measure_peaks(lib, torch):
 
 
 # fp64 pipe ops per BH unit (bh_kernel source): leaf pair = 2 sub + 2 fma (r2)
-# + 5 (rsqrt.approx + 3rd-order correction) + 3 (r^3 + eta) + 3 (rcp.approx +
-# correction) + 2 fma (force); monopole = 19; opening test = 9 (box offsets,
-# squared distance, size^2 vs theta^2 d2 with the guard band; the exact IEEE
-# sqrt path is only taken inside the band).
-BH_OPS = {"leaf_pairs": 17, "monopoles": 19, "node_tests": 9}
+# + 5 (sqrt from the rsqrt.approx seed + 2nd-order series) + 1 fma (r2 r + eta)
+# + 3 (rcp.approx + correction) + 2 fma (force) = 15; monopole = 16 (+1 mass);
+# opening test = 9 (box offsets, squared distance, size^2 vs theta^2 d2 with the
+# guard band; the exact IEEE sqrt path is only taken inside the band).
+BH_OPS = {"leaf_pairs": 15, "monopoles": 16, "node_tests": 9}
 LOCAL_BYTES_PER_VERTEX = 204  # SURVEY.md §8d algorithmic bytes per vertex-iteration
 
 
@@ -303,7 +303,7 @@ def layout_roofline(eng, params, lib, torch):
                "interactions_per_vertex": (prof["leaf_pairs"] - n + prof["monopoles"]) / n,
                "node_tests_per_vertex": prof["node_tests"] / n,
                "lane_efficiency": (prof["leaf_pairs"] + prof["node_tests"]) / max(1, prof["lane_slots"]),
-               "ops_def": "fp64 lane-ops x 2 / bh_kernel time; 17/leaf pair, 19/monopole, 9/opening test",
+               "ops_def": "fp64 lane-ops x 2 / bh_kernel time; 15/leaf pair, 16/monopole, 9/opening test",
                "peak_source": "measured DFMA microbenchmark (mdc_peak_dfma), this run"},
         "local": {"bound": "hbm", "achieved": local_gbs, "peak": hbm, "unit": "GB/s", "frac": local_gbs / hbm,
                   "bytes_per_vertex": LOCAL_BYTES_PER_VERTEX,
