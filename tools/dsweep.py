@@ -43,7 +43,7 @@ def main():
         if d >= 8:
             nc = 16 if d <= 16 else (32 if d <= 32 else (64 if d <= 64 else 128))  # mls_tc.cu pick_nc
             chunks = -(-d // nc)
-            lane_ops, path = 14 + 10 * chunks, "tcgen05"
+            lane_ops, path = 13 + 10 * chunks, "tcgen05"  # pass 1: 13 (alpha = 3/2, sum 1/r)
         else:
             lane_ops, path = 14 + 9 + d, "simt"  # DC = d here (one chunk)
         frac = 2 * pairs * lane_ops / (ms * 1e-3) / peaks["fp32"]
