@@ -55,7 +55,7 @@ __device__ __forceinline__ void run_flush(T &part, double &tot) {
 #define MDC_F64_DC32 2  // pixels per thread for the fp64 32-channel instantiation (0: off; A/B at config 3: 16-ch chunks 41.0, R = 1 49.2, R = 2 56.4 Mpixel*dim/s)
 #endif
 #ifndef MDC_SIMT_P1_UNROLL
-#define MDC_SIMT_P1_UNROLL 8  // control-loop unroll of the scalar (fp64) passes (A/B, fp64 config 3: 2 55.9, 4 56.5, 8 57.6)
+#define MDC_SIMT_P1_UNROLL 8  // control-loop unroll of the scalar (fp64) passes (A/B, fp64 config 3 before the MUFU weights: 2 55.9, 4 56.5, 8 57.6)
 #endif
 #ifndef MDC_SIMT_P2_UNROLL
 #define MDC_SIMT_P2_UNROLL 2

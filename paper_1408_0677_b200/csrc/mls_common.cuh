@@ -18,6 +18,34 @@ static inline int alpha_mode(double a) {
 }
 
 // ---- weights: w = d2^-alpha ------------------------------------------------
+// fp64 reciprocal / reciprocal square root for the weights (MDC_F64_FASTW):
+// the MUFU seed (2^-20) plus one second-order correction, ~1 ulp -- the
+// library's correctly rounded sequences cost about twice the fp64 ops; the
+// fp64 contract is 1e-10.  Inputs are >= 1e-300 (the weight floor), so the
+// flush-to-zero seeds never see a subnormal.
+#ifndef MDC_F64_FASTW
+#define MDC_F64_FASTW 1
+#endif
+__device__ __forceinline__ double rsqrt64(double x) {
+#if MDC_F64_FASTW
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    const double e = fma(-x * y, y, 1.0);
+    return fma(y * e, fma(0.375, e, 0.5), y);
+#else
+    return rsqrt(x);
+#endif
+}
+__device__ __forceinline__ double rcp64(double x) {
+#if MDC_F64_FASTW
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    const double e = fma(-x, r, 1.0);
+    return fma(r, fma(e, e, e), r);
+#else
+    return 1.0 / x;
+#endif
+}
 __device__ __forceinline__ float rsqrt_approx(float x) {
     float y;
     asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -83,14 +111,14 @@ __device__ __forceinline__ double weight(double d2, double neg_alpha) {
     // fp64 mirrors _kernels.py:37-49 including the 1e-300 floor.
     if (d2 < 1e-300) d2 = 1e-300;
     if (AM == A_THREE_HALVES) {
-        double r = rsqrt(d2);
+        double r = rsqrt64(d2);
         return r * r * r;
     } else if (AM == A_ONE) {
-        return 1.0 / d2;
+        return rcp64(d2);
     } else if (AM == A_HALF) {
-        return rsqrt(d2);
+        return rsqrt64(d2);
     } else if (AM == A_TWO) {
-        double r = 1.0 / d2;
+        double r = rcp64(d2);
         return r * r;
     } else {
         return pow(d2, neg_alpha);
