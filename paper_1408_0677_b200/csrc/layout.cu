@@ -1656,6 +1656,24 @@ struct SmallArgs {
     int32_t *ctr;
 };
 
+#ifndef MDC_SMALL_CLUSTER
+#define MDC_SMALL_CLUSTER 8  // CTAs (one thread-block cluster) sharing the persistent small-mesh step
+#endif
+constexpr int SMALL_CLUSTER = MDC_SMALL_CLUSTER;
+
+// barrier over the whole cluster with release/acquire at cluster scope: the
+// CTAs' global-memory writes before it are visible to all of them after it
+__device__ __forceinline__ void small_sync() {
+    if (SMALL_CLUSTER > 1)
+        asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    else
+        __syncthreads();
+}
+
+// The step's phases spread over a cluster of SMALL_CLUSTER CTAs: ranks, BH
+// items, the combine and the local update are split across the cluster (one
+// SM's FP64 pipe bounded the local update); the tree walk stays on CTA 0.
+// Same device code and summation orders: bit-identical to one CTA.
 __global__ void __launch_bounds__(SMALL_THREADS, 1) layout_small_kernel(SmallArgs sa) {
     constexpr int W = SMALL_THREADS / 32;
     __shared__ int s_node[W][BH_STACK];
@@ -1664,6 +1682,8 @@ __global__ void __launch_bounds__(SMALL_THREADS, 1) layout_small_kernel(SmallArg
     __shared__ int32_t s_step;
     __shared__ unsigned long long s_key[2 * MDC_LAYOUT_SMALL_MAX];
     const int tid = threadIdx.x, wib = tid >> 5;
+    const int cta = blockIdx.x, C = gridDim.x;  // the grid is one cluster
+    const int gth = cta * SMALL_THREADS + tid, GTH = C * SMALL_THREADS;
     const int64_t n = sa.ba.n;
     const DevTree &t = sa.ba.t;
     const int32_t *perm = (sa.ba.max_depth & 1) ? sa.ba.xs1 : sa.ba.xs0;  // leaf order after the walk
@@ -1677,58 +1697,68 @@ __global__ void __launch_bounds__(SMALL_THREADS, 1) layout_small_kernel(SmallArg
         const double *pin = sa.bufs[step & 1];
         double *pout = sa.bufs[(step & 1) ^ 1];
         // exact ranks -> ids in (coord, id) order, x run then y run (the
-        // order the radix sort + equal-key fixup produces)
-        for (int64_t e = tid; e < 2 * n; e += SMALL_THREADS) {  // sortable keys staged in shared memory
+        // order the device sort produces); every CTA stages all keys and ranks its share
+        for (int64_t e = tid; e < 2 * n; e += SMALL_THREADS) {
             const int axis = e >= n;
             s_key[e] = order_key(pin[2 * (e - axis * n) + axis]);
         }
         __syncthreads();
-        for (int64_t e = tid; e < 2 * n; e += SMALL_THREADS) {
+        for (int64_t e = gth; e < 2 * n; e += GTH) {
             const int axis = e >= n;
             const int64_t i = e - axis * n;
             const unsigned long long ki = s_key[e];
             const unsigned long long *kk = s_key + axis * n;
             int r = 0;
-            for (int64_t j = 0; j < n; ++j) {
+#pragma unroll 8
+            for (int j = 0; j < (int)n; ++j) {
                 const unsigned long long kj = kk[j];
                 r += (kj < ki) || (kj == ki && j < i);
             }
             sa.ba.xs0[axis * n + r] = (int32_t)i;
         }
-        __syncthreads();
+        small_sync();
         MDC_PH(0);
-        BuildArgs ba = sa.ba;
-        ba.pts = pin;
-        build_levels_body<SMALL_THREADS, BUILD_ONE_CTA>(ba);
-        __syncthreads();
+        if (cta == 0) {
+            BuildArgs ba = sa.ba;
+            ba.pts = pin;
+            build_levels_body<SMALL_THREADS, BUILD_ONE_CTA>(ba);
+        }
+        small_sync();
         MDC_PH(1);
         const int64_t npw = (n + 31) / 32;
-        for (int64_t it = wib; it < npw * t.ntask; it += W)
+        for (int64_t it = (int64_t)cta * W + wib; it < npw * t.ntask; it += (int64_t)C * W)
             bh_body<false>(n, 0, n, t, sa.c, sa.eta, sa.theta, nullptr, it % npw, (int)(it / npw), s_node[wib],
                            s_mask[wib], s_leaf[wib]);
-        __syncthreads();
+        small_sync();
         MDC_PH(2);
-        for (int64_t k = tid; k < n; k += SMALL_THREADS)
+        for (int64_t k = gth; k < n; k += GTH)
             reinterpret_cast<double2 *>(const_cast<double *>(sa.la.bh))[perm[k]] = bh_total(t, n, k);
         if (tid == 0) s_step = step;
-        __syncthreads();
+        small_sync();
         MDC_PH(3);
         LocalArgs la = sa.la;
         la.pos = pin;
         la.pos_out = pout;
         la.ctr = &s_step;
-        for (int64_t base = 0; base < n * SMALL_LG; base += SMALL_THREADS)
-            local_group_body<SMALL_LG>(la, base + tid);
-        __syncthreads();
+        {
+            // lane groups split evenly over the cluster in whole warps (a warp
+            // calls the body together: its reductions are warp collectives)
+            const int64_t lanes = n * SMALL_LG;
+            const int64_t chunk = ((lanes + C - 1) / C + 31) / 32 * 32;
+            const int64_t lo = (int64_t)cta * chunk, hi = min(lanes, lo + chunk);
+            for (int64_t base = lo; base < hi; base += SMALL_THREADS)
+                if (base + (tid & ~31) < hi) local_group_body<SMALL_LG>(la, base + tid);
+        }
+        small_sync();
         MDC_PH(4);
     }
 #if MDC_SMALL_PROF
-    if (tid == 0)
+    if (tid == 0 && cta == 0)
         printf("small-step cycles/step: ranks %lld build %lld bh %lld combine %lld local %lld (n=%lld k=%d)\n",
                ph[0] / sa.k, ph[1] / sa.k, ph[2] / sa.k, ph[3] / sa.k, ph[4] / sa.k, (long long)n, sa.k);
 #endif
 #undef MDC_PH
-    if (tid == 0) *sa.ctr = sa.k;
+    if (tid == 0 && cta == 0) *sa.ctr = sa.k;
 }
 
 // All-gather exchange, receive side: recv holds every rank's packed slice
@@ -2088,6 +2118,8 @@ extern "C" int mdc_layout_plan_create(const MdcLayoutArgs *a, MdcLayoutPlan **pl
                 break;
             }
         }
+        if (SMALL_CLUSTER > 8)
+            cudaFuncSetAttribute(layout_small_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         auto ck = build_levels_kernel<BUILD_CLUSTER_THREADS, BUILD_ONE_CLUSTER>;
         if (BUILD_CLUSTER > 8)
             cudaFuncSetAttribute(ck, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -2191,7 +2223,20 @@ extern "C" int mdc_layout_steps(MdcLayoutPlan *p, int32_t k, const double *temps
         sa.eta = p->a.eta;
         sa.theta = p->a.theta;
         sa.ctr = p->b.ctr;
-        layout_small_kernel<<<1, SMALL_THREADS, 0, s>>>(sa);
+        {
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(SMALL_CLUSTER);
+            cfg.blockDim = dim3(SMALL_THREADS);
+            cfg.stream = s;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = SMALL_CLUSTER;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = SMALL_CLUSTER > 1 ? 1 : 0;
+            MDC_CHECK_CUDA(cudaLaunchKernelEx(&cfg, layout_small_kernel, sa));
+        }
         MDC_CHECK_LAUNCH();
         if (k & 1)
             MDC_CHECK_CUDA(cudaMemcpyAsync(p->a.pos, p->b.pos_b, sizeof(double) * 2 * (size_t)n,
