@@ -1654,7 +1654,64 @@ struct SmallArgs {
     int k;
     double c, eta, theta;
     int32_t *ctr;
+    // shared-memory staging: mesh topology (CSR neighbours, incidences,
+    // triangles) and, on CTA 0, the tree shape and walk scratch
+    int nE, nI, ntri, nn, ns, nl;
 };
+
+// Per-CTA shared-memory carve of the persistent small step (16-byte aligned
+// pieces); the host computes the same size.
+struct SmallSmem {
+    double *pos, *bh;
+    int4 *tris;
+    int32_t *csr_off, *csr_tgt, *inc_off, *inc;
+    int32_t *xs0, *xs1, *ys1, *flag, *oflag, *prefix, *blocksum;
+    int32_t *lo, *hi, *left, *right, *nd_off, *nd_list, *seg_off, *seg_lo, *seg_hi, *seg_node, *seg_split, *seg_of,
+        *leaves, *leaf_lo, *leaf_hi;
+};
+__host__ __device__ inline size_t small_carve(SmallSmem &m, unsigned char *base, int64_t n, int nE, int nI, int ntri,
+                                              int nn, int ns, int nl, int md) {
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        unsigned char *p = base + off;
+        off += (bytes + 15) & ~(size_t)15;
+        return p;
+    };
+    m.pos = (double *)take(16 * (size_t)n);
+    m.bh = (double *)take(16 * (size_t)n);
+    m.tris = (int4 *)take(16 * (size_t)ntri);
+    m.csr_off = (int32_t *)take(4 * (size_t)(n + 1));
+    m.csr_tgt = (int32_t *)take(4 * (size_t)nE);
+    m.inc_off = (int32_t *)take(4 * (size_t)(n + 1));
+    m.inc = (int32_t *)take(4 * (size_t)nI);
+    m.xs0 = (int32_t *)take(8 * (size_t)n);
+    m.xs1 = (int32_t *)take(4 * (size_t)n);
+    m.ys1 = (int32_t *)take(4 * (size_t)n);
+    m.flag = (int32_t *)take(4 * (size_t)n);
+    m.oflag = (int32_t *)take(4 * (size_t)n);
+    m.prefix = (int32_t *)take(4 * (size_t)n);
+    m.blocksum = (int32_t *)take(4 * 32);
+    m.lo = (int32_t *)take(4 * (size_t)nn);
+    m.hi = (int32_t *)take(4 * (size_t)nn);
+    m.left = (int32_t *)take(4 * (size_t)nn);
+    m.right = (int32_t *)take(4 * (size_t)nn);
+    m.nd_off = (int32_t *)take(4 * (size_t)(md + 2));
+    m.nd_list = (int32_t *)take(4 * (size_t)nn);
+    m.seg_off = (int32_t *)take(4 * (size_t)(md + 1));
+    m.seg_lo = (int32_t *)take(4 * (size_t)ns);
+    m.seg_hi = (int32_t *)take(4 * (size_t)ns);
+    m.seg_node = (int32_t *)take(4 * (size_t)ns);
+    m.seg_split = (int32_t *)take(4 * (size_t)ns);
+    m.seg_of = (int32_t *)take(4 * (size_t)md * (size_t)n);
+    m.leaves = (int32_t *)take(4 * (size_t)nl);
+    m.leaf_lo = (int32_t *)take(4 * (size_t)nn);
+    m.leaf_hi = (int32_t *)take(4 * (size_t)nn);
+    return off;
+}
+
+__device__ __forceinline__ void copy_i32(int32_t *dst, const int32_t *src, int64_t count) {
+    for (int64_t i = threadIdx.x; i < count; i += blockDim.x) dst[i] = src[i];
+}
 
 #ifndef MDC_SMALL_CLUSTER
 #define MDC_SMALL_CLUSTER 8  // CTAs (one thread-block cluster) sharing the persistent small-mesh step
@@ -1670,10 +1727,14 @@ __device__ __forceinline__ void small_sync() {
         __syncthreads();
 }
 
-// The step's phases spread over a cluster of SMALL_CLUSTER CTAs: ranks, BH
-// items, the combine and the local update are split across the cluster (one
-// SM's FP64 pipe bounded the local update); the tree walk stays on CTA 0.
-// Same device code and summation orders: bit-identical to one CTA.
+// The step's phases spread over a cluster of SMALL_CLUSTER CTAs: the BH items
+// and the local lanes are split across the cluster (one SM's FP64 pipe
+// bounded the local update), the ranks and the tree walk run on CTA 0.  The
+// mesh topology is staged in each CTA's shared memory once per launch, the
+// tree shape and the walk's scratch in CTA 0's, and every step's positions
+// and combined BH forces in each CTA's -- the local update and the walk then
+// read shared memory instead of L2.  Same device code and summation orders:
+// bit-identical to the multi-kernel step.
 __global__ void __launch_bounds__(SMALL_THREADS, 1) layout_small_kernel(SmallArgs sa) {
     constexpr int W = SMALL_THREADS / 32;
     __shared__ int s_node[W][BH_STACK];
@@ -1681,12 +1742,55 @@ __global__ void __launch_bounds__(SMALL_THREADS, 1) layout_small_kernel(SmallArg
     __shared__ double2 s_leaf[W][32];
     __shared__ int32_t s_step;
     __shared__ unsigned long long s_key[2 * MDC_LAYOUT_SMALL_MAX];
+    extern __shared__ __align__(16) unsigned char s_dyn[];
     const int tid = threadIdx.x, wib = tid >> 5;
     const int cta = blockIdx.x, C = gridDim.x;  // the grid is one cluster
-    const int gth = cta * SMALL_THREADS + tid, GTH = C * SMALL_THREADS;
     const int64_t n = sa.ba.n;
-    const DevTree &t = sa.ba.t;
-    const int32_t *perm = (sa.ba.max_depth & 1) ? sa.ba.xs1 : sa.ba.xs0;  // leaf order after the walk
+    const DevTree &t = sa.ba.t;  // global tree: BH, combine
+    const int md = sa.ba.max_depth;
+    SmallSmem m;
+    small_carve(m, s_dyn, n, sa.nE, sa.nI, sa.ntri, sa.nn, sa.ns, sa.nl, md);
+    // mesh topology (every CTA), tree shape (CTA 0)
+    copy_i32(m.csr_off, sa.la.csr_off, n + 1);
+    copy_i32(m.csr_tgt, sa.la.csr_tgt, sa.nE);
+    copy_i32(m.inc_off, sa.la.inc_off, n + 1);
+    copy_i32(m.inc, sa.la.inc, sa.nI);
+    copy_i32(reinterpret_cast<int32_t *>(m.tris), sa.la.tris, 4 * (int64_t)sa.ntri);
+    BuildArgs ba = sa.ba;  // CTA 0's walk: shape + scratch in shared memory, outputs global
+    if (cta == 0) {
+        copy_i32(m.lo, t.lo, sa.nn);
+        copy_i32(m.hi, t.hi, sa.nn);
+        copy_i32(m.left, t.left, sa.nn);
+        copy_i32(m.right, t.right, sa.nn);
+        copy_i32(m.nd_off, t.nd_off, md + 2);
+        copy_i32(m.nd_list, t.nd_list, sa.nn);
+        copy_i32(m.seg_off, t.seg_off, md + 1);
+        copy_i32(m.seg_lo, t.seg_lo, sa.ns);
+        copy_i32(m.seg_hi, t.seg_hi, sa.ns);
+        copy_i32(m.seg_node, t.seg_node, sa.ns);
+        copy_i32(m.seg_split, t.seg_split, sa.ns);
+        copy_i32(m.seg_of, t.seg_of, (int64_t)md * n);
+        copy_i32(m.leaves, t.leaves, sa.nl);
+        copy_i32(m.leaf_lo, t.leaf_lo, sa.nn);
+        copy_i32(m.leaf_hi, t.leaf_hi, sa.nn);
+        DevTree &u = ba.t;
+        u.lo = m.lo, u.hi = m.hi, u.left = m.left, u.right = m.right;
+        u.nd_off = m.nd_off, u.nd_list = m.nd_list, u.seg_off = m.seg_off;
+        u.seg_lo = m.seg_lo, u.seg_hi = m.seg_hi, u.seg_node = m.seg_node, u.seg_split = m.seg_split;
+        u.seg_of = m.seg_of, u.leaves = m.leaves, u.leaf_lo = m.leaf_lo, u.leaf_hi = m.leaf_hi;
+        ba.xs0 = m.xs0, ba.ys0 = m.xs0 + n, ba.xs1 = m.xs1, ba.ys1 = m.ys1;
+        ba.flag = m.flag, ba.oflag = m.oflag, ba.prefix = m.prefix, ba.blocksum = m.blocksum;
+        ba.pts = m.pos;
+    }
+    const int32_t *sperm = (md & 1) ? m.xs1 : m.xs0;                  // CTA 0: leaf order after the walk
+    int32_t *gperm = (md & 1) ? sa.ba.xs1 : sa.ba.xs0;                 // the same, published for the cluster
+    LocalArgs la = sa.la;
+    la.pos = m.pos;
+    la.bh = m.bh;
+    la.csr_off = m.csr_off, la.csr_tgt = m.csr_tgt, la.inc_off = m.inc_off, la.inc = m.inc;
+    la.tris = reinterpret_cast<const int32_t *>(m.tris);
+    la.ctr = &s_step;
+    __syncthreads();
 #if MDC_SMALL_PROF  // experiments: per-phase clock totals, printed once
     long long ph[6] = {0, 0, 0, 0, 0, 0}, t0 = clock64();
 #define MDC_PH(i) do { if (tid == 0) { long long t1 = clock64(); ph[i] += t1 - t0; t0 = t1; } } while (0)
@@ -1696,32 +1800,34 @@ __global__ void __launch_bounds__(SMALL_THREADS, 1) layout_small_kernel(SmallArg
     for (int step = 0; step < sa.k; ++step) {
         const double *pin = sa.bufs[step & 1];
         double *pout = sa.bufs[(step & 1) ^ 1];
-        // exact ranks -> ids in (coord, id) order, x run then y run (the
-        // order the device sort produces); every CTA stages all keys and ranks its share
-        for (int64_t e = tid; e < 2 * n; e += SMALL_THREADS) {
-            const int axis = e >= n;
-            s_key[e] = order_key(pin[2 * (e - axis * n) + axis]);
-        }
+        for (int64_t e = tid; e < 2 * n; e += SMALL_THREADS) m.pos[e] = pin[e];
         __syncthreads();
-        for (int64_t e = gth; e < 2 * n; e += GTH) {
-            const int axis = e >= n;
-            const int64_t i = e - axis * n;
-            const unsigned long long ki = s_key[e];
-            const unsigned long long *kk = s_key + axis * n;
-            int r = 0;
-#pragma unroll 8
-            for (int j = 0; j < (int)n; ++j) {
-                const unsigned long long kj = kk[j];
-                r += (kj < ki) || (kj == ki && j < i);
-            }
-            sa.ba.xs0[axis * n + r] = (int32_t)i;
-        }
-        small_sync();
-        MDC_PH(0);
         if (cta == 0) {
-            BuildArgs ba = sa.ba;
-            ba.pts = pin;
+            // exact ranks -> ids in (coord, id) order, x run then y run (the
+            // order the device sort produces)
+            for (int64_t e = tid; e < 2 * n; e += SMALL_THREADS) {
+                const int axis = e >= n;
+                s_key[e] = order_key(m.pos[2 * (e - axis * n) + axis]);
+            }
+            __syncthreads();
+            for (int64_t e = tid; e < 2 * n; e += SMALL_THREADS) {
+                const int axis = e >= n;
+                const int64_t i = e - axis * n;
+                const unsigned long long ki = s_key[e];
+                const unsigned long long *kk = s_key + axis * n;
+                int r = 0;
+#pragma unroll 8
+                for (int j = 0; j < (int)n; ++j) {
+                    const unsigned long long kj = kk[j];
+                    r += (kj < ki) || (kj == ki && j < i);
+                }
+                m.xs0[axis * n + r] = (int32_t)i;
+            }
+            __syncthreads();
+            MDC_PH(0);
             build_levels_body<SMALL_THREADS, BUILD_ONE_CTA>(ba);
+            __syncthreads();
+            for (int64_t k = tid; k < n; k += SMALL_THREADS) gperm[k] = sperm[k];
         }
         small_sync();
         MDC_PH(1);
@@ -1731,15 +1837,13 @@ __global__ void __launch_bounds__(SMALL_THREADS, 1) layout_small_kernel(SmallArg
                            s_mask[wib], s_leaf[wib]);
         small_sync();
         MDC_PH(2);
-        for (int64_t k = gth; k < n; k += GTH)
-            reinterpret_cast<double2 *>(const_cast<double *>(sa.la.bh))[perm[k]] = bh_total(t, n, k);
+        // every CTA combines all points into its own shared copy
+        for (int64_t k = tid; k < n; k += SMALL_THREADS)
+            reinterpret_cast<double2 *>(m.bh)[gperm[k]] = bh_total(t, n, k);
         if (tid == 0) s_step = step;
-        small_sync();
+        __syncthreads();
         MDC_PH(3);
-        LocalArgs la = sa.la;
-        la.pos = pin;
         la.pos_out = pout;
-        la.ctr = &s_step;
         {
             // lane groups split evenly over the cluster in whole warps (a warp
             // calls the body together: its reductions are warp collectives)
@@ -1792,6 +1896,7 @@ struct MdcLayoutPlan {
     int sms = 148;
     // profiling (mdc_layout_profile): events recorded between step phases
     bool cluster_ok = false;  // the device can co-schedule one BUILD_CLUSTER cluster
+    int small_nE = 0, small_nI = 0;  // CSR neighbour / incidence counts (persistent small-mesh step)
     int subtree_l0 = -1;      // grid walk: first level handed to build_subtree_kernel (-1: none)
     int subtree_nseg = 0;
     cudaEvent_t ev[8] = {};
@@ -2137,6 +2242,10 @@ extern "C" int mdc_layout_plan_create(const MdcLayoutArgs *a, MdcLayoutPlan **pl
         p->cluster_ok = cudaOccupancyMaxActiveClusters(&nclusters, ck, &cfg) == cudaSuccess && nclusters >= 1;
         cudaGetLastError();  // a refused query leaves the cooperative path in charge
     }
+    if (p->shape.n <= MDC_LAYOUT_SMALL_MAX) {  // staged topology sizes of the persistent small step
+        cudaMemcpyAsync(&p->small_nE, a->csr_off + p->shape.n, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+        cudaMemcpyAsync(&p->small_nI, a->inc_off + p->shape.n, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+    }
     cudaMemsetAsync(p->b.runflag, 0, sizeof(int32_t) * 2 * (size_t)p->shape.n, s);
     cudaMemsetAsync(p->b.rank, 0, sizeof(int32_t) * 2 * (size_t)p->shape.n, s);
     cudaMemsetAsync(p->b.bk_hist, 0, sizeof(int32_t) * (2 * (size_t)p->b.nbucket + 1), s);
@@ -2223,10 +2332,22 @@ extern "C" int mdc_layout_steps(MdcLayoutPlan *p, int32_t k, const double *temps
         sa.eta = p->a.eta;
         sa.theta = p->a.theta;
         sa.ctr = p->b.ctr;
+        sa.nE = p->small_nE;
+        sa.nI = p->small_nI;
+        sa.ntri = (int)p->a.ntri;
+        sa.nn = (int)p->shape.lo.size();
+        sa.ns = (int)p->shape.seg_lo.size();
+        sa.nl = (int)p->shape.leaves.size();
         {
+            SmallSmem mm;
+            const size_t smem = small_carve(mm, nullptr, n, sa.nE, sa.nI, sa.ntri, sa.nn, sa.ns, sa.nl,
+                                            p->shape.max_depth);
+            MDC_CHECK_CUDA(cudaFuncSetAttribute(layout_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)smem));
             cudaLaunchConfig_t cfg = {};
             cfg.gridDim = dim3(SMALL_CLUSTER);
             cfg.blockDim = dim3(SMALL_THREADS);
+            cfg.dynamicSmemBytes = smem;
             cfg.stream = s;
             cudaLaunchAttribute attr[1];
             attr[0].id = cudaLaunchAttributeClusterDimension;
