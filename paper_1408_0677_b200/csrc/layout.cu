@@ -777,10 +777,13 @@ __device__ __forceinline__ void build_levels_body(const BuildArgs &a) {
     __shared__ int s_carry;
     const DevTree &t = a.t;
     const int64_t n = a.n;
-    const int G = gridDim.x, tid = threadIdx.x;
-    const int64_t gtid = (int64_t)blockIdx.x * BUILD_THREADS + tid, gsz = (int64_t)G * BUILD_THREADS;
+    // one CTA walks alone even when launched inside a larger grid (the
+    // persistent small-mesh step runs it on CTA 0 of its cluster)
+    const int G = MODE == BUILD_ONE_CTA ? 1 : (int)gridDim.x, tid = threadIdx.x;
+    const int bid = MODE == BUILD_ONE_CTA ? 0 : (int)blockIdx.x;
+    const int64_t gtid = (int64_t)bid * BUILD_THREADS + tid, gsz = (int64_t)G * BUILD_THREADS;
     const int64_t chunk = (((n + G - 1) / G) + BUILD_THREADS - 1) / BUILD_THREADS * BUILD_THREADS;
-    const int64_t c_lo = min((int64_t)blockIdx.x * chunk, n), c_hi = min(c_lo + chunk, n);
+    const int64_t c_lo = min((int64_t)bid * chunk, n), c_hi = min(c_lo + chunk, n);
     int32_t *X = a.xs0, *Y = a.ys0, *Xn = a.xs1, *Yn = a.ys1;
     for (int L = 0; L <= a.max_depth; ++L) {
         if (L >= a.l_end) return;  // deeper levels and the tail run per subtree
@@ -812,11 +815,11 @@ __device__ __forceinline__ void build_levels_body(const BuildArgs &a) {
             cnt += v;
         }
         cnt = BR(tmp.r).Sum(cnt);
-        if (tid == 0) a.blocksum[blockIdx.x] = cnt;
+        if (tid == 0) a.blocksum[bid] = cnt;
         grid.sync();
         // ---- phase 3: global exclusive prefix
         int base = 0;
-        for (int b = tid; b < (int)blockIdx.x; b += BUILD_THREADS) base += a.blocksum[b];
+        for (int b = tid; b < bid; b += BUILD_THREADS) base += a.blocksum[b];
         __syncthreads();
         base = BR(tmp.r).Sum(base);
         if (tid == 0) s_carry = base;
@@ -1639,7 +1642,7 @@ __global__ void incr_kernel(int32_t *ctr) {
 #define MDC_LAYOUT_SMALL_MAX 512  // one CTA only pays off for tiny meshes (n = 2000: 1.9 ms vs ~0.1 ms per step)
 #endif
 #ifndef MDC_SMALL_THREADS
-#define MDC_SMALL_THREADS 512
+#define MDC_SMALL_THREADS 256  // per CTA of the cluster (A/B at config 1: 128 29.5, 256 27.0, 512 28.2 us/step)
 #endif
 constexpr int SMALL_THREADS = MDC_SMALL_THREADS;
 #ifndef MDC_SMALL_LG
