@@ -1900,6 +1900,7 @@ struct MdcLayoutPlan {
     // profiling (mdc_layout_profile): events recorded between step phases
     bool cluster_ok = false;  // the device can co-schedule one BUILD_CLUSTER cluster
     int small_nE = 0, small_nI = 0;  // CSR neighbour / incidence counts (persistent small-mesh step)
+    bool small_ok = false;           // the device co-schedules the small step's cluster (else: multi-kernel step)
     int subtree_l0 = -1;      // grid walk: first level handed to build_subtree_kernel (-1: none)
     int subtree_nseg = 0;
     cudaEvent_t ev[8] = {};
@@ -2244,6 +2245,25 @@ extern "C" int mdc_layout_plan_create(const MdcLayoutArgs *a, MdcLayoutPlan **pl
         int nclusters = 0;
         p->cluster_ok = cudaOccupancyMaxActiveClusters(&nclusters, ck, &cfg) == cudaSuccess && nclusters >= 1;
         cudaGetLastError();  // a refused query leaves the cooperative path in charge
+        if (p->shape.n <= MDC_LAYOUT_SMALL_MAX) {
+            // the small step's cluster at its largest shared-memory carve (n = SMALL_MAX-sized bound)
+            cudaFuncSetAttribute(layout_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+            cudaLaunchConfig_t sc = {};
+            sc.gridDim = dim3(SMALL_CLUSTER);
+            sc.blockDim = dim3(SMALL_THREADS);
+            sc.dynamicSmemBytes = 160 * 1024;
+            cudaLaunchAttribute sat[1];
+            sat[0].id = cudaLaunchAttributeClusterDimension;
+            sat[0].val.clusterDim.x = SMALL_CLUSTER;
+            sat[0].val.clusterDim.y = 1;
+            sat[0].val.clusterDim.z = 1;
+            sc.attrs = sat;
+            sc.numAttrs = SMALL_CLUSTER > 1 ? 1 : 0;
+            int nsc = 0;
+            p->small_ok = SMALL_CLUSTER <= 1 ||
+                          (cudaOccupancyMaxActiveClusters(&nsc, layout_small_kernel, &sc) == cudaSuccess && nsc >= 1);
+            cudaGetLastError();
+        }
     }
     if (p->shape.n <= MDC_LAYOUT_SMALL_MAX) {  // staged topology sizes of the persistent small step
         cudaMemcpyAsync(&p->small_nE, a->csr_off + p->shape.n, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
@@ -2294,7 +2314,7 @@ extern "C" int mdc_layout_steps(MdcLayoutPlan *p, int32_t k, const double *temps
     double *bufs[2] = {p->a.pos, p->b.pos_b};
     bool dbg = p->a.dbg_bh || p->a.dbg_force || p->a.dbg_scale;
     const int64_t n = p->shape.n;
-    if (use_graph && !dbg && MDC_LOCAL_LG && n >= 2 && n <= MDC_LAYOUT_SMALL_MAX && n <= BUILD_SINGLE_MAX &&
+    if (use_graph && !dbg && MDC_LOCAL_LG && p->small_ok && n >= 2 && n <= MDC_LAYOUT_SMALL_MAX && n <= BUILD_SINGLE_MAX &&
         p->a.part_world <= 1) {
         // small mesh: every step of the call in one persistent CTA
         SmallArgs sa;
